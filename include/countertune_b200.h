@@ -1,0 +1,183 @@
+/*
+ * countertune_b200.h -- C ABI of the B200 searcher hot path.
+ *
+ * The reference (`countertune`, pure Python + numpy) has no native code and
+ * therefore no FFI of its own.  Each entry point below replaces one function
+ * of the reference's Python API on the searcher's data-parallel hot path; the
+ * replaced interface is cited as <file>:<line> relative to
+ * /root/reference/pkg/src/countertune/.  The Python mirror in
+ * paper_2102_05297_b200/ binds these through ctypes.
+ *
+ * Conventions
+ *   - plain C types only; host pointers are borrowed for the duration of the
+ *     call and never retained;
+ *   - every function returns CT_OK (0) or a negative CT_ERR_* status and
+ *     leaves a message in ct_last_error() (thread-local); no C++ exception
+ *     ever crosses the boundary;
+ *   - one ct_ctx per GPU; calls on one context are serialised by the caller;
+ *     different contexts may be driven from different host threads;
+ *   - all floating point is IEEE binary64, evaluated in the reference's
+ *     operation order (no FMA contraction on the parity path).
+ */
+#ifndef COUNTERTUNE_B200_H
+#define COUNTERTUNE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CT_ABI_VERSION 1
+
+/* status codes; the Python shim maps them onto the reference's exception
+ * classes (errors.py:4-43) */
+#define CT_OK                 0
+#define CT_ERR_CUDA          -1  /* CUDA runtime failure                  -> CounterTuneError      */
+#define CT_ERR_VALUE         -2  /* bad argument (search.py:353-356,177)  -> ValueError            */
+#define CT_ERR_EXHAUSTED     -3  /* empty pool (search.py:155,183)        -> SpaceExhaustedError   */
+#define CT_ERR_NO_RECORD     -4  /* replay miss (search.py:209)           -> CounterTuneError      */
+#define CT_ERR_MISMATCH      -5  /* table/space mismatch (search.py:69)   -> CounterTuneError      */
+#define CT_ERR_STATE         -6  /* call-order error (no table uploaded)  -> CounterTuneError      */
+#define CT_ERR_NONFINITE     -7  /* NaN weight reached selection          -> CounterTuneError      */
+#define CT_ERR_UNSUPPORTED   -8  /* feature outside the device path       -> CounterTuneError      */
+
+/* SearchTrace.status (search.py:33-35) */
+#define CT_STATUS_BUDGET      0
+#define CT_STATUS_STOPPED     1
+#define CT_STATUS_EXHAUSTED   2
+#define CT_STATUS_ERROR       3  /* see ct_rep_error codes below */
+
+/* number of counters analyze() reads, REQUIRED_COUNTERS order
+ * (bottlenecks.py:21-30) */
+#define CT_N_REQUIRED 23
+/* number of keys react() emits, insertion order (bottlenecks.py:216-229) */
+#define CT_N_DELTA 18
+
+typedef struct ct_ctx ct_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+int         ct_abi_version(void);
+const char* ct_last_error(void);
+int         ct_device_count(int* count);
+int         ct_create(int device, ct_ctx** out);
+int         ct_destroy(ct_ctx* ctx);
+/* launch on an external cudaStream_t (e.g. torch's current stream); NULL
+ * restores the context's own stream */
+int         ct_set_stream(ct_ctx* ctx, void* cuda_stream);
+int         ct_synchronize(ct_ctx* ctx);
+
+/* ---- resident inputs -------------------------------------------------- */
+
+/* PredictionTable.matrix (search.py:38-63): n_configs x n_counters float64,
+ * row-major as the reference stores it.  Stored on the device column-major
+ * (one contiguous float64 column per counter). */
+int ct_table_upload(ct_ctx* ctx, const double* matrix_rowmajor,
+                    int64_t n_configs, int32_t n_counters);
+
+/* Parameter assignments (space.py:67-104), n_configs x n_params row-major;
+ * only needed for score_top_k (search.py:133-140). */
+int ct_space_upload(ct_ctx* ctx, const double* assignments_rowmajor,
+                    int64_t n_configs, int32_t n_params);
+
+/* DatasetReplaySource (search.py:197-217) over Dataset.records
+ * (space.py:130-174): per configuration runtime_us, global_threads and the
+ * 23 REQUIRED_COUNTERS (row-major n x 23).  has_record[i] == 0 marks a
+ * configuration without a measurement (measuring it is an error).
+ * stop_mask (nullable) is the well-performing set (space.py:177-186). */
+int ct_replay_upload(ct_ctx* ctx, int64_t n_configs, const double* runtime_us,
+                     const int64_t* global_threads, const double* counters_rowmajor,
+                     const uint8_t* has_record, const uint8_t* stop_mask);
+
+/* ---- single-call hot-path functions ------------------------------------ */
+
+/* score_configurations (search.py:89-141).  delta_columns[k] is the table
+ * column of the k-th delta key in react() insertion order (-1: the table has
+ * no such counter), delta_values[k] its value.  explored: n bytes.
+ * score_top_k < 0 means None.  raw_out: n float64.  scoreable_out (n bytes,
+ * nullable) receives the top-K mask; *has_scoreable tells whether top-K was
+ * applied (ScoreVector.scoreable is None otherwise). */
+int ct_score(ct_ctx* ctx, int64_t profile_index, const int32_t* delta_columns,
+             const double* delta_values, int32_t n_delta, const uint8_t* explored,
+             int32_t literal_sign, int64_t score_top_k, double* raw_out,
+             uint8_t* scoreable_out, int32_t* has_scoreable);
+
+/* normalize_scores (search.py:144-172): pool = scoreable & ~explored.
+ * Weights use a correctly rounded x**8 (the reference's numpy pow is within
+ * 1 ulp of it); norm_out: n float64.  Returns CT_ERR_EXHAUSTED on an empty
+ * pool. */
+int ct_normalize(ct_ctx* ctx, const double* raw, const uint8_t* pool, int64_t n,
+                 double gamma, double* norm_out);
+
+/* weighted_select (search.py:175-185) with the uniform u = rng.random()
+ * already drawn by the caller.  The inverse-CDF index is found on an exact
+ * fixed-point prefix of the weights and certified against the rounding of
+ * the reference's sequential float cumsum; an uncertified draw is re-decided
+ * on the device with the sequential float64 cumsum.  *certified_out = 1 when
+ * the exact and sequential decisions provably agree. */
+int ct_select(ct_ctx* ctx, const double* norm, int64_t n, double u,
+              int64_t* chosen_out, int32_t* certified_out);
+
+/* ---- batched replay searches (harness.py:139-163) ---------------------- */
+
+typedef struct {
+    int32_t outer_iterations;      /* i  (search.py:338)                    */
+    int32_t inner_steps;           /* n  (search.py:338)                    */
+    double  inst_reaction;         /* bottlenecks.py:62-65                  */
+    double  issue_delta_sign;      /* bottlenecks.py:60                     */
+    double  gamma;                 /* search.py:30                          */
+    int32_t literal_sign;          /* search.py:126                         */
+    int64_t score_top_k;           /* < 0: None (search.py:133)             */
+    int32_t use_stop;              /* stop_indices is not None              */
+    int32_t generation;            /* 0 pre_volta, 1 volta_plus (counters.py:30-31) */
+    int64_t cores;                 /* ArchProfile.cores (counters.py:151)   */
+    int32_t delta_columns[CT_N_DELTA]; /* table column per react() key, -1 absent */
+} ct_search_params;
+
+/* numpy SeedSequence of repetition r (harness.py:135-136):
+ *   SeedSequence(entropy, spawn_key = spawn_prefix [+ (rep_offset + r,)]) */
+typedef struct {
+    const uint32_t* entropy;       /* entropy as little-endian uint32 words */
+    int32_t         n_entropy;
+    const uint32_t* spawn_prefix;  /* spawn key words                       */
+    int32_t         n_prefix;
+    int32_t         child_per_rep; /* 1: append (rep_offset + r) to the key */
+    int64_t         rep_offset;
+} ct_seed_spec;
+
+typedef struct {
+    int64_t configs_scored;        /* sum of pool sizes at scoring time     */
+    int64_t draws;                 /* weighted draws made                   */
+    int64_t uncertified;           /* draws re-decided by sequential cumsum */
+    int64_t outer_iterations;      /* outer iterations executed             */
+} ct_batch_stats;
+
+/* run_profile_search (search.py:338-399) for n_reps repetitions on the
+ * resident table + replay data.  Launches asynchronously; results stay on
+ * the device until ct_profile_results(). */
+int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* params,
+                             const ct_seed_spec* seeds, int32_t n_reps);
+
+/* run_random_search (search.py:317-335); max_steps < 0 means None. */
+int ct_random_search_launch(ct_ctx* ctx, const ct_seed_spec* seeds, int32_t n_reps,
+                            int64_t max_steps, int32_t use_stop);
+
+/* Trajectories of the last launch.  step_index / step_profiled are
+ * n_reps x max_steps (row-major, max_steps = ct_result_max_steps()),
+ * n_steps / status / rep_error are n_reps each (rep_error: CT_ERR_* of a
+ * repetition that stopped with CT_STATUS_ERROR, else 0).  Any pointer may
+ * be NULL.  Synchronises. */
+int ct_result_max_steps(ct_ctx* ctx, int64_t* max_steps);
+int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled,
+                     int32_t* n_steps, int32_t* status, int32_t* rep_error,
+                     ct_batch_stats* stats);
+
+/* Device pointers of the last launch's result buffers (for zero-copy
+ * consumers such as torch); valid until the next launch. */
+int ct_result_device_ptrs(ct_ctx* ctx, void** step_index, void** step_profiled,
+                          void** n_steps, void** status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COUNTERTUNE_B200_H */

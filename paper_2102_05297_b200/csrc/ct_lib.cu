@@ -1,0 +1,705 @@
+// ct_lib.cu -- C ABI (include/countertune_b200.h) over the sm_100a kernels.
+//
+// Owns the device copies of the searcher's inputs (prediction table, replay
+// data, space assignments), the result buffers of batched searches and the
+// single-call kernels behind score_configurations / normalize_scores /
+// weighted_select.  No C++ exception crosses the ABI; errors are negative
+// status codes with a thread-local message.
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "countertune_b200.h"
+#include "ct_search.cuh"
+
+using namespace ct;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CT_CUDA(call)                                                              \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess)                                                     \
+            return fail(CT_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+    cudaError_t ensure(size_t n) {
+        if (n <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr; cap = 0;
+        size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = std::max<size_t>(n, 1);
+        return e;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+}  // namespace
+
+struct ct_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    // prediction table (column-major)
+    DevBuf<double> table;
+    int64_t n = 0;
+    int32_t n_counters = 0;
+    // space assignments (row-major n x P)
+    DevBuf<double> assign;
+    int32_t n_params = 0;
+    int64_t assign_n = 0;
+    // replay data
+    DevBuf<double> runtime;
+    DevBuf<int64_t> threads;
+    DevBuf<double> counters;
+    DevBuf<uint8_t> has_record;
+    DevBuf<uint32_t> stop_bits;
+    int64_t replay_n = 0;
+    bool has_stop = false;
+    // results of the last batched launch
+    DevBuf<int32_t> step_index;
+    DevBuf<uint8_t> step_profiled;
+    DevBuf<int32_t> n_steps, status, rep_error;
+    DevBuf<unsigned long long> stats;
+    int64_t res_reps = 0, res_max_steps = 0;
+    bool res_valid = false;
+    // scratch
+    DevBuf<double> scratch_w;
+    DevBuf<uint32_t> scratch_e;
+    DevBuf<int32_t> scratch_perm;
+    DevBuf<uint32_t> seed_words;
+    // single-call buffers
+    DevBuf<double> vec_a, vec_b;
+    DevBuf<uint8_t> mask_a, mask_b;
+    DevBuf<unsigned long long> key_a, key_b;
+    DevBuf<int32_t> val_a, val_b;
+    DevBuf<unsigned char> cub_tmp;
+    DevBuf<double> part_d;
+    DevBuf<int32_t> part_i;
+    DevBuf<u128> tiles;
+    DevBuf<long long> pick;
+};
+
+// ===========================================================================
+// single-call kernels
+// ===========================================================================
+namespace {
+
+struct ScoreSingleArgs {
+    const double* table; int64_t ld; int64_t n;
+    int64_t profile;
+    int32_t n_delta;
+    int32_t cols[CT_N_DELTA];
+    double vals[CT_N_DELTA];
+    const uint8_t* explored;
+    const uint8_t* scoreable;  // nullable
+    int32_t literal_sign;
+    double* raw;
+};
+
+__global__ void k_score_single(const ScoreSingleArgs a) {
+    __shared__ ActiveTerm act[CT_N_DELTA];
+    __shared__ int n_act;
+    if (threadIdx.x == 0) {
+        int na = 0;
+        for (int k = 0; k < a.n_delta; ++k) {
+            if (a.vals[k] == 0.0 || a.cols[k] < 0) continue;
+            double pv = a.table[(size_t)a.cols[k] * a.ld + a.profile];
+            if (pv == 0.0) continue;
+            act[na].col = a.cols[k]; act[na].d = a.vals[k]; act[na].p = pv; ++na;
+        }
+        n_act = na;
+    }
+    __syncthreads();
+    const bool lit = a.literal_sign != 0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double raw = 0.0;
+        if (!a.explored[e] && (!a.scoreable || a.scoreable[e])) {
+            for (int k = 0; k < n_act; ++k)
+                raw = add(raw, raw_term(__ldg(a.table + (size_t)act[k].col * a.ld + e), act[k], lit));
+        }
+        a.raw[e] = raw;
+    }
+}
+
+// Euclidean parameter distance to the profile (search.py:134-136) as an
+// order-preserving key; explored -> +inf.  numpy evaluates
+// sqrt(add.reduce(d*d, axis=1)) with its pairwise summation over the row
+// (DOUBLE_pairwise_sum: sequential below 8 terms, else 8 accumulators);
+// rows here are at most 64 terms, below the 128-term recursion block.
+__device__ __forceinline__ double np_row_sum(const double* a, int n) {
+    if (n < 8) {
+        double r = -0.0;
+        for (int i = 0; i < n; ++i) r = add(r, a[i]);
+        return r;
+    }
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; ++j) r[j] = add(r[j], a[i + j]);
+    double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+    for (; i < n; ++i) res = add(res, a[i]);
+    return res;
+}
+
+__global__ void k_topk_keys(const double* assign, int32_t P, int64_t n, int64_t profile,
+                            const uint8_t* explored, unsigned long long* keys, int32_t* vals) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double sq[64];
+        int k = P < 64 ? P : 64;
+        for (int j = 0; j < k; ++j) {
+            double d = sub(assign[(size_t)e * P + j], assign[(size_t)profile * P + j]);
+            sq[j] = mul(d, d);
+        }
+        double dist = dsqrt(np_row_sum(sq, k));
+        if (explored[e]) dist = INFINITY;
+        keys[e] = (unsigned long long)dbits(dist);   // dist >= 0: bit order == value order
+        vals[e] = (int32_t)e;
+    }
+}
+
+__global__ void k_topk_mark(const int32_t* sorted_vals, int64_t k, uint8_t* scoreable, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x)
+        scoreable[sorted_vals[i]] = 1;
+}
+
+// normalize_scores: pool extrema (per-block partials)
+__global__ void k_minmax(const double* raw, const uint8_t* pool, int64_t n,
+                         double* pmax, double* pmin, int32_t* pcount) {
+    double mx = -INFINITY, mn = INFINITY;
+    int cnt = 0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (pool[e]) { mx = nmax(mx, raw[e]); mn = nmin(mn, raw[e]); ++cnt; }
+    }
+    __shared__ double smx[32], smn[32];
+    __shared__ int scn[32];
+    mx = warp_max(mx); mn = warp_min(mn); cnt = warp_sum_i(cnt);
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { smx[warp] = mx; smn[warp] = mn; scn[warp] = cnt; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            mx = nmax(mx, smx[i]); mn = nmin(mn, smn[i]); cnt += scn[i];
+        }
+        pmax[blockIdx.x] = mx; pmin[blockIdx.x] = mn; pcount[blockIdx.x] = cnt;
+    }
+}
+
+__global__ void k_weights(const double* raw, const uint8_t* pool, int64_t n, const double* pmax,
+                          const double* pmin, int nparts, double gamma, double* norm) {
+    __shared__ double smax, smin;
+    if (threadIdx.x == 0) {
+        double mx = pmax[0], mn = pmin[0];
+        for (int i = 1; i < nparts; ++i) { mx = nmax(mx, pmax[i]); mn = nmin(mn, pmin[i]); }
+        smax = mx; smin = mn;
+    }
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x)
+        norm[e] = pool[e] ? weight(raw[e], smax, smin, gamma) : 0.0;
+}
+
+// weighted_select: exact tile totals, then one warp locates + certifies.
+__global__ void k_tile_totals(const double* w, int64_t n, int rows, int ntiles, u128* tiles,
+                              int32_t* bad) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int64_t tile_len = 32LL * rows;
+    for (int t = gw; t < ntiles; t += nw) {
+        u128 s = 0;
+        int b = 0;
+        for (int j = 0; j < rows; ++j) {
+            int64_t e = (int64_t)t * tile_len + 32LL * j + lane;
+            if (e < n) { u128 f; if (to_fx(w[e], &f)) s += f; else b = 1; }
+        }
+        s = warp_sum(s);
+        b = __any_sync(FULL, b);
+        if (lane == 0) { tiles[t] = s; if (b) atomicExch(bad, 1); }
+    }
+}
+
+__global__ void k_select_single(const double* w, int64_t n, int rows, int ntiles,
+                                const u128* tiles, const int32_t* bad, double u, long long* out) {
+    const int lane = threadIdx.x;
+    if (*bad) {
+        if (lane == 0) { out[0] = sequential_select(w, n, u); out[1] = 0; out[2] = 1; }
+        return;
+    }
+    u128 total = 0;
+    for (int t = lane; t < ntiles; t += 32) total += tiles[t];
+    total = warp_sum(total);
+    if (total == 0) { if (lane == 0) { out[0] = -1; out[1] = 0; out[2] = 0; } return; }
+    double total_d = fx_to_double(total);
+    double r = mul(u, total_d);
+    u128 r_fx = floor_fx(r);
+    Located pk = warp_locate(tiles, ntiles, w, n, rows, r_fx, lane);
+    bool ok = certify(pk, r_fx, total_d, n);
+    if (lane == 0) {
+        out[0] = ok ? pk.idx : sequential_select(w, n, u);
+        out[1] = ok ? 1 : 0;
+        out[2] = 0;
+    }
+}
+
+int rows_for(int64_t n) {
+    int rows = (int)std::lround(std::sqrt((double)n) / 32.0);
+    return std::max(1, rows);
+}
+
+int grid_for(int64_t n, int threads) {
+    int64_t g = (n + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+int check_ctx(ct_ctx* ctx) {
+    if (!ctx) return fail(CT_ERR_VALUE, "null context");
+    CT_CUDA(cudaSetDevice(ctx->device));
+    return CT_OK;
+}
+
+int upload_seeds(ct_ctx* ctx, const ct_seed_spec* seeds, const uint32_t** ent,
+                        const uint32_t** pre) {
+    if (!seeds) return fail(CT_ERR_VALUE, "null seed spec");
+    if (seeds->n_entropy < 0 || seeds->n_prefix < 0 || (seeds->n_entropy && !seeds->entropy) ||
+        (seeds->n_prefix && !seeds->spawn_prefix))
+        return fail(CT_ERR_VALUE, "bad seed spec");
+    size_t words = (size_t)seeds->n_entropy + seeds->n_prefix;
+    CT_CUDA(ctx->seed_words.ensure(words + 1));
+    std::vector<uint32_t> host(words + 1, 0u);
+    for (int i = 0; i < seeds->n_entropy; ++i) host[i] = seeds->entropy[i];
+    for (int i = 0; i < seeds->n_prefix; ++i) host[seeds->n_entropy + i] = seeds->spawn_prefix[i];
+    CT_CUDA(cudaMemcpyAsync(ctx->seed_words.p, host.data(), sizeof(uint32_t) * (words + 1),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    *ent = ctx->seed_words.p;
+    *pre = ctx->seed_words.p + seeds->n_entropy;
+    // host vector must outlive the async copy
+    CT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return CT_OK;
+}
+
+int ensure_results(ct_ctx* ctx, int64_t reps, int64_t max_steps) {
+    CT_CUDA(ctx->step_index.ensure((size_t)reps * max_steps));
+    CT_CUDA(ctx->step_profiled.ensure((size_t)reps * max_steps));
+    CT_CUDA(ctx->n_steps.ensure(reps));
+    CT_CUDA(ctx->status.ensure(reps));
+    CT_CUDA(ctx->rep_error.ensure(reps));
+    CT_CUDA(cudaMemsetAsync(ctx->stats.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    ctx->res_reps = reps;
+    ctx->res_max_steps = max_steps;
+    ctx->res_valid = true;
+    return CT_OK;
+}
+
+template <int NT>
+int launch_profile(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
+    auto kern = k_profile_search<NT>;
+    if (smem > 48 * 1024)
+        CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
+    if (occ < 1) return fail(CT_ERR_CUDA, "search kernel does not fit on an SM");
+    int grid = std::min(n_reps, occ * ctx->sm_count);
+    if (!a.w_in_smem) {
+        CT_CUDA(ctx->scratch_w.ensure((size_t)grid * a.n));
+        a.scratch_w = ctx->scratch_w.p;
+    }
+    if (!a.e_in_smem) {
+        CT_CUDA(ctx->scratch_e.ensure((size_t)grid * a.nwords));
+        a.scratch_e = ctx->scratch_e.p;
+    }
+    kern<<<grid, NT, smem, ctx->stream>>>(a);
+    CT_CUDA(cudaGetLastError());
+    return CT_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int ct_abi_version(void) { return CT_ABI_VERSION; }
+
+const char* ct_last_error(void) { return g_err.c_str(); }
+
+int ct_device_count(int* count) {
+    if (!count) return fail(CT_ERR_VALUE, "null count");
+    CT_CUDA(cudaGetDeviceCount(count));
+    return CT_OK;
+}
+
+int ct_create(int device, ct_ctx** out) {
+    if (!out) return fail(CT_ERR_VALUE, "null output");
+    *out = nullptr;
+    CT_CUDA(cudaSetDevice(device));
+    ct_ctx* c = new ct_ctx();
+    c->device = device;
+    cudaError_t e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete c; return fail(CT_ERR_CUDA, cudaGetErrorString(e)); }
+    c->stream = c->own;
+    e = c->stats.ensure(4);
+    if (e != cudaSuccess) { delete c; return fail(CT_ERR_CUDA, cudaGetErrorString(e)); }
+    *out = c;
+    return CT_OK;
+}
+
+int ct_destroy(ct_ctx* ctx) {
+    if (!ctx) return CT_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->table.release(); ctx->assign.release(); ctx->runtime.release();
+    ctx->threads.release(); ctx->counters.release(); ctx->has_record.release();
+    ctx->stop_bits.release(); ctx->step_index.release(); ctx->step_profiled.release();
+    ctx->n_steps.release(); ctx->status.release(); ctx->rep_error.release();
+    ctx->stats.release(); ctx->scratch_w.release(); ctx->scratch_e.release();
+    ctx->scratch_perm.release(); ctx->seed_words.release(); ctx->vec_a.release();
+    ctx->vec_b.release(); ctx->mask_a.release(); ctx->mask_b.release(); ctx->key_a.release();
+    ctx->key_b.release(); ctx->val_a.release(); ctx->val_b.release(); ctx->cub_tmp.release();
+    ctx->part_d.release(); ctx->part_i.release(); ctx->tiles.release(); ctx->pick.release();
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+    return CT_OK;
+}
+
+int ct_set_stream(ct_ctx* ctx, void* cuda_stream) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    CT_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own;
+    return CT_OK;
+}
+
+int ct_synchronize(ct_ctx* ctx) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    CT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return CT_OK;
+}
+
+int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!matrix || n < 1 || c < 1) return fail(CT_ERR_VALUE, "table needs n >= 1 and counters >= 1");
+    if (n > INT32_MAX) return fail(CT_ERR_VALUE, "spaces above 2^31-1 configurations are not supported");
+    // transpose to column-major on the host (one pass over the borrowed matrix)
+    std::vector<double> colmajor((size_t)n * c);
+    for (int64_t i = 0; i < n; ++i)
+        for (int32_t j = 0; j < c; ++j) colmajor[(size_t)j * n + i] = matrix[(size_t)i * c + j];
+    CT_CUDA(ctx->table.ensure((size_t)n * c));
+    CT_CUDA(cudaMemcpyAsync(ctx->table.p, colmajor.data(), sizeof(double) * n * c,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    CT_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->n = n;
+    ctx->n_counters = c;
+    return CT_OK;
+}
+
+int ct_space_upload(ct_ctx* ctx, const double* assign, int64_t n, int32_t p) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!assign || n < 1 || p < 1) return fail(CT_ERR_VALUE, "space needs n >= 1 and params >= 1");
+    if (p > 64) return fail(CT_ERR_UNSUPPORTED, "top-K distance supports at most 64 parameters");
+    CT_CUDA(ctx->assign.ensure((size_t)n * p));
+    CT_CUDA(cudaMemcpyAsync(ctx->assign.p, assign, sizeof(double) * n * p,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    CT_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->assign_n = n;
+    ctx->n_params = p;
+    return CT_OK;
+}
+
+int ct_replay_upload(ct_ctx* ctx, int64_t n, const double* runtime, const int64_t* threads,
+                     const double* counters, const uint8_t* has_record, const uint8_t* stop_mask) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (n < 1 || !runtime || !threads || !counters || !has_record)
+        return fail(CT_ERR_VALUE, "replay upload needs runtime, threads, counters and has_record");
+    CT_CUDA(ctx->runtime.ensure(n));
+    CT_CUDA(ctx->threads.ensure(n));
+    CT_CUDA(ctx->counters.ensure((size_t)n * CT_N_REQUIRED));
+    CT_CUDA(ctx->has_record.ensure(n));
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(cudaMemcpyAsync(ctx->runtime.p, runtime, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    CT_CUDA(cudaMemcpyAsync(ctx->threads.p, threads, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    CT_CUDA(cudaMemcpyAsync(ctx->counters.p, counters, sizeof(double) * n * CT_N_REQUIRED,
+                            cudaMemcpyHostToDevice, s));
+    CT_CUDA(cudaMemcpyAsync(ctx->has_record.p, has_record, n, cudaMemcpyHostToDevice, s));
+    ctx->has_stop = stop_mask != nullptr;
+    if (stop_mask) {
+        size_t words = (size_t)((n + 31) / 32);
+        std::vector<uint32_t> bits(words, 0u);
+        for (int64_t i = 0; i < n; ++i)
+            if (stop_mask[i]) bits[i >> 5] |= 1u << (i & 31);
+        CT_CUDA(ctx->stop_bits.ensure(words));
+        CT_CUDA(cudaMemcpyAsync(ctx->stop_bits.p, bits.data(), words * 4, cudaMemcpyHostToDevice, s));
+        CT_CUDA(cudaStreamSynchronize(s));
+    }
+    CT_CUDA(cudaStreamSynchronize(s));
+    ctx->replay_n = n;
+    return CT_OK;
+}
+
+int ct_score(ct_ctx* ctx, int64_t profile, const int32_t* cols, const double* vals, int32_t n_delta,
+             const uint8_t* explored, int32_t literal_sign, int64_t top_k, double* raw_out,
+             uint8_t* scoreable_out, int32_t* has_scoreable) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!ctx->table.p) return fail(CT_ERR_STATE, "no prediction table uploaded");
+    if (n_delta < 0 || n_delta > CT_N_DELTA || (n_delta && (!cols || !vals)))
+        return fail(CT_ERR_VALUE, "delta must hold at most 18 keys");
+    if (!explored || !raw_out) return fail(CT_ERR_VALUE, "null explored/raw buffer");
+    const int64_t n = ctx->n;
+    if (profile < 0 || profile >= n) return fail(CT_ERR_VALUE, "profile index out of range");
+    for (int k = 0; k < n_delta; ++k)
+        if (cols[k] >= ctx->n_counters) return fail(CT_ERR_VALUE, "delta column out of range");
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(ctx->mask_a.ensure(n));
+    CT_CUDA(ctx->vec_a.ensure(n));
+    CT_CUDA(cudaMemcpyAsync(ctx->mask_a.p, explored, n, cudaMemcpyHostToDevice, s));
+    int64_t pool = 0;
+    for (int64_t i = 0; i < n; ++i) pool += explored[i] ? 0 : 1;
+    bool topk = top_k >= 0 && top_k < pool;
+    if (has_scoreable) *has_scoreable = topk ? 1 : 0;
+    if (topk) {
+        if (!ctx->assign.p || ctx->assign_n != n)
+            return fail(CT_ERR_STATE, "score_top_k needs the space assignments (ct_space_upload)");
+        CT_CUDA(ctx->key_a.ensure(n)); CT_CUDA(ctx->key_b.ensure(n));
+        CT_CUDA(ctx->val_a.ensure(n)); CT_CUDA(ctx->val_b.ensure(n));
+        CT_CUDA(ctx->mask_b.ensure(n));
+        k_topk_keys<<<grid_for(n, 256), 256, 0, s>>>(ctx->assign.p, ctx->n_params, n, profile,
+                                                      ctx->mask_a.p, ctx->key_a.p, ctx->val_a.p);
+        size_t tmp = 0;
+        CT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ctx->key_a.p, ctx->key_b.p,
+                                                ctx->val_a.p, ctx->val_b.p, (int)n, 0, 64, s));
+        CT_CUDA(ctx->cub_tmp.ensure(tmp));
+        CT_CUDA(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tmp, ctx->key_a.p, ctx->key_b.p,
+                                                ctx->val_a.p, ctx->val_b.p, (int)n, 0, 64, s));
+        CT_CUDA(cudaMemsetAsync(ctx->mask_b.p, 0, n, s));
+        if (top_k > 0)
+            k_topk_mark<<<grid_for(top_k, 256), 256, 0, s>>>(ctx->val_b.p, top_k, ctx->mask_b.p, n);
+    }
+    ScoreSingleArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.table = ctx->table.p; a.ld = n; a.n = n; a.profile = profile; a.n_delta = n_delta;
+    for (int k = 0; k < n_delta; ++k) { a.cols[k] = cols[k]; a.vals[k] = vals[k]; }
+    a.explored = ctx->mask_a.p; a.scoreable = topk ? ctx->mask_b.p : nullptr;
+    a.literal_sign = literal_sign; a.raw = ctx->vec_a.p;
+    k_score_single<<<grid_for(n, 256), 256, 0, s>>>(a);
+    CT_CUDA(cudaGetLastError());
+    CT_CUDA(cudaMemcpyAsync(raw_out, ctx->vec_a.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    if (topk && scoreable_out)
+        CT_CUDA(cudaMemcpyAsync(scoreable_out, ctx->mask_b.p, n, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
+    return CT_OK;
+}
+
+int ct_normalize(ct_ctx* ctx, const double* raw, const uint8_t* pool, int64_t n, double gamma,
+                 double* norm_out) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!raw || !pool || !norm_out || n < 0) return fail(CT_ERR_VALUE, "null buffers");
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; ++i) cnt += pool[i] ? 1 : 0;
+    if (cnt == 0) return fail(CT_ERR_EXHAUSTED, "no unexplored configurations to normalize");
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(ctx->vec_a.ensure(n)); CT_CUDA(ctx->vec_b.ensure(n)); CT_CUDA(ctx->mask_a.ensure(n));
+    int g = std::min(grid_for(n, 256), 512);
+    CT_CUDA(ctx->part_d.ensure(2 * (size_t)g)); CT_CUDA(ctx->part_i.ensure(g));
+    CT_CUDA(cudaMemcpyAsync(ctx->vec_a.p, raw, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    CT_CUDA(cudaMemcpyAsync(ctx->mask_a.p, pool, n, cudaMemcpyHostToDevice, s));
+    k_minmax<<<g, 256, 0, s>>>(ctx->vec_a.p, ctx->mask_a.p, n, ctx->part_d.p, ctx->part_d.p + g,
+                               ctx->part_i.p);
+    k_weights<<<grid_for(n, 256), 256, 0, s>>>(ctx->vec_a.p, ctx->mask_a.p, n, ctx->part_d.p,
+                                               ctx->part_d.p + g, g, gamma, ctx->vec_b.p);
+    CT_CUDA(cudaGetLastError());
+    CT_CUDA(cudaMemcpyAsync(norm_out, ctx->vec_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
+    return CT_OK;
+}
+
+int ct_select(ct_ctx* ctx, const double* norm, int64_t n, double u, int64_t* chosen,
+              int32_t* certified) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!norm || !chosen || n < 1) return fail(CT_ERR_EXHAUSTED, "every configuration is explored");
+    cudaStream_t s = ctx->stream;
+    int rows = rows_for(n);
+    int ntiles = (int)((n + 32LL * rows - 1) / (32LL * rows));
+    CT_CUDA(ctx->vec_a.ensure(n)); CT_CUDA(ctx->tiles.ensure(ntiles));
+    CT_CUDA(ctx->part_i.ensure(1)); CT_CUDA(ctx->pick.ensure(3));
+    CT_CUDA(cudaMemcpyAsync(ctx->vec_a.p, norm, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    CT_CUDA(cudaMemsetAsync(ctx->part_i.p, 0, sizeof(int32_t), s));
+    int blocks = std::max(1, std::min((ntiles + 7) / 8, 1024));
+    k_tile_totals<<<blocks, 256, 0, s>>>(ctx->vec_a.p, n, rows, ntiles, ctx->tiles.p, ctx->part_i.p);
+    k_select_single<<<1, 32, 0, s>>>(ctx->vec_a.p, n, rows, ntiles, ctx->tiles.p, ctx->part_i.p, u,
+                                     ctx->pick.p);
+    CT_CUDA(cudaGetLastError());
+    long long out[3];
+    CT_CUDA(cudaMemcpyAsync(out, ctx->pick.p, sizeof(out), cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
+    if (out[0] < 0) return fail(CT_ERR_EXHAUSTED, "every configuration is explored");
+    *chosen = out[0];
+    if (certified) *certified = (int32_t)out[1];
+    return CT_OK;
+}
+
+// ------------------------------------------------------------ batched searches
+
+int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_seed_spec* seeds,
+                             int32_t n_reps) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!prm) return fail(CT_ERR_VALUE, "null params");
+    if (!ctx->table.p) return fail(CT_ERR_STATE, "no prediction table uploaded");
+    if (!ctx->runtime.p || ctx->replay_n != ctx->n)
+        return fail(CT_ERR_MISMATCH, "prediction table was built for a different space");
+    if (prm->outer_iterations < 1)
+        return fail(CT_ERR_VALUE, "need at least one outer iteration, got i=" +
+                                      std::to_string(prm->outer_iterations));
+    if (prm->inner_steps < 0)
+        return fail(CT_ERR_VALUE, "inner step count must be >= 0, got n=" +
+                                      std::to_string(prm->inner_steps));
+    if (!(prm->inst_reaction > 0.0 && prm->inst_reaction < 1.0))
+        return fail(CT_ERR_VALUE, "inst_reaction must lie in (0, 1)");
+    if (prm->score_top_k >= 0)
+        return fail(CT_ERR_UNSUPPORTED, "score_top_k is not yet supported by the batched kernel");
+    if (prm->use_stop && !ctx->has_stop) return fail(CT_ERR_STATE, "no stop mask uploaded");
+    if (n_reps < 0) return fail(CT_ERR_VALUE, "n_reps must be >= 0");
+    for (int k = 0; k < CT_N_DELTA; ++k)
+        if (prm->delta_columns[k] >= ctx->n_counters) return fail(CT_ERR_VALUE, "delta column out of range");
+    const uint32_t *ent = nullptr, *pre = nullptr;
+    rc = upload_seeds(ctx, seeds, &ent, &pre); if (rc) return rc;
+    const int64_t n = ctx->n;
+    const int64_t max_steps = (int64_t)prm->outer_iterations * (prm->inner_steps + 1);
+    rc = ensure_results(ctx, std::max(n_reps, 1), max_steps); if (rc) return rc;
+    ctx->res_reps = n_reps;
+    if (n_reps == 0) return CT_OK;
+
+    SearchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.table = ctx->table.p; a.ld = n; a.n = n;
+    a.runtime = ctx->runtime.p; a.threads = ctx->threads.p; a.counters = ctx->counters.p;
+    a.has_record = ctx->has_record.p; a.stop_bits = prm->use_stop ? ctx->stop_bits.p : nullptr;
+    a.outer = prm->outer_iterations; a.inner = prm->inner_steps;
+    a.inst_reaction = prm->inst_reaction; a.issue_sign = prm->issue_delta_sign; a.gamma = prm->gamma;
+    a.literal_sign = prm->literal_sign; a.generation = prm->generation; a.cores = prm->cores;
+    for (int k = 0; k < CT_N_DELTA; ++k) a.delta_col[k] = prm->delta_columns[k];
+    a.entropy = ent; a.n_entropy = seeds->n_entropy; a.prefix = pre; a.n_prefix = seeds->n_prefix;
+    a.child_per_rep = seeds->child_per_rep; a.rep_offset = seeds->rep_offset; a.n_reps = n_reps;
+    a.rows = rows_for(n);
+    a.ntiles = (int)((n + 32LL * a.rows - 1) / (32LL * a.rows));
+    a.nwords = (n + 31) / 32;
+    a.step_index = ctx->step_index.p; a.step_profiled = ctx->step_profiled.p;
+    a.max_steps = max_steps; a.n_steps = ctx->n_steps.p; a.status = ctx->status.p;
+    a.rep_error = ctx->rep_error.p; a.stats = ctx->stats.p;
+
+    const size_t budget = 200 * 1024;
+    size_t tiles_b = 16 * (size_t)a.ntiles, w_b = 8 * (size_t)n, e_b = 4 * (size_t)a.nwords;
+    a.w_in_smem = (tiles_b + w_b + e_b <= budget) ? 1 : 0;
+    a.e_in_smem = (tiles_b + (a.w_in_smem ? w_b : 0) + e_b <= budget) ? 1 : 0;
+    size_t smem = tiles_b + (a.w_in_smem ? w_b : 0) + (a.e_in_smem ? e_b : 0);
+    if (tiles_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the tile index");
+    if (n <= 4096) return launch_profile<128>(ctx, a, smem, n_reps);
+    if (n <= 65536) return launch_profile<256>(ctx, a, smem, n_reps);
+    return launch_profile<512>(ctx, a, smem, n_reps);
+}
+
+int ct_random_search_launch(ct_ctx* ctx, const ct_seed_spec* seeds, int32_t n_reps,
+                            int64_t max_steps_req, int32_t use_stop) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!ctx->runtime.p) return fail(CT_ERR_STATE, "no replay data uploaded");
+    if (use_stop && !ctx->has_stop) return fail(CT_ERR_STATE, "no stop mask uploaded");
+    if (n_reps < 0) return fail(CT_ERR_VALUE, "n_reps must be >= 0");
+    const uint32_t *ent = nullptr, *pre = nullptr;
+    rc = upload_seeds(ctx, seeds, &ent, &pre); if (rc) return rc;
+    const int64_t n = ctx->replay_n;
+    int64_t max_steps = n;
+    if (max_steps_req >= 0 && max_steps_req < n) max_steps = max_steps_req;
+    rc = ensure_results(ctx, std::max(n_reps, 1), std::max<int64_t>(max_steps, 1)); if (rc) return rc;
+    ctx->res_reps = n_reps;
+    if (n_reps == 0) return CT_OK;
+    const int threads = 64;
+    int slots = std::min<int64_t>(n_reps, std::max<int64_t>(ctx->sm_count * 2 * threads,
+                                                            threads));
+    int blocks = (slots + threads - 1) / threads;
+    slots = blocks * threads;
+    CT_CUDA(ctx->scratch_perm.ensure((size_t)slots * n));
+    RandomArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.n = n; a.has_record = ctx->has_record.p; a.stop_bits = use_stop ? ctx->stop_bits.p : nullptr;
+    a.max_steps_req = max_steps_req;
+    a.entropy = ent; a.n_entropy = seeds->n_entropy; a.prefix = pre; a.n_prefix = seeds->n_prefix;
+    a.child_per_rep = seeds->child_per_rep; a.rep_offset = seeds->rep_offset; a.n_reps = n_reps;
+    a.perm_scratch = ctx->scratch_perm.p; a.n_slots = slots;
+    a.step_index = ctx->step_index.p; a.step_profiled = ctx->step_profiled.p;
+    a.max_steps = ctx->res_max_steps; a.n_steps = ctx->n_steps.p; a.status = ctx->status.p;
+    a.rep_error = ctx->rep_error.p;
+    k_random_search<<<blocks, threads, 0, ctx->stream>>>(a);
+    CT_CUDA(cudaGetLastError());
+    return CT_OK;
+}
+
+int ct_result_max_steps(ct_ctx* ctx, int64_t* max_steps) {
+    if (!ctx || !max_steps) return fail(CT_ERR_VALUE, "null argument");
+    if (!ctx->res_valid) return fail(CT_ERR_STATE, "no batched search launched");
+    *max_steps = ctx->res_max_steps;
+    return CT_OK;
+}
+
+int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled, int32_t* n_steps,
+                     int32_t* status, int32_t* rep_error, ct_batch_stats* stats) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!ctx->res_valid) return fail(CT_ERR_STATE, "no batched search launched");
+    cudaStream_t s = ctx->stream;
+    size_t r = (size_t)ctx->res_reps, m = (size_t)ctx->res_max_steps;
+    if (r) {
+        if (step_index)
+            CT_CUDA(cudaMemcpyAsync(step_index, ctx->step_index.p, 4 * r * m, cudaMemcpyDeviceToHost, s));
+        if (step_profiled)
+            CT_CUDA(cudaMemcpyAsync(step_profiled, ctx->step_profiled.p, r * m, cudaMemcpyDeviceToHost, s));
+        if (n_steps) CT_CUDA(cudaMemcpyAsync(n_steps, ctx->n_steps.p, 4 * r, cudaMemcpyDeviceToHost, s));
+        if (status) CT_CUDA(cudaMemcpyAsync(status, ctx->status.p, 4 * r, cudaMemcpyDeviceToHost, s));
+        if (rep_error) CT_CUDA(cudaMemcpyAsync(rep_error, ctx->rep_error.p, 4 * r, cudaMemcpyDeviceToHost, s));
+    }
+    unsigned long long st[4] = {0, 0, 0, 0};
+    CT_CUDA(cudaMemcpyAsync(st, ctx->stats.p, sizeof(st), cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+        stats->configs_scored = (int64_t)st[0];
+        stats->draws = (int64_t)st[1];
+        stats->uncertified = (int64_t)st[2];
+        stats->outer_iterations = (int64_t)st[3];
+    }
+    return CT_OK;
+}
+
+int ct_result_device_ptrs(ct_ctx* ctx, void** step_index, void** step_profiled, void** n_steps,
+                          void** status) {
+    if (!ctx) return fail(CT_ERR_VALUE, "null context");
+    if (!ctx->res_valid) return fail(CT_ERR_STATE, "no batched search launched");
+    if (step_index) *step_index = ctx->step_index.p;
+    if (step_profiled) *step_profiled = ctx->step_profiled.p;
+    if (n_steps) *n_steps = ctx->n_steps.p;
+    if (status) *status = ctx->status.p;
+    return CT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,355 @@
+// ct_search.cuh -- the batched replay search kernel (Alg. 1 over R repetitions).
+//
+// One CTA runs one repetition of run_profile_search (search.py:338-399) end to
+// end and then takes the next repetition (persistent grid sized to the
+// resident-CTA capacity).  Per outer iteration, inside the CTA:
+//
+//   thread 0   record the profiled step, replay its counters, analyze() +
+//              react() (Eqs. 6-15), build the active-term list        [serial]
+//   all warps  Eq. 16 raw score of every unexplored configuration,
+//              coalesced column reads of the column-major table, pool
+//              max/min                                                 [parallel]
+//   all warps  Eq. 17 weights + exact 2^-66 fixed-point tile totals    [parallel]
+//   warp 0     n certified inverse-CDF draws with progressive zeroing,
+//              replay lookups, stop test, argmin with later ties      [serial]
+//
+// Weights live in shared memory when the space fits (N <~ 20k), otherwise in
+// a per-CTA-slot global scratch slice.  The numpy Generator stream of the
+// repetition is regenerated on the device (ct_rng.cuh).
+#pragma once
+#include "ct_select.cuh"
+#include "ct_expert.cuh"
+#include "ct_rng.cuh"
+#include "countertune_b200.h"
+
+namespace ct {
+
+constexpr int MAX_ACTIVE = 18;
+
+struct SearchArgs {
+    // prediction table, column-major: column j of config i at table[j * ld + i]
+    const double* table;
+    int64_t ld;
+    int64_t n;
+    // replay data (DatasetReplaySource)
+    const double* runtime;
+    const int64_t* threads;
+    const double* counters;      // n x 23, REQUIRED_COUNTERS order
+    const uint8_t* has_record;
+    const uint32_t* stop_bits;   // nullable
+    // search parameters
+    int32_t outer, inner;
+    double inst_reaction, issue_sign, gamma;
+    int32_t literal_sign, generation;
+    int64_t cores;
+    int32_t delta_col[18];
+    // seeds
+    const uint32_t* entropy; int32_t n_entropy;
+    const uint32_t* prefix;  int32_t n_prefix;
+    int32_t child_per_rep;   int64_t rep_offset;
+    int32_t n_reps;
+    // tiling
+    int32_t rows, ntiles;
+    // storage
+    int32_t w_in_smem, e_in_smem;
+    double* scratch_w;           // gridDim.x * n doubles (if !w_in_smem)
+    uint32_t* scratch_e;         // gridDim.x * nwords   (if !e_in_smem)
+    int64_t nwords;
+    // outputs
+    int32_t* step_index;
+    uint8_t* step_profiled;
+    int64_t max_steps;
+    int32_t* n_steps;
+    int32_t* status;
+    int32_t* rep_error;
+    unsigned long long* stats;   // configs_scored, draws, uncertified, outer
+};
+
+struct __align__(16) Ctl {
+    u128 total;
+    u128 red_tot[32];
+    double red_max[32];
+    double red_min[32];
+    int red_pos[32];
+    int red_bad[32];
+    ActiveTerm act[MAX_ACTIVE];
+    double s_max, s_min;
+    int n_act;
+    int done;
+    int positive;
+    int nonfinite;
+};
+
+__device__ __forceinline__ bool bit_get(const uint32_t* b, int64_t i) {
+    return (b[i >> 5] >> (i & 31)) & 1u;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ Ctl ctl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t N = a.n;
+    const int64_t tile_len = 32LL * a.rows;
+
+    u128* tile_tot = reinterpret_cast<u128*>(smem);
+    unsigned char* p = smem + sizeof(u128) * (size_t)a.ntiles;
+    double* w;
+    if (a.w_in_smem) { w = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)N; }
+    else { w = a.scratch_w + (size_t)blockIdx.x * (size_t)N; }
+    uint32_t* expl;
+    if (a.e_in_smem) { expl = reinterpret_cast<uint32_t*>(p); }
+    else { expl = a.scratch_e + (size_t)blockIdx.x * (size_t)a.nwords; }
+
+    for (int rep = blockIdx.x; rep < a.n_reps; rep += gridDim.x) {
+        for (int64_t i = tid; i < a.nwords; i += NT) expl[i] = 0u;
+
+        // per-repetition serial state (thread 0 only)
+        Pcg64 rng;
+        int64_t c_prof = 0, ns = 0, n_expl = 0;
+        int st = CT_STATUS_BUDGET, err = 0;
+        unsigned long long scored = 0, draws = 0, uncert = 0, outers = 0;
+        int32_t* out_idx = a.step_index + (size_t)rep * a.max_steps;
+        uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
+        if (tid == 0) {
+            SeedWords sw{a.entropy, a.n_entropy, a.prefix, a.n_prefix,
+                         a.child_per_rep != 0, (uint32_t)(a.rep_offset + rep)};
+            rng.seed(seed_pool(sw));
+            c_prof = (int64_t)rng.integers((uint64_t)N);
+            ctl.done = 0;
+        }
+        __syncthreads();
+
+        for (int it = 0; it < a.outer; ++it) {
+            // ---------------- profile step, expert system (thread 0) ----------
+            if (tid == 0) {
+                if (!a.has_record[c_prof]) { st = CT_STATUS_ERROR; err = -4; ctl.done = 1; }
+                else {
+                    out_idx[ns] = (int32_t)c_prof; out_prof[ns] = 1; ++ns;
+                    uint32_t m = 1u << (c_prof & 31);
+                    if (!(expl[c_prof >> 5] & m)) { expl[c_prof >> 5] |= m; ++n_expl; }
+                    if (a.stop_bits && bit_get(a.stop_bits, c_prof)) { st = CT_STATUS_STOPPED; ctl.done = 1; }
+                }
+                if (!ctl.done) {
+                    double b[N_COMP], d[N_COMP];
+                    analyze(a.counters + (size_t)c_prof * N_REQ, a.generation, a.cores,
+                            a.threads[c_prof], b);
+                    react(b, a.inst_reaction, a.issue_sign, d);
+                    int na = 0;
+                    for (int k = 0; k < N_COMP; ++k) {
+                        if (d[k] == 0.0 || a.delta_col[k] < 0) continue;
+                        double pv = a.table[(size_t)a.delta_col[k] * a.ld + c_prof];
+                        if (pv == 0.0) continue;
+                        ctl.act[na].col = a.delta_col[k]; ctl.act[na].d = d[k]; ctl.act[na].p = pv;
+                        ++na;
+                    }
+                    ctl.n_act = na;
+                    if (n_expl >= N) { st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
+                    else { scored += (unsigned long long)(N - n_expl); ++outers; }
+                }
+            }
+            __syncthreads();
+            if (ctl.done) break;
+
+            // ---------------- Eq. 16 raw scores (all threads) ------------------
+            const int n_act = ctl.n_act;
+            const bool lit = a.literal_sign != 0;
+            double lmax = -INFINITY, lmin = INFINITY;
+            for (int64_t base = tid; base < N; base += 4LL * NT) {
+                double acc[4];
+                bool in[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    int64_t e = base + (int64_t)u * NT;
+                    in[u] = (e < N) && !bit_get(expl, e);
+                    acc[u] = 0.0;
+                }
+                for (int k = 0; k < n_act; ++k) {
+                    const ActiveTerm t = ctl.act[k];
+                    const double* col = a.table + (size_t)t.col * a.ld;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (in[u]) {
+                            double c = __ldg(col + base + (int64_t)u * NT);
+                            acc[u] = add(acc[u], raw_term(c, t, lit));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    int64_t e = base + (int64_t)u * NT;
+                    if (e < N) {
+                        w[e] = in[u] ? acc[u] : 0.0;
+                        if (in[u]) { lmax = nmax(lmax, acc[u]); lmin = nmin(lmin, acc[u]); }
+                    }
+                }
+            }
+            lmax = warp_max(lmax);
+            lmin = warp_min(lmin);
+            if (lane == 0) { ctl.red_max[warp] = lmax; ctl.red_min[warp] = lmin; }
+            __syncthreads();
+            if (tid == 0) {
+                double mx = ctl.red_max[0], mn = ctl.red_min[0];
+                for (int i = 1; i < NW; ++i) { mx = nmax(mx, ctl.red_max[i]); mn = nmin(mn, ctl.red_min[i]); }
+                ctl.s_max = mx; ctl.s_min = mn;
+            }
+            __syncthreads();
+
+            // ---------------- Eq. 17 weights + exact tile totals ---------------
+            {
+                const double smax = ctl.s_max, smin = ctl.s_min, gamma = a.gamma;
+                u128 wtot = 0;
+                int pos = 0, bad = 0;
+                for (int t = warp; t < a.ntiles; t += NW) {
+                    u128 sum = 0;
+                    for (int j = 0; j < a.rows; ++j) {
+                        int64_t e = (int64_t)t * tile_len + 32LL * j + lane;
+                        if (e < N) {
+                            double wt = 0.0;
+                            if (!bit_get(expl, e)) wt = weight(w[e], smax, smin, gamma);
+                            w[e] = wt;
+                            u128 f;
+                            if (to_fx(wt, &f)) sum += f; else bad = 1;
+                            pos += (wt > 0.0);
+                        }
+                    }
+                    sum = warp_sum(sum);
+                    if (lane == 0) tile_tot[t] = sum;
+                    wtot += sum;
+                }
+                pos = warp_sum_i(pos);
+                bad = __any_sync(FULL, bad);
+                if (lane == 0) { ctl.red_tot[warp] = wtot; ctl.red_pos[warp] = pos; ctl.red_bad[warp] = bad; }
+            }
+            __syncthreads();
+
+            // ---------------- n certified draws (warp 0) ----------------------
+            if (warp == 0) {
+                u128 total = 0;
+                int positive = 0, bad = 0;
+                for (int i = 0; i < NW; ++i) {
+                    total += ctl.red_tot[i]; positive += ctl.red_pos[i]; bad |= ctl.red_bad[i];
+                }
+                int done = 0;
+                if (bad) { if (lane == 0) { st = CT_STATUS_ERROR; err = -7; } done = 1; }
+                double t_best = INFINITY;
+                for (int k = 0; k < a.inner && !done; ++k) {
+                    if (positive <= 0) { if (lane == 0) st = CT_STATUS_EXHAUSTED; done = 1; break; }
+                    double u = 0.0;
+                    if (lane == 0) u = rng.next_double();
+                    u = __shfl_sync(FULL, u, 0);
+                    double total_d = fx_to_double(total);
+                    double r = mul(u, total_d);
+                    u128 r_fx = floor_fx(r);
+                    Located pk = warp_locate(tile_tot, a.ntiles, w, N, a.rows, r_fx, lane);
+                    int64_t chosen = pk.idx;
+                    if (!certify(pk, r_fx, total_d, N)) {
+                        if (lane == 0) { chosen = sequential_select(w, N, u); ++uncert; }
+                        chosen = __shfl_sync(FULL, (long long)chosen, 0);
+                    }
+                    if (lane == 0) ++draws;
+                    if (chosen < 0 || chosen >= N || !a.has_record[chosen]) {
+                        if (lane == 0) { st = CT_STATUS_ERROR; err = -4; }
+                        done = 1; break;
+                    }
+                    // zero the drawn weight: exact prefix stays exact
+                    u128 f = 0;
+                    to_fx(w[chosen], &f);
+                    __syncwarp();
+                    if (lane == 0) {
+                        w[chosen] = 0.0;
+                        tile_tot[chosen / tile_len] -= f;
+                    }
+                    total -= f;
+                    --positive;
+                    double rt = a.runtime[chosen];
+                    if (lane == 0) {
+                        out_idx[ns] = (int32_t)chosen; out_prof[ns] = 0; ++ns;
+                        uint32_t m = 1u << (chosen & 31);
+                        if (!(expl[chosen >> 5] & m)) { expl[chosen >> 5] |= m; ++n_expl; }
+                    }
+                    if (a.stop_bits && bit_get(a.stop_bits, chosen)) {
+                        if (lane == 0) st = CT_STATUS_STOPPED;
+                        done = 1; break;
+                    }
+                    if (rt <= t_best) { t_best = rt; if (lane == 0) c_prof = chosen; }
+                    __syncwarp();
+                }
+                if (lane == 0) ctl.done = done;
+            }
+            __syncthreads();
+            if (ctl.done) break;
+        }
+
+        if (tid == 0) {
+            a.n_steps[rep] = (int32_t)ns;
+            a.status[rep] = st;
+            a.rep_error[rep] = err;
+            atomicAdd(&a.stats[0], scored);
+            atomicAdd(&a.stats[1], draws);
+            atomicAdd(&a.stats[2], uncert);
+            atomicAdd(&a.stats[3], outers);
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// run_random_search (search.py:317-335): one thread per repetition shuffles
+// arange(N) with numpy's Fisher-Yates (random_interval) in a scratch slice and
+// emits the prefix up to the first stop configuration.
+struct RandomArgs {
+    int64_t n;
+    const uint8_t* has_record;
+    const uint32_t* stop_bits;     // nullable
+    int64_t max_steps_req;         // < 0: None
+    const uint32_t* entropy; int32_t n_entropy;
+    const uint32_t* prefix;  int32_t n_prefix;
+    int32_t child_per_rep;   int64_t rep_offset;
+    int32_t n_reps;
+    int32_t* perm_scratch;         // n_slots * n
+    int32_t n_slots;
+    int32_t* step_index;
+    uint8_t* step_profiled;
+    int64_t max_steps;
+    int32_t* n_steps;
+    int32_t* status;
+    int32_t* rep_error;
+};
+
+__global__ void k_random_search(const RandomArgs a) {
+    for (int rep = blockIdx.x * blockDim.x + threadIdx.x; rep < a.n_reps;
+         rep += gridDim.x * blockDim.x) {
+        int slot = (blockIdx.x * blockDim.x + threadIdx.x);
+        int32_t* perm = a.perm_scratch + (size_t)slot * a.n;
+        const int64_t N = a.n;
+        SeedWords sw{a.entropy, a.n_entropy, a.prefix, a.n_prefix,
+                     a.child_per_rep != 0, (uint32_t)(a.rep_offset + rep)};
+        Pcg64 rng;
+        rng.seed(seed_pool(sw));
+        for (int64_t i = 0; i < N; ++i) perm[i] = (int32_t)i;
+        for (int64_t i = N - 1; i > 0; --i) {
+            int64_t j = (int64_t)rng.interval((uint64_t)i);
+            int32_t t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+        }
+        int64_t lim = N;
+        if (a.max_steps_req >= 0 && a.max_steps_req < N) lim = a.max_steps_req;
+        int st = (a.max_steps_req < 0 || a.max_steps_req >= N) ? CT_STATUS_EXHAUSTED : CT_STATUS_BUDGET;
+        int err = 0;
+        int64_t ns = 0;
+        int32_t* out_idx = a.step_index + (size_t)rep * a.max_steps;
+        uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
+        for (int64_t pos = 0; pos < lim; ++pos) {
+            int32_t idx = perm[pos];
+            if (!a.has_record[idx]) { st = CT_STATUS_ERROR; err = -4; break; }
+            out_idx[ns] = idx; out_prof[ns] = 0; ++ns;
+            if (a.stop_bits && bit_get(a.stop_bits, idx)) { st = CT_STATUS_STOPPED; break; }
+        }
+        a.n_steps[rep] = (int32_t)ns;
+        a.status[rep] = st;
+        a.rep_error[rep] = err;
+    }
+}
+
+}  // namespace ct
