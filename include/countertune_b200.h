@@ -53,6 +53,8 @@ extern "C" {
 #define CT_N_REQUIRED 23
 /* number of keys react() emits, insertion order (bottlenecks.py:216-229) */
 #define CT_N_DELTA 18
+/* most keys a single score_configurations call may carry */
+#define CT_MAX_SCORE_KEYS 32
 
 typedef struct ct_ctx ct_ctx;
 
@@ -118,6 +120,14 @@ int ct_normalize(ct_ctx* ctx, const double* raw, const uint8_t* pool, int64_t n,
 int ct_select(ct_ctx* ctx, const double* norm, int64_t n, double u,
               int64_t* chosen_out, int32_t* certified_out);
 
+/* analyze() + react() (bottlenecks.py:115-230) on the device for one
+ * measured counter map (REQUIRED_COUNTERS order).  out37 receives the 18
+ * bottleneck components (COMPONENT_NAMES order), the 18 deltas (react()
+ * insertion order) and the degenerate_instructions flag as 0.0 / 1.0. */
+int ct_analyze_react(ct_ctx* ctx, const double* counters23, int32_t generation, int64_t cores,
+                     int64_t global_threads, double inst_reaction, double issue_delta_sign,
+                     double* out37);
+
 /* ---- batched replay searches (harness.py:139-163) ---------------------- */
 
 typedef struct {
@@ -150,6 +160,7 @@ typedef struct {
     int64_t draws;                 /* weighted draws made                   */
     int64_t uncertified;           /* draws re-decided by sequential cumsum */
     int64_t outer_iterations;      /* outer iterations executed             */
+    int64_t algorithmic_bytes;     /* sum over scorings of pool * (8 * C_used + 16) */
 } ct_batch_stats;
 
 /* run_profile_search (search.py:338-399) for n_reps repetitions on the

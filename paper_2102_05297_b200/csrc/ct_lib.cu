@@ -108,8 +108,8 @@ struct ScoreSingleArgs {
     const double* table; int64_t ld; int64_t n;
     int64_t profile;
     int32_t n_delta;
-    int32_t cols[CT_N_DELTA];
-    double vals[CT_N_DELTA];
+    int32_t cols[CT_MAX_SCORE_KEYS];
+    double vals[CT_MAX_SCORE_KEYS];
     const uint8_t* explored;
     const uint8_t* scoreable;  // nullable
     int32_t literal_sign;
@@ -117,7 +117,7 @@ struct ScoreSingleArgs {
 };
 
 __global__ void k_score_single(const ScoreSingleArgs a) {
-    __shared__ ActiveTerm act[CT_N_DELTA];
+    __shared__ ActiveTerm act[CT_MAX_SCORE_KEYS];
     __shared__ int n_act;
     if (threadIdx.x == 0) {
         int na = 0;
@@ -266,6 +266,16 @@ __global__ void k_select_single(const double* w, int64_t n, int rows, int ntiles
     }
 }
 
+__global__ void k_analyze_react(const double* c, int gen, int64_t cores, int64_t threads,
+                                double inst_reaction, double issue_sign, double* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double b[N_COMP], d[N_COMP];
+    bool deg = analyze(c, gen, cores, threads, b);
+    react(b, inst_reaction, issue_sign, d);
+    for (int k = 0; k < N_COMP; ++k) { out[k] = b[k]; out[N_COMP + k] = d[k]; }
+    out[2 * N_COMP] = deg ? 1.0 : 0.0;
+}
+
 int rows_for(int64_t n) {
     int rows = (int)std::lround(std::sqrt((double)n) / 32.0);
     return std::max(1, rows);
@@ -308,7 +318,7 @@ int ensure_results(ct_ctx* ctx, int64_t reps, int64_t max_steps) {
     CT_CUDA(ctx->n_steps.ensure(reps));
     CT_CUDA(ctx->status.ensure(reps));
     CT_CUDA(ctx->rep_error.ensure(reps));
-    CT_CUDA(cudaMemsetAsync(ctx->stats.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    CT_CUDA(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
     ctx->res_reps = reps;
     ctx->res_max_steps = max_steps;
     ctx->res_valid = true;
@@ -364,7 +374,7 @@ int ct_create(int device, ct_ctx** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete c; return fail(CT_ERR_CUDA, cudaGetErrorString(e)); }
     c->stream = c->own;
-    e = c->stats.ensure(4);
+    e = c->stats.ensure(8);
     if (e != cudaSuccess) { delete c; return fail(CT_ERR_CUDA, cudaGetErrorString(e)); }
     *out = c;
     return CT_OK;
@@ -466,8 +476,8 @@ int ct_score(ct_ctx* ctx, int64_t profile, const int32_t* cols, const double* va
              uint8_t* scoreable_out, int32_t* has_scoreable) {
     int rc = check_ctx(ctx); if (rc) return rc;
     if (!ctx->table.p) return fail(CT_ERR_STATE, "no prediction table uploaded");
-    if (n_delta < 0 || n_delta > CT_N_DELTA || (n_delta && (!cols || !vals)))
-        return fail(CT_ERR_VALUE, "delta must hold at most 18 keys");
+    if (n_delta < 0 || n_delta > CT_MAX_SCORE_KEYS || (n_delta && (!cols || !vals)))
+        return fail(CT_ERR_VALUE, "delta must hold at most 32 scored keys");
     if (!explored || !raw_out) return fail(CT_ERR_VALUE, "null explored/raw buffer");
     const int64_t n = ctx->n;
     if (profile < 0 || profile >= n) return fail(CT_ERR_VALUE, "profile index out of range");
@@ -559,6 +569,26 @@ int ct_select(ct_ctx* ctx, const double* norm, int64_t n, double u, int64_t* cho
     if (out[0] < 0) return fail(CT_ERR_EXHAUSTED, "every configuration is explored");
     *chosen = out[0];
     if (certified) *certified = (int32_t)out[1];
+    return CT_OK;
+}
+
+int ct_analyze_react(ct_ctx* ctx, const double* counters23, int32_t generation, int64_t cores,
+                     int64_t global_threads, double inst_reaction, double issue_sign,
+                     double* out37) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!counters23 || !out37) return fail(CT_ERR_VALUE, "null buffers");
+    if (!(inst_reaction > 0.0 && inst_reaction < 1.0))
+        return fail(CT_ERR_VALUE, "inst_reaction must lie in (0, 1), got " + std::to_string(inst_reaction));
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(ctx->vec_a.ensure(CT_N_REQUIRED + 2 * CT_N_DELTA + 1));
+    double* dc = ctx->vec_a.p;
+    double* dout = ctx->vec_a.p + CT_N_REQUIRED;
+    CT_CUDA(cudaMemcpyAsync(dc, counters23, sizeof(double) * CT_N_REQUIRED, cudaMemcpyHostToDevice, s));
+    k_analyze_react<<<1, 32, 0, s>>>(dc, generation, cores, global_threads, inst_reaction,
+                                     issue_sign, dout);
+    CT_CUDA(cudaGetLastError());
+    CT_CUDA(cudaMemcpyAsync(out37, dout, sizeof(double) * (2 * CT_N_DELTA + 1), cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
     return CT_OK;
 }
 
@@ -679,7 +709,7 @@ int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled, i
         if (status) CT_CUDA(cudaMemcpyAsync(status, ctx->status.p, 4 * r, cudaMemcpyDeviceToHost, s));
         if (rep_error) CT_CUDA(cudaMemcpyAsync(rep_error, ctx->rep_error.p, 4 * r, cudaMemcpyDeviceToHost, s));
     }
-    unsigned long long st[4] = {0, 0, 0, 0};
+    unsigned long long st[5] = {0, 0, 0, 0, 0};
     CT_CUDA(cudaMemcpyAsync(st, ctx->stats.p, sizeof(st), cudaMemcpyDeviceToHost, s));
     CT_CUDA(cudaStreamSynchronize(s));
     if (stats) {
@@ -687,6 +717,7 @@ int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled, i
         stats->draws = (int64_t)st[1];
         stats->uncertified = (int64_t)st[2];
         stats->outer_iterations = (int64_t)st[3];
+        stats->algorithmic_bytes = (int64_t)st[4];
     }
     return CT_OK;
 }

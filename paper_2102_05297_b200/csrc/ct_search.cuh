@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
         Pcg64 rng;
         int64_t c_prof = 0, ns = 0, n_expl = 0;
         int st = CT_STATUS_BUDGET, err = 0;
-        unsigned long long scored = 0, draws = 0, uncert = 0, outers = 0;
+        unsigned long long scored = 0, draws = 0, uncert = 0, outers = 0, abytes = 0;
         int32_t* out_idx = a.step_index + (size_t)rep * a.max_steps;
         uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
         if (tid == 0) {
@@ -124,7 +124,10 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
         for (int it = 0; it < a.outer; ++it) {
             // ---------------- profile step, expert system (thread 0) ----------
             if (tid == 0) {
-                if (!a.has_record[c_prof]) { st = CT_STATUS_ERROR; err = -4; ctl.done = 1; }
+                if (!a.has_record[c_prof]) {
+                    st = CT_STATUS_ERROR; err = -4; ctl.done = 1;
+                    if (ns < a.max_steps) out_idx[ns] = (int32_t)c_prof;   // failing index
+                }
                 else {
                     out_idx[ns] = (int32_t)c_prof; out_prof[ns] = 1; ++ns;
                     uint32_t m = 1u << (c_prof & 31);
@@ -146,7 +149,11 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
                     }
                     ctl.n_act = na;
                     if (n_expl >= N) { st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
-                    else { scored += (unsigned long long)(N - n_expl); ++outers; }
+                    else {
+                        unsigned long long pool = (unsigned long long)(N - n_expl);
+                        scored += pool; ++outers;
+                        abytes += pool * (8ull * (unsigned long long)na + 16ull);
+                    }
                 }
             }
             __syncthreads();
@@ -250,7 +257,10 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
                     }
                     if (lane == 0) ++draws;
                     if (chosen < 0 || chosen >= N || !a.has_record[chosen]) {
-                        if (lane == 0) { st = CT_STATUS_ERROR; err = -4; }
+                        if (lane == 0) {
+                            st = CT_STATUS_ERROR; err = -4;
+                            if (ns < a.max_steps) out_idx[ns] = (int32_t)chosen;
+                        }
                         done = 1; break;
                     }
                     // zero the drawn weight: exact prefix stays exact
@@ -290,6 +300,7 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
             atomicAdd(&a.stats[1], draws);
             atomicAdd(&a.stats[2], uncert);
             atomicAdd(&a.stats[3], outers);
+            atomicAdd(&a.stats[4], abytes);
         }
         __syncthreads();
     }
@@ -342,7 +353,7 @@ __global__ void k_random_search(const RandomArgs a) {
         uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
         for (int64_t pos = 0; pos < lim; ++pos) {
             int32_t idx = perm[pos];
-            if (!a.has_record[idx]) { st = CT_STATUS_ERROR; err = -4; break; }
+            if (!a.has_record[idx]) { st = CT_STATUS_ERROR; err = -4; out_idx[ns] = idx; break; }
             out_idx[ns] = idx; out_prof[ns] = 0; ++ns;
             if (a.stop_bits && bit_get(a.stop_bits, idx)) { st = CT_STATUS_STOPPED; break; }
         }

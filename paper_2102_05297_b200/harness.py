@@ -1,0 +1,402 @@
+"""Replay experiments on the GPU (the reference's harness.py:49-398).
+
+simulate() runs all R repetitions of one ExperimentSpec as ONE batched device
+launch (one CTA per repetition, the numpy Generator streams regenerated on
+the device from the master seed), or split over several GPUs by contiguous
+repetition ranges.  Aggregation follows harness.py:187-244 operation for
+operation, so reports are byte-identical to the reference's for the same
+trajectories.
+"""
+
+import math
+import os
+import threading
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native
+from .counters import GLOBAL_THREADS
+from .errors import AnalysisError, CounterTuneError
+from .search import (DEFAULT_INST_REACTION, PredictionTable, _as_table, rep_error,
+                     search_params)
+from .space import missing_required, replay_arrays, well_performing_mask
+
+WORKERS_ENV = "COUNTERTUNE_WORKERS"
+SEARCHER_PROFILE = "profile"
+SEARCHER_RANDOM = "random"
+DEFAULT_REPETITIONS = 1000
+DEFAULT_TIME_REPETITIONS = 100
+DEFAULT_PROFILING_OVERHEAD = 3.0
+TIME_GRID_POINTS = 100
+
+
+@dataclass
+class ExperimentSpec:
+    """Everything one batch of simulated repetitions depends on (harness.py:49-96)."""
+
+    dataset: object
+    searcher: str = SEARCHER_RANDOM
+    model: object = None
+    name: str = "experiment"
+    repetitions: int = DEFAULT_REPETITIONS
+    inner_steps: int = 5
+    outer_iterations: Optional[int] = None
+    seed: int = 0
+    slack: float = 1.1
+    profiling_overhead: float = DEFAULT_PROFILING_OVERHEAD
+    inst_reaction: float = DEFAULT_INST_REACTION
+    literal_sign: bool = False
+    score_top_k: Optional[int] = None
+    time_repetitions: Optional[int] = None
+    # extension: False replays every repetition for its full budget
+    # (stop_indices=frozenset(), the throughput mode of BASELINE.md)
+    stop_at_well_performing: bool = True
+
+    def __post_init__(self):
+        if self.searcher not in (SEARCHER_PROFILE, SEARCHER_RANDOM):
+            raise ValueError(f"unknown searcher {self.searcher!r}")
+        if self.repetitions < 1:
+            raise ValueError("repetitions must be >= 1")
+        if self.time_repetitions is not None and self.time_repetitions < 1:
+            raise ValueError("time_repetitions must be >= 1")
+        if self.slack < 1.0:
+            raise ValueError("slack must be >= 1.0")
+        if self.profiling_overhead < 1.0:
+            raise ValueError("profiling_overhead must be >= 1.0")
+        if self.inner_steps < 0:
+            raise ValueError("inner_steps must be >= 0")
+        if self.searcher == SEARCHER_PROFILE and self.model is None:
+            raise ValueError("the profile searcher needs a model")
+
+    def resolved_outer_iterations(self) -> int:
+        if self.outer_iterations is not None:
+            if self.outer_iterations < 1:
+                raise ValueError("outer_iterations must be >= 1")
+            return self.outer_iterations
+        n = len(self.dataset.space)
+        if self.inner_steps == 0:
+            return n
+        return max(1, math.ceil((n - 1) / self.inner_steps))
+
+
+@dataclass
+class ConvergenceReport:
+    """Aggregated outcome of one experiment's repetitions (harness.py:98-132)."""
+
+    name: str
+    searcher: str
+    dataset_label: str
+    repetitions: int
+    inner_steps: int
+    outer_iterations: int
+    seed: int
+    slack: float
+    profiling_overhead: float
+    steps: np.ndarray
+    censored: int
+    mean_time_seconds: float
+    step_curve_mean: np.ndarray
+    step_curve_std: np.ndarray
+    time_grid_seconds: np.ndarray
+    time_curve_mean: np.ndarray
+    time_curve_std: np.ndarray
+    baseline_name: Optional[str] = None
+    improvement: Optional[float] = None
+    # device-side accounting of the run (not part of the reference's report)
+    configs_scored: int = 0
+    uncertified_draws: int = 0
+
+    @property
+    def mean_steps(self) -> float:
+        return float(np.mean(self.steps))
+
+    @property
+    def median_steps(self) -> float:
+        return float(np.median(self.steps))
+
+    @property
+    def stddev_steps(self) -> float:
+        return float(np.std(self.steps))
+
+
+def _worker_count() -> int:
+    """COUNTERTUNE_WORKERS is validated as in the reference (harness.py:166-172);
+    the device batch makes process fan-out unnecessary."""
+    raw = os.environ.get(WORKERS_ENV, "1")
+    try:
+        workers = int(raw)
+    except ValueError:
+        raise CounterTuneError(f"{WORKERS_ENV} must be an integer, got {raw!r}")
+    return max(1, workers)
+
+
+@dataclass
+class BatchResult:
+    """Raw trajectories of R repetitions (rows), as the device returns them."""
+
+    step_index: np.ndarray      # R x max_steps int32
+    step_profiled: np.ndarray   # R x max_steps uint8
+    n_steps: np.ndarray         # R int32
+    status: np.ndarray          # R int32
+    configs_scored: int
+    uncertified: int
+    draws: int
+    algorithmic_bytes: int = 0
+
+
+def prepare_device(ctx: "_native.Context", spec: ExperimentSpec, table=None):
+    """Upload replay data, stop mask and (profile searcher) the prediction table."""
+    ds = spec.dataset
+    rt, th, req, hr = replay_arrays(ds)
+    stop = well_performing_mask(ds, spec.slack)
+    if not spec.stop_at_well_performing:
+        stop[:] = False
+    ctx.upload_replay(rt, th, np.nan_to_num(req), hr, stop.astype(np.uint8))
+    params = None
+    if spec.searcher == SEARCHER_PROFILE:
+        missing = missing_required(ds)
+        if missing:
+            raise AnalysisError(f"counter map is missing {', '.join(missing)}")
+        if table is None:
+            table = _as_table(spec.model, ds.space)
+        ctx.upload_table(table.matrix)
+        if spec.score_top_k is not None:
+            raise CounterTuneError("score_top_k is not supported by the batched device search")
+        params = search_params(table, ds.arch, i=spec.resolved_outer_iterations(),
+                               n=spec.inner_steps, inst_reaction=spec.inst_reaction,
+                               literal_sign=spec.literal_sign, score_top_k=None, use_stop=True)
+        if not 0.0 < spec.inst_reaction < 1.0:
+            raise ValueError(f"inst_reaction must lie in (0, 1), got {spec.inst_reaction}")
+    return params, rt
+
+
+def launch(ctx, spec: ExperimentSpec, params, rep_offset: int, n_reps: int):
+    seeds = _native.SeedWords(spec.seed, child_per_rep=True, rep_offset=rep_offset)
+    if spec.searcher == SEARCHER_RANDOM:
+        ctx.launch_random(seeds, n_reps, None, use_stop=True)
+    else:
+        ctx.launch_profile(params, seeds, n_reps)
+
+
+def run_batch(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None,
+              table=None) -> Tuple[BatchResult, np.ndarray]:
+    """All repetitions of spec on the given GPUs (contiguous rep ranges)."""
+    devices = list(devices) if devices else [0]
+    R = spec.repetitions
+    parts = np.array_split(np.arange(R), len(devices))
+    if table is None and spec.searcher == SEARCHER_PROFILE:
+        table = _as_table(spec.model, spec.dataset.space)
+    results = [None] * len(devices)
+    errors = [None] * len(devices)
+    runtime = [None]
+
+    def work(k):
+        try:
+            ctx = _native.context(devices[k])
+            params, rt = prepare_device(ctx, spec, table)
+            runtime[0] = rt
+            idxs = parts[k]
+            if idxs.size == 0:
+                results[k] = None
+                return
+            launch(ctx, spec, params, int(idxs[0]), int(idxs.size))
+            results[k] = ctx.fetch(int(idxs.size))
+        except BaseException as exc:   # re-raised on the caller's thread
+            errors[k] = exc
+
+    if len(devices) == 1:
+        work(0)
+    else:
+        threads = [threading.Thread(target=work, args=(k,)) for k in range(len(devices))]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    for exc in errors:
+        if exc is not None:
+            raise exc
+    parts_ok = [r for r in results if r is not None]
+    width = max(r[0].shape[1] for r in parts_ok)
+
+    def cat(j, dtype):
+        rows = []
+        for r in parts_ok:
+            a = r[j]
+            if a.ndim == 2 and a.shape[1] < width:
+                a = np.pad(a, ((0, 0), (0, width - a.shape[1])))
+            rows.append(a)
+        return np.concatenate(rows).astype(dtype, copy=False)
+
+    res = BatchResult(step_index=cat(0, np.int32), step_profiled=cat(1, np.uint8),
+                      n_steps=cat(2, np.int32), status=cat(3, np.int32),
+                      configs_scored=sum(r[5].configs_scored for r in parts_ok),
+                      uncertified=sum(r[5].uncertified for r in parts_ok),
+                      draws=sum(r[5].draws for r in parts_ok),
+                      algorithmic_bytes=sum(r[5].algorithmic_bytes for r in parts_ok))
+    err = cat(4, np.int32)
+    bad = np.flatnonzero(res.status == _native.CT_STATUS_ERROR)
+    if bad.size:
+        r = int(bad[0])
+        ns = int(res.n_steps[r])
+        failing = int(res.step_index[r, ns]) if ns < res.step_index.shape[1] else -1
+        raise rep_error(int(err[r]), failing)
+    return res, runtime[0]
+
+
+def aggregate(spec: ExperimentSpec, res: BatchResult, runtime: np.ndarray) -> ConvergenceReport:
+    """harness.py:187-244 on the device trajectories (same float operations)."""
+    reps = spec.repetitions
+    nst = res.n_steps.astype(np.int64)
+    hit = res.status == _native.CT_STATUS_STOPPED
+    idx = res.step_index
+    valid = np.arange(idx.shape[1])[None, :] < nst[:, None]
+    rts = np.where(valid, runtime[np.where(valid, idx, 0)], np.inf)
+    overhead = spec.profiling_overhead
+    costs = np.where(valid, rts * np.where(res.step_profiled.astype(bool), overhead, 1.0), 0.0)
+    bsf_all = np.minimum.accumulate(rts, axis=1)
+    times_all = np.cumsum(costs, axis=1)
+
+    steps = nst.astype(float)
+    censored = int(np.count_nonzero(~hit))
+    total_times = times_all[np.arange(reps), nst - 1]
+
+    max_len = int(nst.max())
+    col_sum = np.zeros(max_len)
+    col_sq = np.zeros(max_len)
+    for r in range(reps):
+        bsf = bsf_all[r, :nst[r]]
+        padded = np.concatenate([bsf, np.full(max_len - nst[r], bsf[-1])])
+        col_sum += padded
+        col_sq += padded * padded
+    mean = col_sum / reps
+    var = np.maximum(0.0, col_sq / reps - mean * mean)
+    step_std = np.sqrt(var)
+
+    tr = reps if spec.time_repetitions is None else min(reps, spec.time_repetitions)
+    t_start = max(float(times_all[r, 0]) for r in range(tr))
+    t_end = max(float(times_all[r, nst[r] - 1]) for r in range(tr))
+    if t_end > t_start:
+        grid = np.linspace(t_start, t_end, TIME_GRID_POINTS)
+    else:
+        grid = np.array([t_start])
+    tc_sum = np.zeros(grid.size)
+    tc_sq = np.zeros(grid.size)
+    for r in range(tr):
+        times = times_all[r, :nst[r]]
+        bsf = bsf_all[r, :nst[r]]
+        pos = np.searchsorted(times, grid, side="right") - 1
+        sampled = bsf[np.clip(pos, 0, len(bsf) - 1)]
+        tc_sum += sampled
+        tc_sq += sampled * sampled
+    tmean = tc_sum / tr
+    tvar = np.maximum(0.0, tc_sq / tr - tmean * tmean)
+    ds = spec.dataset
+    return ConvergenceReport(
+        name=spec.name, searcher=spec.searcher,
+        dataset_label=f"{ds.arch.name}/{ds.input_label}", repetitions=reps,
+        inner_steps=spec.inner_steps, outer_iterations=spec.resolved_outer_iterations(),
+        seed=spec.seed, slack=spec.slack, profiling_overhead=spec.profiling_overhead,
+        steps=steps, censored=censored, mean_time_seconds=float(np.mean(total_times)) / 1e6,
+        step_curve_mean=mean, step_curve_std=step_std, time_grid_seconds=grid / 1e6,
+        time_curve_mean=tmean, time_curve_std=np.sqrt(tvar),
+        configs_scored=int(res.configs_scored), uncertified_draws=int(res.uncertified))
+
+
+def simulate(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None) -> ConvergenceReport:
+    """Run the repetitions on the GPU(s) and aggregate (harness.py:175-244)."""
+    _worker_count()
+    res, runtime = run_batch(spec, devices)
+    return aggregate(spec, res, runtime)
+
+
+def pair_with_baseline(candidate: ConvergenceReport,
+                       baseline: ConvergenceReport) -> ConvergenceReport:
+    if candidate.repetitions != baseline.repetitions:
+        raise ValueError("improvement factors require identical repetition counts")
+    candidate.baseline_name = baseline.name
+    candidate.improvement = baseline.mean_steps / candidate.mean_steps
+    return candidate
+
+
+def _fmt(value) -> str:
+    if value is None:
+        return ""
+    if isinstance(value, float):
+        return repr(value)
+    return str(value)
+
+
+def _safe_name(name: str) -> str:
+    return "".join(ch if ch.isalnum() or ch in "-_" else "-" for ch in name)
+
+
+SUMMARY_COLUMNS = ("name", "searcher", "dataset", "repetitions", "n", "i", "seed",
+                   "slack", "profiling_overhead", "mean_steps", "median_steps",
+                   "stddev_steps", "censored", "mean_time_seconds",
+                   "improvement_vs_baseline", "baseline")
+
+
+def report(reports: List[ConvergenceReport], out_dir) -> List[str]:
+    """summary.csv + per-experiment curves, byte-stable (harness.py:344-388)."""
+    os.makedirs(out_dir, exist_ok=True)
+    written = []
+    lines = [",".join(SUMMARY_COLUMNS)]
+    for rep in reports:
+        lines.append(",".join([
+            rep.name, rep.searcher, rep.dataset_label, str(rep.repetitions),
+            str(rep.inner_steps), str(rep.outer_iterations), str(rep.seed),
+            _fmt(rep.slack), _fmt(rep.profiling_overhead), _fmt(rep.mean_steps),
+            _fmt(rep.median_steps), _fmt(rep.stddev_steps), str(rep.censored),
+            _fmt(rep.mean_time_seconds), _fmt(rep.improvement), rep.baseline_name or "",
+        ]))
+    path = os.path.join(out_dir, "summary.csv")
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("\n".join(lines) + "\n")
+    written.append(path)
+    for rep in reports:
+        base = _safe_name(rep.name)
+        rows = ["step,mean,stddev"]
+        for i in range(rep.step_curve_mean.size):
+            rows.append(f"{i + 1},{_fmt(float(rep.step_curve_mean[i]))},"
+                        f"{_fmt(float(rep.step_curve_std[i]))}")
+        path = os.path.join(out_dir, f"curve_{base}.csv")
+        with open(path, "w", encoding="utf-8", newline="\n") as fh:
+            fh.write("\n".join(rows) + "\n")
+        written.append(path)
+        rows = ["seconds,mean,stddev"]
+        for i in range(rep.time_grid_seconds.size):
+            rows.append(f"{_fmt(float(rep.time_grid_seconds[i]))},"
+                        f"{_fmt(float(rep.time_curve_mean[i]))},"
+                        f"{_fmt(float(rep.time_curve_std[i]))}")
+        path = os.path.join(out_dir, f"curve_{base}_time.csv")
+        with open(path, "w", encoding="utf-8", newline="\n") as fh:
+            fh.write("\n".join(rows) + "\n")
+        written.append(path)
+    return written
+
+
+def counter_prediction_errors(models, dataset) -> Dict[str, Tuple[float, float]]:
+    """Per-counter (MAE, RMSE) over all records (harness.py:268-289)."""
+    table = PredictionTable.from_model_set(models, dataset.space)
+    rt, th, _, hr = replay_arrays(dataset)
+    names = getattr(dataset, "counter_names", None)
+    errors: Dict[str, Tuple[float, float]] = {}
+    for abbr in table.counter_names:
+        col = table.column[abbr]
+        measured, predicted = [], []
+        for rec in dataset.records:
+            if abbr == GLOBAL_THREADS:
+                measured.append(float(rec.global_threads))
+            elif abbr in rec.counters:
+                measured.append(rec.counters[abbr])
+            else:
+                continue
+            predicted.append(table.matrix[rec.config_index, col])
+        if not measured:
+            continue
+        err = np.array(predicted) - np.array(measured)
+        errors[abbr] = (float(np.mean(np.abs(err))), float(math.sqrt(np.mean(err * err))))
+    del rt, th, hr, names
+    return errors
