@@ -138,7 +138,7 @@ def cpu_baseline(reps: int, cores: int):
     of the same workload, fanned out over `cores` processes as the reference's
     harness does (COUNTERTUNE_WORKERS)."""
     from concurrent.futures import ProcessPoolExecutor
-    chunks = [(k * reps // cores, (k + 1) * reps // cores, REPS) for k in range(cores)]
+    chunks = [(k * reps // cores, (k + 1) * reps // cores, max(REPS, reps)) for k in range(cores)]
     t0 = time.perf_counter()
     if cores == 1:
         out = [_oracle_chunk(chunks[0])]
@@ -239,6 +239,13 @@ def run_ours(args):
     per_launch = t_total / args.steps
     hbm, peak_kind = _peaks()
     achieved_gbs = bytes_per_step / per_launch / 1e9
+    print(f"[bench] rank {rank}: {configs_per_step} configs/step, {per_launch * 1e3:.3f} ms/step, "
+          f"{value:.4g} configs/s, {achieved_gbs:.1f} GB/s algorithmic, "
+          f"uncertified {stats0.uncertified}", file=sys.stderr, flush=True)
+    if args.kernel_only:
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     # e2e through the public API: harness.simulate with host buffers
     # (H2D: table, replay arrays, stop mask, seeds; D2H: trajectories)
@@ -325,6 +332,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-only", action="store_true",
+                    help="time the search kernel only (for ncu captures)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

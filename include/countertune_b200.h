@@ -128,6 +128,14 @@ int ct_analyze_react(ct_ctx* ctx, const double* counters23, int32_t generation, 
                      int64_t global_threads, double inst_reaction, double issue_delta_sign,
                      double* out37);
 
+/* Diagnostics: the device's inline IEEE division (ct_hd.cuh dvd_fast)
+ * against __ddiv_rn on n generated operand pairs of 4 kinds (raw bit
+ * patterns, small integers, two Eq. 16 shapes); *mismatches counts pairs
+ * whose quotients differ in any bit (NaN == NaN).  first_bad (nullable,
+ * 16 doubles) receives a, b, fast, reference of the first mismatch per kind. */
+int ct_check_division(ct_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches,
+                      double* first_bad);
+
 /* ---- batched replay searches (harness.py:139-163) ---------------------- */
 
 typedef struct {

@@ -105,6 +105,7 @@ SIGNATURES = {
     "ct_fetch_results": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _P(BatchStats)]),
     "ct_result_device_ptrs": (ctypes.c_int, [_vp, _P(_vp), _P(_vp), _P(_vp), _P(_vp)]),
     "ct_analyze_react": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64, _dbl, _dbl, _vp]),
+    "ct_check_division": (ctypes.c_int, [_vp, _i64, ctypes.c_uint64, _P(_i64), _vp]),
 }
 
 _lib = None
@@ -253,6 +254,13 @@ class Context:
                                          int(global_threads), float(inst_reaction),
                                          float(issue_sign), ptr(out)))
         return out[:N_DELTA], out[N_DELTA:2 * N_DELTA], bool(out[2 * N_DELTA])
+
+    def check_division(self, n: int, seed: int = 1, samples: bool = False):
+        out = ctypes.c_int64(-1)
+        first = np.zeros(16)
+        check(library().ct_check_division(self.handle, int(n), int(seed), ctypes.byref(out),
+                                          ptr(first)))
+        return (int(out.value), first.reshape(4, 4)) if samples else int(out.value)
 
     # -- batched replay searches ----------------------------------------------
     def launch_profile(self, params: SearchParams, seeds: "SeedWords", n_reps: int):

@@ -276,9 +276,53 @@ __global__ void k_analyze_react(const double* c, int gen, int64_t cores, int64_t
     out[2 * N_COMP] = deg ? 1.0 : 0.0;
 }
 
+// Self-check of dvd_fast against __ddiv_rn on generated operand pairs:
+// raw random bit patterns (all classes incl. zero/denormal/inf/nan), small
+// integers (exact quotients), and Eq. 16-shaped operands d*(c-p) / (c+p).
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull; x ^= x >> 27; x *= 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+__global__ void k_check_division(int64_t n, uint64_t seed, unsigned long long* bad,
+                                 double* first) {
+    unsigned long long local = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t h1 = mix64(seed ^ (uint64_t)i * 0x9e3779b97f4a7c15ull);
+        uint64_t h2 = mix64(h1 + 0x632be59bd9b4e019ull);
+        double a, b;
+        switch ((int)(h1 & 3)) {
+        case 0: a = bitsd(h1); b = bitsd(h2); break;
+        case 1: a = (double)(int64_t)(h1 % 20001) - 10000.0; b = (double)(int64_t)(h2 % 2001) - 1000.0; break;
+        case 2: {
+            double c = (double)(h1 >> 11) * 0x1.0p-53 * 1e6, p = (double)(h2 >> 11) * 0x1.0p-53 * 1e6;
+            double d = (double)((h1 ^ h2) >> 11) * 0x1.0p-52 - 1.0;
+            a = mul(d, sub(c, p)); b = add(c, p); break; }
+        default: {
+            double c = (double)(h1 % 100000), p = (double)(h2 % 100000) + 1.0;
+            double d = (double)((h1 ^ h2) >> 11) * 0x1.0p-52 - 1.0;
+            a = mul(d, sub(c, p)); b = add(c, p); break; }
+        }
+        double x = dvd_fast(a, b), y = __ddiv_rn(a, b);
+        bool same = (dbits(x) == dbits(y)) || (x != x && y != y);
+        if (!same) {
+            int cat = (int)(h1 & 3);
+            if (atomicAdd(&bad[1 + cat], 1ull) == 0ull) {
+                first[4 * cat + 0] = a; first[4 * cat + 1] = b;
+                first[4 * cat + 2] = x; first[4 * cat + 3] = y;
+            }
+            ++local;
+        }
+    }
+    if (local) atomicAdd(bad, local);
+}
+
 int rows_for(int64_t n) {
+    // ~sqrt(N)/32 rows balances the two scans of a draw; at least 2 rows so
+    // that each lane sums two weights per tile before the warp reduction
     int rows = (int)std::lround(std::sqrt((double)n) / 32.0);
-    return std::max(1, rows);
+    return std::max(2, rows);
 }
 
 int grid_for(int64_t n, int threads) {
@@ -589,6 +633,27 @@ int ct_analyze_react(ct_ctx* ctx, const double* counters23, int32_t generation, 
     CT_CUDA(cudaGetLastError());
     CT_CUDA(cudaMemcpyAsync(out37, dout, sizeof(double) * (2 * CT_N_DELTA + 1), cudaMemcpyDeviceToHost, s));
     CT_CUDA(cudaStreamSynchronize(s));
+    return CT_OK;
+}
+
+int ct_check_division(ct_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches,
+                      double* first_bad) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!mismatches || n < 0) return fail(CT_ERR_VALUE, "bad arguments");
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(ctx->pick.ensure(5));
+    CT_CUDA(ctx->part_d.ensure(16));
+    CT_CUDA(cudaMemsetAsync(ctx->pick.p, 0, 5 * sizeof(long long), s));
+    CT_CUDA(cudaMemsetAsync(ctx->part_d.p, 0, 16 * sizeof(double), s));
+    k_check_division<<<ctx->sm_count * 8, 256, 0, s>>>(n, seed, (unsigned long long*)ctx->pick.p,
+                                                        ctx->part_d.p);
+    CT_CUDA(cudaGetLastError());
+    long long out[5] = {0, 0, 0, 0, 0};
+    CT_CUDA(cudaMemcpyAsync(out, ctx->pick.p, sizeof(out), cudaMemcpyDeviceToHost, s));
+    if (first_bad)
+        CT_CUDA(cudaMemcpyAsync(first_bad, ctx->part_d.p, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
+    *mismatches = out[0];
     return CT_OK;
 }
 

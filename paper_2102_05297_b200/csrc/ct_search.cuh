@@ -73,6 +73,8 @@ struct __align__(16) Ctl {
     int red_pos[32];
     int red_bad[32];
     ActiveTerm act[MAX_ACTIVE];
+    double cnt[N_REQ];
+    double pv[N_COMP];
     double s_max, s_min;
     int n_act;
     int done;
@@ -85,7 +87,7 @@ __device__ __forceinline__ bool bit_get(const uint32_t* b, int64_t i) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
+__global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_search(const SearchArgs a) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ Ctl ctl;
@@ -122,37 +124,50 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
         __syncthreads();
 
         for (int it = 0; it < a.outer; ++it) {
-            // ---------------- profile step, expert system (thread 0) ----------
-            if (tid == 0) {
-                if (!a.has_record[c_prof]) {
-                    st = CT_STATUS_ERROR; err = -4; ctl.done = 1;
-                    if (ns < a.max_steps) out_idx[ns] = (int32_t)c_prof;   // failing index
+            // ---------------- profile step, expert system (warp 0) ------------
+            if (warp == 0) {
+                // the profile's counters and p values arrive with one parallel
+                // load per lane; lane 0 then runs the scalar expert system
+                const int64_t cp = __shfl_sync(FULL, (long long)c_prof, 0);
+                if (lane < N_REQ) ctl.cnt[lane] = a.counters[(size_t)cp * N_REQ + lane];
+                if (lane < N_COMP) {
+                    const int col = a.delta_col[lane];
+                    ctl.pv[lane] = (col >= 0) ? a.table[(size_t)col * a.ld + cp] : 0.0;
                 }
-                else {
-                    out_idx[ns] = (int32_t)c_prof; out_prof[ns] = 1; ++ns;
-                    uint32_t m = 1u << (c_prof & 31);
-                    if (!(expl[c_prof >> 5] & m)) { expl[c_prof >> 5] |= m; ++n_expl; }
-                    if (a.stop_bits && bit_get(a.stop_bits, c_prof)) { st = CT_STATUS_STOPPED; ctl.done = 1; }
-                }
-                if (!ctl.done) {
-                    double b[N_COMP], d[N_COMP];
-                    analyze(a.counters + (size_t)c_prof * N_REQ, a.generation, a.cores,
-                            a.threads[c_prof], b);
-                    react(b, a.inst_reaction, a.issue_sign, d);
-                    int na = 0;
-                    for (int k = 0; k < N_COMP; ++k) {
-                        if (d[k] == 0.0 || a.delta_col[k] < 0) continue;
-                        double pv = a.table[(size_t)a.delta_col[k] * a.ld + c_prof];
-                        if (pv == 0.0) continue;
-                        ctl.act[na].col = a.delta_col[k]; ctl.act[na].d = d[k]; ctl.act[na].p = pv;
-                        ++na;
+                const bool rec_ok = a.has_record[cp] != 0;
+                const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cp);
+                const int64_t thr = a.threads[cp];
+                __syncwarp();
+                if (lane == 0) {
+                    if (!rec_ok) {
+                        st = CT_STATUS_ERROR; err = -4; ctl.done = 1;
+                        if (ns < a.max_steps) out_idx[ns] = (int32_t)cp;   // failing index
+                    } else {
+                        out_idx[ns] = (int32_t)cp; out_prof[ns] = 1; ++ns;
+                        uint32_t m = 1u << (cp & 31);
+                        if (!(expl[cp >> 5] & m)) { expl[cp >> 5] |= m; ++n_expl; }
+                        if (is_stop) { st = CT_STATUS_STOPPED; ctl.done = 1; }
                     }
-                    ctl.n_act = na;
-                    if (n_expl >= N) { st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
-                    else {
-                        unsigned long long pool = (unsigned long long)(N - n_expl);
-                        scored += pool; ++outers;
-                        abytes += pool * (8ull * (unsigned long long)na + 16ull);
+                    if (!ctl.done) {
+                        double b[N_COMP], d[N_COMP];
+                        analyze(ctl.cnt, a.generation, a.cores, thr, b);
+                        react(b, a.inst_reaction, a.issue_sign, d);
+                        int na = 0;
+                        for (int k = 0; k < N_COMP; ++k) {
+                            const double pv = ctl.pv[k];
+                            if (d[k] == 0.0 || a.delta_col[k] < 0 || pv == 0.0) continue;
+                            ctl.act[na].col = a.delta_col[k]; ctl.act[na].p = pv;
+                            // literal sign: (-d)(c - p) == d(p - c) exactly
+                            ctl.act[na].d = a.literal_sign ? -d[k] : d[k];
+                            ++na;
+                        }
+                        ctl.n_act = na;
+                        if (n_expl >= N) { st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
+                        else {
+                            unsigned long long pool = (unsigned long long)(N - n_expl);
+                            scored += pool; ++outers;
+                            abytes += pool * (8ull * (unsigned long long)na + 16ull);
+                        }
                     }
                 }
             }
@@ -161,27 +176,26 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
 
             // ---------------- Eq. 16 raw scores (all threads) ------------------
             const int n_act = ctl.n_act;
-            const bool lit = a.literal_sign != 0;
             double lmax = -INFINITY, lmin = INFINITY;
             for (int64_t base = tid; base < N; base += 4LL * NT) {
                 double acc[4];
                 bool in[4];
+                int64_t el[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     int64_t e = base + (int64_t)u * NT;
                     in[u] = (e < N) && !bit_get(expl, e);
+                    el[u] = (e < N) ? e : N - 1;      // clamped: branch-free loads
                     acc[u] = 0.0;
                 }
                 for (int k = 0; k < n_act; ++k) {
-                    const ActiveTerm t = ctl.act[k];
-                    const double* col = a.table + (size_t)t.col * a.ld;
+                    const double d = ctl.act[k].d, pv = ctl.act[k].p;
+                    const double* col = a.table + (size_t)ctl.act[k].col * a.ld;
+                    double c[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (in[u]) {
-                            double c = __ldg(col + base + (int64_t)u * NT);
-                            acc[u] = add(acc[u], raw_term(c, t, lit));
-                        }
-                    }
+                    for (int u = 0; u < 4; ++u) c[u] = __ldg(col + el[u]);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] = add(acc[u], raw_term_nb(c[u], d, pv));
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -256,7 +270,13 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
                         chosen = __shfl_sync(FULL, (long long)chosen, 0);
                     }
                     if (lane == 0) ++draws;
-                    if (chosen < 0 || chosen >= N || !a.has_record[chosen]) {
+                    const bool in_range = chosen >= 0 && chosen < N;
+                    const int64_t cs = in_range ? chosen : 0;
+                    // the replay lookups of the draw, issued together
+                    const bool rec_ok = in_range && a.has_record[cs];
+                    const double rt = a.runtime[cs];
+                    const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cs);
+                    if (!rec_ok) {
                         if (lane == 0) {
                             st = CT_STATUS_ERROR; err = -4;
                             if (ns < a.max_steps) out_idx[ns] = (int32_t)chosen;
@@ -273,13 +293,12 @@ __global__ void __launch_bounds__(NT) k_profile_search(const SearchArgs a) {
                     }
                     total -= f;
                     --positive;
-                    double rt = a.runtime[chosen];
                     if (lane == 0) {
                         out_idx[ns] = (int32_t)chosen; out_prof[ns] = 0; ++ns;
                         uint32_t m = 1u << (chosen & 31);
                         if (!(expl[chosen >> 5] & m)) { expl[chosen >> 5] |= m; ++n_expl; }
                     }
-                    if (a.stop_bits && bit_get(a.stop_bits, chosen)) {
+                    if (is_stop) {
                         if (lane == 0) st = CT_STATUS_STOPPED;
                         done = 1; break;
                     }

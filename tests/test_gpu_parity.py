@@ -225,3 +225,10 @@ def test_large_space_properties():
     idx2, _, nst2, _, _, _ = ctx.fetch(3)
     for r in range(3):
         assert idx2[r, :nst2[r]].tolist() == res.step_index[3 + r, :res.n_steps[3 + r]].tolist()
+
+
+def test_inline_division_is_ddiv_rn():
+    """dvd_fast (ct_hd.cuh) == __ddiv_rn bit for bit on 2^28 operand pairs."""
+    from paper_2102_05297_b200 import _native
+    ctx = _native.context(0)
+    assert ctx.check_division(1 << 28, seed=12345) == 0
