@@ -32,65 +32,79 @@ CT_HD double share(double part, double total) { return total > 0.0 ? dvd(part, t
 // Python max()/min() keep the first of equal arguments
 CT_HD double pymax(double a, double b) { return b > a ? b : a; }
 
+CT_HD bool degenerate_of(const double* c) {
+    return c[INST_EXE] <= 0.0 || c[WARP_E] <= 0.0 || c[WARP_NP_E] <= 0.0;
+}
+
+// Component k of analyze() (COMPONENT_NAMES index), clamped.  One function
+// per component lets one warp evaluate the 18 components on 18 lanes while
+// analyze() below, the scalar form, calls the very same code.
+CT_HD double analyze_component(const double* c, int k, int generation, int64_t cores,
+                               int64_t global_threads, bool degenerate) {
+    double v;
+    if (k < B_TEX) {                                  // memory read/write pairs
+        const int rd = (k < 2) ? DRAM_RT : (k < 4 ? L2_RT : SHR_LT);
+        const int util = (k < 2) ? DRAM_U : (k < 4 ? L2_U : SHR_U);
+        const double tot = add(c[rd], c[rd + 1]);
+        v = dvd(mul(share(c[rd + (k & 1)], tot), c[util]), 10.0);
+    } else if (k == B_TEX) {
+        v = dvd(c[TEX_U], 10.0);
+    } else if (k == B_LOCAL) {
+        const double busiest = pymax(pymax(c[DRAM_U], c[L2_U]), c[TEX_U]);
+        v = dvd(mul(dvd(c[LOC_O], 100.0), busiest), 10.0);
+    } else if (k <= B_ISSUE) {                        // instruction classes
+        if (degenerate) return 0.0;
+        const double fitted = mul(mul(mul(32.0, c[INST_EXE]), dvd(100.0, c[WARP_E])),
+                                  dvd(100.0, c[WARP_NP_E]));
+        if (k < B_ISSUE) {
+            double util;
+            if (generation == 0) {
+                util = dvd(c[INST_ISSUE_U], 100.0);
+            } else {
+                const double u = dvd(c[INST_ISSUE_U], 50.0);
+                util = (u < 1.0) ? u : 1.0;           // min(1.0, u)
+            }
+            v = mul(dvd(c[INST_F32 + (k - B_FP32)], fitted), util);
+        } else {
+            double util_max = dvd(c[INST_F32], fitted);
+            for (int j = 1; j < 7; ++j) util_max = pymax(util_max, dvd(c[INST_F32 + j], fitted));
+            v = dvd(mul(util_max, sub(100.0, c[INST_ISSUE_U])), 100.0);
+        }
+    } else if (k == B_SM) {
+        v = dvd(sub(100.0, c[SM_E_]), 100.0);
+    } else {
+        const double sat = (double)(cores * 5);
+        const double par = dvd(sub(sat, (double)global_threads), sat);
+        v = par > 0.0 ? par : 0.0;                    // max(0.0, par)
+    }
+    return clamp01(v);
+}
+
 // analyze(): c = 23 counters, generation 0 = pre_volta, 1 = volta_plus.
 // Returns the degenerate_instructions flag.
 CT_HD bool analyze(const double* c, int generation, int64_t cores, int64_t global_threads,
                    double* b) {
-    double rw = add(c[DRAM_RT], c[DRAM_WT]);
-    b[B_DRAM_READ] = dvd(mul(share(c[DRAM_RT], rw), c[DRAM_U]), 10.0);
-    b[B_DRAM_WRITE] = dvd(mul(share(c[DRAM_WT], rw), c[DRAM_U]), 10.0);
-    double l2 = add(c[L2_RT], c[L2_WT]);
-    b[B_L2_READ] = dvd(mul(share(c[L2_RT], l2), c[L2_U]), 10.0);
-    b[B_L2_WRITE] = dvd(mul(share(c[L2_WT], l2), c[L2_U]), 10.0);
-    double sh = add(c[SHR_LT], c[SHR_WT]);
-    b[B_SHARED_READ] = dvd(mul(share(c[SHR_LT], sh), c[SHR_U]), 10.0);
-    b[B_SHARED_WRITE] = dvd(mul(share(c[SHR_WT], sh), c[SHR_U]), 10.0);
-    b[B_TEX] = dvd(c[TEX_U], 10.0);
-    double busiest = pymax(pymax(c[DRAM_U], c[L2_U]), c[TEX_U]);
-    b[B_LOCAL] = dvd(mul(dvd(c[LOC_O], 100.0), busiest), 10.0);
-
-    bool degenerate = c[INST_EXE] <= 0.0 || c[WARP_E] <= 0.0 || c[WARP_NP_E] <= 0.0;
-    if (degenerate) {
-        for (int k = B_FP32; k <= B_ISSUE; ++k) b[k] = 0.0;
-    } else {
-        double fitted = mul(mul(mul(32.0, c[INST_EXE]), dvd(100.0, c[WARP_E])),
-                            dvd(100.0, c[WARP_NP_E]));
-        double util;
-        if (generation == 0) {
-            util = dvd(c[INST_ISSUE_U], 100.0);
-        } else {
-            double u = dvd(c[INST_ISSUE_U], 50.0);
-            util = (u < 1.0) ? u : 1.0;                       // min(1.0, u)
-        }
-        double util_max = 0.0;
-        for (int k = 0; k < 7; ++k) {
-            double ratio = dvd(c[INST_F32 + k], fitted);
-            b[B_FP32 + k] = mul(ratio, util);
-            util_max = (k == 0) ? ratio : pymax(util_max, ratio);
-        }
-        b[B_ISSUE] = dvd(mul(util_max, sub(100.0, c[INST_ISSUE_U])), 100.0);
-    }
-    b[B_SM] = dvd(sub(100.0, c[SM_E_]), 100.0);
-    double sat = (double)(cores * 5);
-    double par = dvd(sub(sat, (double)global_threads), sat);
-    b[B_PARAL] = par > 0.0 ? par : 0.0;                       // max(0.0, par)
-    for (int k = 0; k < N_COMP; ++k) b[k] = clamp01(b[k]);
+    const bool degenerate = degenerate_of(c);
+    for (int k = 0; k < N_COMP; ++k)
+        b[k] = analyze_component(c, k, generation, cores, global_threads, degenerate);
     return degenerate;
 }
 
-// react(): delta[k] for the k-th key of react()'s insertion order.
-CT_HD void react(const double* b, double inst_reaction, double issue_sign, double* delta) {
-    for (int k = 0; k <= B_LOCAL; ++k) delta[k] = clamp_signed(-b[k]);
-    for (int k = B_FP32; k <= B_ISSUE; ++k) {
-        double v = b[k];
-        double scaled = (v <= inst_reaction)
+// react() value of key k (react()'s insertion order == component order).
+CT_HD double react_component(double b, int k, double inst_reaction, double issue_sign) {
+    if (k <= B_LOCAL) return clamp_signed(-b);
+    if (k <= B_ISSUE) {
+        double scaled = (b <= inst_reaction)
                             ? 0.0
-                            : dvd(-sub(v, inst_reaction), sub(1.0, inst_reaction));
+                            : dvd(-sub(b, inst_reaction), sub(1.0, inst_reaction));
         if (k == B_ISSUE) scaled = mul(issue_sign, fabs(scaled));
-        delta[k] = clamp_signed(scaled);
+        return clamp_signed(scaled);
     }
-    delta[B_SM] = clamp_signed(b[B_SM]);
-    delta[B_PARAL] = clamp_signed(b[B_PARAL]);
+    return clamp_signed(b);                           // SM_E, GLOBAL_THREADS
+}
+
+CT_HD void react(const double* b, double inst_reaction, double issue_sign, double* delta) {
+    for (int k = 0; k < N_COMP; ++k) delta[k] = react_component(b[k], k, inst_reaction, issue_sign);
 }
 
 }  // namespace ct

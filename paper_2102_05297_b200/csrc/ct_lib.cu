@@ -62,6 +62,7 @@ struct ct_ctx {
     // prediction table (column-major)
     DevBuf<double> table;
     int64_t n = 0;
+    int64_t ld = 0;          // padded column stride
     int32_t n_counters = 0;
     // space assignments (row-major n x P)
     DevBuf<double> assign;
@@ -304,8 +305,10 @@ __global__ void k_check_division(int64_t n, uint64_t seed, unsigned long long* b
             double d = (double)((h1 ^ h2) >> 11) * 0x1.0p-52 - 1.0;
             a = mul(d, sub(c, p)); b = add(c, p); break; }
         }
-        double x = dvd_fast(a, b), y = __ddiv_rn(a, b);
+        double x = dvd_fast(a, b), y = __ddiv_rn(a, b), z = dvd_term(a, b);
         bool same = (dbits(x) == dbits(y)) || (x != x && y != y);
+        // dvd_term: equal value (a zero's sign is unspecified)
+        same = same && ((dbits(z) == dbits(y)) || (z != z && y != y) || (z == 0.0 && y == 0.0));
         if (!same) {
             int cat = (int)(h1 & 3);
             if (atomicAdd(&bad[1 + cat], 1ull) == 0ull) {
@@ -460,14 +463,19 @@ int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
     if (!matrix || n < 1 || c < 1) return fail(CT_ERR_VALUE, "table needs n >= 1 and counters >= 1");
     if (n > INT32_MAX) return fail(CT_ERR_VALUE, "spaces above 2^31-1 configurations are not supported");
     // transpose to column-major on the host (one pass over the borrowed matrix)
-    std::vector<double> colmajor((size_t)n * c);
+    // columns padded with zeros to a multiple of 2048 configurations: the
+    // search kernel's unrolled loads (4 x up to 512 threads) never need a
+    // bounds test
+    const int64_t ld = (n + 2047) / 2048 * 2048;
+    std::vector<double> colmajor((size_t)ld * c, 0.0);
     for (int64_t i = 0; i < n; ++i)
-        for (int32_t j = 0; j < c; ++j) colmajor[(size_t)j * n + i] = matrix[(size_t)i * c + j];
-    CT_CUDA(ctx->table.ensure((size_t)n * c));
-    CT_CUDA(cudaMemcpyAsync(ctx->table.p, colmajor.data(), sizeof(double) * n * c,
+        for (int32_t j = 0; j < c; ++j) colmajor[(size_t)j * ld + i] = matrix[(size_t)i * c + j];
+    CT_CUDA(ctx->table.ensure((size_t)ld * c));
+    CT_CUDA(cudaMemcpyAsync(ctx->table.p, colmajor.data(), sizeof(double) * ld * c,
                             cudaMemcpyHostToDevice, ctx->stream));
     CT_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->n = n;
+    ctx->ld = ld;
     ctx->n_counters = c;
     return CT_OK;
 }
@@ -555,7 +563,7 @@ int ct_score(ct_ctx* ctx, int64_t profile, const int32_t* cols, const double* va
     }
     ScoreSingleArgs a;
     std::memset(&a, 0, sizeof(a));
-    a.table = ctx->table.p; a.ld = n; a.n = n; a.profile = profile; a.n_delta = n_delta;
+    a.table = ctx->table.p; a.ld = ctx->ld; a.n = n; a.profile = profile; a.n_delta = n_delta;
     for (int k = 0; k < n_delta; ++k) { a.cols[k] = cols[k]; a.vals[k] = vals[k]; }
     a.explored = ctx->mask_a.p; a.scoreable = topk ? ctx->mask_b.p : nullptr;
     a.literal_sign = literal_sign; a.raw = ctx->vec_a.p;
@@ -690,7 +698,7 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
 
     SearchArgs a;
     std::memset(&a, 0, sizeof(a));
-    a.table = ctx->table.p; a.ld = n; a.n = n;
+    a.table = ctx->table.p; a.ld = ctx->ld; a.n = n;
     a.runtime = ctx->runtime.p; a.threads = ctx->threads.p; a.counters = ctx->counters.p;
     a.has_record = ctx->has_record.p; a.stop_bits = prm->use_stop ? ctx->stop_bits.p : nullptr;
     a.outer = prm->outer_iterations; a.inner = prm->inner_steps;

@@ -125,20 +125,38 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
 
         for (int it = 0; it < a.outer; ++it) {
             // ---------------- profile step, expert system (warp 0) ------------
+            // One lane per counter fetches the profile's replayed counters and
+            // one lane per delta key its predicted value p; the 18 bottleneck
+            // components and their reactions are then evaluated on 18 lanes
+            // (the same per-component code as the scalar analyze()/react())
+            // and the active terms compacted in react() order with a ballot.
             if (warp == 0) {
-                // the profile's counters and p values arrive with one parallel
-                // load per lane; lane 0 then runs the scalar expert system
                 const int64_t cp = __shfl_sync(FULL, (long long)c_prof, 0);
                 if (lane < N_REQ) ctl.cnt[lane] = a.counters[(size_t)cp * N_REQ + lane];
-                if (lane < N_COMP) {
-                    const int col = a.delta_col[lane];
-                    ctl.pv[lane] = (col >= 0) ? a.table[(size_t)col * a.ld + cp] : 0.0;
-                }
+                const int col = (lane < N_COMP) ? a.delta_col[lane] : -1;
+                const double pv = (col >= 0) ? a.table[(size_t)col * a.ld + cp] : 0.0;
                 const bool rec_ok = a.has_record[cp] != 0;
                 const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cp);
                 const int64_t thr = a.threads[cp];
                 __syncwarp();
+                double dk = 0.0;
+                if (lane < N_COMP) {
+                    const double bk = analyze_component(ctl.cnt, lane, a.generation, a.cores, thr,
+                                                        degenerate_of(ctl.cnt));
+                    dk = react_component(bk, lane, a.inst_reaction, a.issue_sign);
+                }
+                const bool act = (lane < N_COMP) && dk != 0.0 && col >= 0 && pv != 0.0;
+                const unsigned amask = __ballot_sync(FULL, act);
+                if (act) {
+                    const int slot = __popc(amask & ((1u << lane) - 1u));
+                    ctl.act[slot].col = col;
+                    ctl.act[slot].p = pv;
+                    // literal sign: (-d)(c - p) == d(p - c) exactly
+                    ctl.act[slot].d = a.literal_sign ? -dk : dk;
+                }
                 if (lane == 0) {
+                    const int na = __popc(amask);
+                    ctl.n_act = na;
                     if (!rec_ok) {
                         st = CT_STATUS_ERROR; err = -4; ctl.done = 1;
                         if (ns < a.max_steps) out_idx[ns] = (int32_t)cp;   // failing index
@@ -147,22 +165,7 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                         uint32_t m = 1u << (cp & 31);
                         if (!(expl[cp >> 5] & m)) { expl[cp >> 5] |= m; ++n_expl; }
                         if (is_stop) { st = CT_STATUS_STOPPED; ctl.done = 1; }
-                    }
-                    if (!ctl.done) {
-                        double b[N_COMP], d[N_COMP];
-                        analyze(ctl.cnt, a.generation, a.cores, thr, b);
-                        react(b, a.inst_reaction, a.issue_sign, d);
-                        int na = 0;
-                        for (int k = 0; k < N_COMP; ++k) {
-                            const double pv = ctl.pv[k];
-                            if (d[k] == 0.0 || a.delta_col[k] < 0 || pv == 0.0) continue;
-                            ctl.act[na].col = a.delta_col[k]; ctl.act[na].p = pv;
-                            // literal sign: (-d)(c - p) == d(p - c) exactly
-                            ctl.act[na].d = a.literal_sign ? -d[k] : d[k];
-                            ++na;
-                        }
-                        ctl.n_act = na;
-                        if (n_expl >= N) { st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
+                        else if (n_expl >= N) { st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
                         else {
                             unsigned long long pool = (unsigned long long)(N - n_expl);
                             scored += pool; ++outers;
@@ -175,34 +178,28 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
             if (ctl.done) break;
 
             // ---------------- Eq. 16 raw scores (all threads) ------------------
+            // Columns are padded to a multiple of 4*NT, so the four loads of an
+            // iteration use one base pointer and immediate offsets.
             const int n_act = ctl.n_act;
             double lmax = -INFINITY, lmin = INFINITY;
             for (int64_t base = tid; base < N; base += 4LL * NT) {
-                double acc[4];
-                bool in[4];
-                int64_t el[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    int64_t e = base + (int64_t)u * NT;
-                    in[u] = (e < N) && !bit_get(expl, e);
-                    el[u] = (e < N) ? e : N - 1;      // clamped: branch-free loads
-                    acc[u] = 0.0;
-                }
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
                 for (int k = 0; k < n_act; ++k) {
                     const double d = ctl.act[k].d, pv = ctl.act[k].p;
-                    const double* col = a.table + (size_t)ctl.act[k].col * a.ld;
+                    const double* col = a.table + (size_t)ctl.act[k].col * a.ld + base;
                     double c[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) c[u] = __ldg(col + el[u]);
+                    for (int u = 0; u < 4; ++u) c[u] = __ldg(col + u * NT);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) acc[u] = add(acc[u], raw_term_nb(c[u], d, pv));
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    int64_t e = base + (int64_t)u * NT;
+                    const int64_t e = base + (int64_t)u * NT;
                     if (e < N) {
-                        w[e] = in[u] ? acc[u] : 0.0;
-                        if (in[u]) { lmax = nmax(lmax, acc[u]); lmin = nmin(lmin, acc[u]); }
+                        const bool in = !bit_get(expl, e);
+                        w[e] = in ? acc[u] : 0.0;
+                        if (in) { lmax = nmax(lmax, acc[u]); lmin = nmin(lmin, acc[u]); }
                     }
                 }
             }
@@ -210,16 +207,13 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
             lmin = warp_min(lmin);
             if (lane == 0) { ctl.red_max[warp] = lmax; ctl.red_min[warp] = lmin; }
             __syncthreads();
-            if (tid == 0) {
-                double mx = ctl.red_max[0], mn = ctl.red_min[0];
-                for (int i = 1; i < NW; ++i) { mx = nmax(mx, ctl.red_max[i]); mn = nmin(mn, ctl.red_min[i]); }
-                ctl.s_max = mx; ctl.s_min = mn;
-            }
-            __syncthreads();
 
             // ---------------- Eq. 17 weights + exact tile totals ---------------
             {
-                const double smax = ctl.s_max, smin = ctl.s_min, gamma = a.gamma;
+                double smax = ctl.red_max[0], smin = ctl.red_min[0];
+#pragma unroll
+                for (int i = 1; i < NW; ++i) { smax = nmax(smax, ctl.red_max[i]); smin = nmin(smin, ctl.red_min[i]); }
+                const double gamma = a.gamma;
                 u128 wtot = 0;
                 int pos = 0, bad = 0;
                 for (int t = warp; t < a.ntiles; t += NW) {
@@ -252,6 +246,13 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                 for (int i = 0; i < NW; ++i) {
                     total += ctl.red_tot[i]; positive += ctl.red_pos[i]; bad |= ctl.red_bad[i];
                 }
+                // each lane owns a contiguous chunk of tiles; its inclusive
+                // prefix is kept across the draws and patched after a zeroing
+                const int cpl = (a.ntiles + 31) >> 5;
+                const int t0 = lane * cpl, t1 = min(t0 + cpl, a.ntiles);
+                u128 mine = 0;
+                for (int t = t0; t < t1; ++t) mine += tile_tot[t];
+                u128 lane_pref = warp_incl_scan(mine, lane);
                 int done = 0;
                 if (bad) { if (lane == 0) { st = CT_STATUS_ERROR; err = -7; } done = 1; }
                 double t_best = INFINITY;
@@ -260,10 +261,11 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                     double u = 0.0;
                     if (lane == 0) u = rng.next_double();
                     u = __shfl_sync(FULL, u, 0);
-                    double total_d = fx_to_double(total);
-                    double r = mul(u, total_d);
-                    u128 r_fx = floor_fx(r);
-                    Located pk = warp_locate(tile_tot, a.ntiles, w, N, a.rows, r_fx, lane);
+                    const double total_d = fx_to_double(total);
+                    const double r = mul(u, total_d);
+                    const u128 r_fx = floor_fx(r);
+                    Located pk = warp_locate_pref(tile_tot, t0, t1, lane_pref, mine, w, N, a.rows,
+                                                  r_fx, lane);
                     int64_t chosen = pk.idx;
                     if (!certify(pk, r_fx, total_d, N)) {
                         if (lane == 0) { chosen = sequential_select(w, N, u); ++uncert; }
@@ -283,14 +285,17 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                         }
                         done = 1; break;
                     }
-                    // zero the drawn weight: exact prefix stays exact
+                    // zero the drawn weight: the exact prefix stays exact
                     u128 f = 0;
                     to_fx(w[chosen], &f);
+                    const int tc = (int)(chosen / tile_len);
                     __syncwarp();
                     if (lane == 0) {
                         w[chosen] = 0.0;
-                        tile_tot[chosen / tile_len] -= f;
+                        tile_tot[tc] -= f;
                     }
+                    if (tc >= t0 && tc < t1) mine -= f;
+                    if (tc < t1) lane_pref -= f;
                     total -= f;
                     --positive;
                     if (lane == 0) {

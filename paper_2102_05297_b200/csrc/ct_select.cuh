@@ -22,35 +22,14 @@ struct Located {
     u128 wfx;         // fixed-point weight of idx
 };
 
-// Executed by one full warp.  Tiles are tile_len = 32 * rows consecutive
-// elements; tile_tot[t] is the exact sum of tile t.
-__device__ __forceinline__ Located warp_locate(const u128* tile_tot, int ntiles,
-                                               const double* w, int64_t n, int rows,
-                                               u128 r_fx, int lane) {
+// In-tile part of a draw (one full warp): rows of 32 consecutive elements,
+// one exact warp scan per row until the row containing r is found.  carry
+// is the exact prefix before the tile.
+__device__ __forceinline__ Located warp_locate_rows(int tile, u128 carry, const double* w,
+                                                    int64_t n, int rows, u128 r_fx, int lane) {
     Located out;
     out.idx = -1; out.tile = -1; out.before = 0; out.wfx = 0;
-    int cpl = (ntiles + 31) >> 5;
-    int t0 = lane * cpl;
-    int t1 = min(t0 + cpl, ntiles);
-    u128 mine = 0;
-    for (int t = t0; t < t1; ++t) mine += tile_tot[t];
-    u128 incl = warp_incl_scan(mine, lane);
-    unsigned bal = __ballot_sync(FULL, incl > r_fx);
-    if (bal == 0) return out;
-    int L = __ffs(bal) - 1;
-    int tile = -1;
-    u128 carry = incl - mine;
-    if (lane == L) {
-        for (int t = t0; t < t1; ++t) {
-            u128 nxt = carry + tile_tot[t];
-            if (nxt > r_fx) { tile = t; break; }
-            carry = nxt;
-        }
-    }
-    tile = __shfl_sync(FULL, tile, L);
-    carry = shfl_u128(carry, L);
-    const int64_t tile_len = 32LL * rows;
-    const int64_t base = (int64_t)tile * tile_len;
+    const int64_t base = (int64_t)tile * (32LL * rows);
     for (int j = 0; j < rows; ++j) {
         int64_t e = base + 32LL * j + lane;
         double wv = (e < n) ? w[e] : 0.0;
@@ -70,6 +49,47 @@ __device__ __forceinline__ Located warp_locate(const u128* tile_tot, int ntiles,
         carry += tot;
     }
     return out;
+}
+
+// Tile part with a per-lane inclusive prefix kept by the caller: lane L owns
+// tiles [t0, t1) (a contiguous chunk), mine is their exact sum and
+// lane_pref the inclusive prefix over lanes.  A ballot finds the lane whose
+// chunk holds r, that lane walks its chunk.
+__device__ __forceinline__ Located warp_locate_pref(const u128* tile_tot, int t0, int t1,
+                                                    u128 lane_pref, u128 mine, const double* w,
+                                                    int64_t n, int rows, u128 r_fx, int lane) {
+    unsigned bal = __ballot_sync(FULL, lane_pref > r_fx);
+    if (bal == 0) {
+        Located out;
+        out.idx = -1; out.tile = -1; out.before = 0; out.wfx = 0;
+        return out;
+    }
+    int L = __ffs(bal) - 1;
+    int tile = -1;
+    u128 carry = lane_pref - mine;
+    if (lane == L) {
+        for (int t = t0; t < t1; ++t) {
+            u128 nxt = carry + tile_tot[t];
+            if (nxt > r_fx) { tile = t; break; }
+            carry = nxt;
+        }
+    }
+    tile = __shfl_sync(FULL, tile, L);
+    carry = shfl_u128(carry, L);
+    return warp_locate_rows(tile, carry, w, n, rows, r_fx, lane);
+}
+
+// Stateless form (single-call API): the lane prefix is built on the spot.
+__device__ __forceinline__ Located warp_locate(const u128* tile_tot, int ntiles,
+                                               const double* w, int64_t n, int rows,
+                                               u128 r_fx, int lane) {
+    int cpl = (ntiles + 31) >> 5;
+    int t0 = lane * cpl;
+    int t1 = min(t0 + cpl, ntiles);
+    u128 mine = 0;
+    for (int t = t0; t < t1; ++t) mine += tile_tot[t];
+    u128 incl = warp_incl_scan(mine, lane);
+    return warp_locate_pref(tile_tot, t0, t1, incl, mine, w, n, rows, r_fx, lane);
 }
 
 // Certification: |c_seq(i) - S(i)| + |r_ref - r| <= (2N + 7) 2^-53 T for the
