@@ -94,6 +94,15 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)["k_profile_search"]
+        return int(t["dram_bytes_per_launch"]), t["source"]
+    except Exception:
+        return None, None
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -238,6 +247,7 @@ def run_ours(args):
     value = world * configs_per_step * args.steps / t_total
     per_launch = t_total / args.steps
     hbm, peak_kind = _peaks()
+    traffic, traffic_src = _traffic()
     achieved_gbs = bytes_per_step / per_launch / 1e9
     print(f"[bench] rank {rank}: {configs_per_step} configs/step, {per_launch * 1e3:.3f} ms/step, "
           f"{value:.4g} configs/s, {achieved_gbs:.1f} GB/s algorithmic, "
@@ -309,7 +319,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "api": "harness.simulate"},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm, "traffic": None,
+                     "frac": achieved_gbs / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": bytes_per_step,
                      "note": "8*C_used+16 B per scored config (BASELINE.md); table is "
