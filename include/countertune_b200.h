@@ -196,6 +196,33 @@ int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled,
 int ct_result_device_ptrs(ct_ctx* ctx, void** step_index, void** step_profiled,
                           void** n_steps, void** status);
 
+/* ---- on-device aggregation of the last launch (harness.py:187-244) ------
+ * The ConvergenceReport statistics computed where the trajectories live, with
+ * the reference's float operations in its order (sequential sums over
+ * repetitions), so that reports stay byte-identical while only O(R + steps)
+ * numbers cross PCIe.  Repetitions split over several contexts are chained:
+ * the *_init arrays (nullable = zeros) carry the partial sums of the
+ * contexts holding the earlier repetitions.
+ *
+ * ct_aggregate_steps: per repetition best-so-far and completion times
+ * (SearchTrace.best_so_far / completion_times_us, search.py:294-304, with
+ * profiled steps charged `overhead`), then for every step column k < max_len
+ * the sums over repetitions of the padded best-so-far value and its square.
+ * total_times_out / first_times_out (nullable) receive times[-1] / times[0]
+ * of each repetition. */
+int ct_aggregate_steps(ct_ctx* ctx, double overhead, int32_t max_len,
+                       const double* col_sum_init, const double* col_sq_init,
+                       double* col_sum_out, double* col_sq_out,
+                       double* total_times_out, double* first_times_out);
+
+/* ct_aggregate_time: the time-curve sums over the first time_reps repetitions
+ * of the last launch: for every grid point g, best-so-far sampled at
+ * searchsorted(times, grid[g], 'right') - 1 (clipped), summed with its
+ * square.  Requires ct_aggregate_steps on the same launch. */
+int ct_aggregate_time(ct_ctx* ctx, int32_t time_reps, const double* grid, int32_t n_grid,
+                      const double* sum_init, const double* sq_init,
+                      double* sum_out, double* sq_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -106,6 +106,8 @@ SIGNATURES = {
     "ct_result_device_ptrs": (ctypes.c_int, [_vp, _P(_vp), _P(_vp), _P(_vp), _P(_vp)]),
     "ct_analyze_react": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64, _dbl, _dbl, _vp]),
     "ct_check_division": (ctypes.c_int, [_vp, _i64, ctypes.c_uint64, _P(_i64), _vp]),
+    "ct_aggregate_steps": (ctypes.c_int, [_vp, _dbl, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ct_aggregate_time": (ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None
@@ -288,6 +290,44 @@ class Context:
                                          ptr(status), ptr(err), ctypes.byref(stats)))
         return idx, prof, nst, status, err, stats
 
+    def fetch_status(self, n_reps: int):
+        """n_steps, status, rep_error and stats of the last launch (no trajectories)."""
+        nst = np.empty(n_reps, dtype=np.int32)
+        status = np.empty(n_reps, dtype=np.int32)
+        err = np.empty(n_reps, dtype=np.int32)
+        stats = BatchStats()
+        check(library().ct_fetch_results(self.handle, None, None, ptr(nst), ptr(status),
+                                         ptr(err), ctypes.byref(stats)))
+        return nst, status, err, stats
+
+    def failing_index(self, rep: int, n_reps: int) -> int:
+        """Configuration index a repetition stopped on with an error."""
+        idx, _, nst, _, _, _ = self.fetch(n_reps, want_profiled=False)
+        return int(idx[rep, nst[rep]]) if nst[rep] < idx.shape[1] else -1
+
+    def aggregate_steps(self, overhead: float, n_reps: int, max_len: int, sum0=None, sq0=None):
+        """(col_sum, col_sq, total_times, first_times) of the last launch."""
+        col_sum = np.empty(max_len)
+        col_sq = np.empty(max_len)
+        total = np.empty(n_reps)
+        first = np.empty(n_reps)
+        s0 = None if sum0 is None else np.ascontiguousarray(sum0, dtype=np.float64)
+        q0 = None if sq0 is None else np.ascontiguousarray(sq0, dtype=np.float64)
+        check(library().ct_aggregate_steps(self.handle, float(overhead), int(max_len), ptr(s0),
+                                           ptr(q0), ptr(col_sum), ptr(col_sq), ptr(total),
+                                           ptr(first)))
+        return col_sum, col_sq, total, first
+
+    def aggregate_time(self, time_reps: int, grid: np.ndarray, sum0=None, sq0=None):
+        g = np.ascontiguousarray(grid, dtype=np.float64)
+        out_s = np.empty(g.size)
+        out_q = np.empty(g.size)
+        s0 = None if sum0 is None else np.ascontiguousarray(sum0, dtype=np.float64)
+        q0 = None if sq0 is None else np.ascontiguousarray(sq0, dtype=np.float64)
+        check(library().ct_aggregate_time(self.handle, int(time_reps), ptr(g), g.size, ptr(s0),
+                                          ptr(q0), ptr(out_s), ptr(out_q)))
+        return out_s, out_q
+
     def fetch_stats(self):
         stats = BatchStats()
         check(library().ct_fetch_results(self.handle, None, None, None, None, None,
@@ -363,11 +403,12 @@ _ctx_lock = threading.Lock()
 _contexts = {}
 
 
-def context(device: int = 0) -> Context:
-    """Process-wide default context for one device."""
+def context(device: int = 0, slot: int = 0) -> Context:
+    """Process-wide context for one device; distinct slots are independent
+    contexts on the same GPU (own buffers, own stream)."""
     with _ctx_lock:
-        ctx = _contexts.get(device)
+        ctx = _contexts.get((device, slot))
         if ctx is None:
             ctx = Context(device)
-            _contexts[device] = ctx
+            _contexts[(device, slot)] = ctx
         return ctx

@@ -64,6 +64,7 @@ struct ct_ctx {
     int64_t n = 0;
     int64_t ld = 0;          // padded column stride
     int32_t n_counters = 0;
+    uint64_t col_cert = 0;   // columns inside raw_term_cert's domain
     // space assignments (row-major n x P)
     DevBuf<double> assign;
     int32_t n_params = 0;
@@ -87,7 +88,6 @@ struct ct_ctx {
     DevBuf<double> scratch_w;
     DevBuf<uint32_t> scratch_e;
     DevBuf<int32_t> scratch_perm;
-    DevBuf<uint32_t> seed_words;
     // single-call buffers
     DevBuf<double> vec_a, vec_b;
     DevBuf<uint8_t> mask_a, mask_b;
@@ -98,6 +98,10 @@ struct ct_ctx {
     DevBuf<int32_t> part_i;
     DevBuf<u128> tiles;
     DevBuf<long long> pick;
+    // on-device aggregation
+    DevBuf<double> agg_bsf, agg_times, agg_vec, agg_sampled;
+    bool agg_valid = false;
+    double agg_overhead = 1.0;
 };
 
 // ===========================================================================
@@ -321,6 +325,81 @@ __global__ void k_check_division(int64_t n, uint64_t seed, unsigned long long* b
     if (local) atomicAdd(bad, local);
 }
 
+// ---- aggregation (harness.py:187-244) ---------------------------------
+// One thread per repetition: best-so-far and cumulative completion times.
+__global__ void k_agg_rows(const int32_t* step_index, const uint8_t* step_profiled,
+                           const int32_t* n_steps, int32_t reps, int64_t width,
+                           const double* runtime, double overhead, double* bsf, double* times,
+                           double* total, double* first) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < reps; r += gridDim.x * blockDim.x) {
+        const int n = n_steps[r];
+        double best = INFINITY, t = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const size_t o = (size_t)r * width + k;
+            const double rt = runtime[step_index[o]];
+            const double cost = mul(rt, step_profiled[o] ? overhead : 1.0);
+            t = (k == 0) ? cost : add(t, cost);
+            best = (k == 0) ? rt : nmin(best, rt);
+            bsf[o] = best;
+            times[o] = t;
+        }
+        total[r] = t;
+        first[r] = times[(size_t)r * width];
+    }
+}
+
+// One thread per step column: sums over repetitions in repetition order.
+__global__ void k_agg_cols(const double* bsf, const int32_t* n_steps, int32_t reps, int64_t width,
+                           int32_t max_len, const double* sum0, const double* sq0,
+                           double* sum, double* sq) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < max_len; k += gridDim.x * blockDim.x) {
+        double s = sum0 ? sum0[k] : 0.0, q = sq0 ? sq0[k] : 0.0;
+        for (int r = 0; r < reps; ++r) {
+            const int last = n_steps[r] - 1;
+            const double v = bsf[(size_t)r * width + (k < last ? k : last)];
+            s = add(s, v);
+            q = add(q, mul(v, v));
+        }
+        sum[k] = s;
+        sq[k] = q;
+    }
+}
+
+// One thread per (grid point, repetition): sampled best-so-far.
+__global__ void k_agg_sample(const double* bsf, const double* times, const int32_t* n_steps,
+                             int32_t reps, int64_t width, const double* grid, int32_t n_grid,
+                             double* sampled) {
+    const int64_t total = (int64_t)reps * n_grid;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int g = (int)(i / reps), r = (int)(i % reps);
+        const double x = grid[g];
+        const double* t = times + (size_t)r * width;
+        int lo = 0, hi = n_steps[r];          // first index with t[idx] > x
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (t[mid] > x) hi = mid; else lo = mid + 1;
+        }
+        int pos = lo - 1;
+        pos = pos < 0 ? 0 : (pos > n_steps[r] - 1 ? n_steps[r] - 1 : pos);
+        sampled[(size_t)g * reps + r] = bsf[(size_t)r * width + pos];
+    }
+}
+
+__global__ void k_agg_time_sums(const double* sampled, int32_t reps, int32_t n_grid,
+                                const double* sum0, const double* sq0, double* sum, double* sq) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n_grid; g += gridDim.x * blockDim.x) {
+        double s = sum0 ? sum0[g] : 0.0, q = sq0 ? sq0[g] : 0.0;
+        for (int r = 0; r < reps; ++r) {
+            const double v = sampled[(size_t)g * reps + r];
+            s = add(s, v);
+            q = add(q, mul(v, v));
+        }
+        sum[g] = s;
+        sq[g] = q;
+    }
+}
+
 int rows_for(int64_t n) {
     // ~sqrt(N)/32 rows balances the two scans of a draw; at least 2 rows so
     // that each lane sums two weights per tile before the warp reduction
@@ -339,23 +418,21 @@ int check_ctx(ct_ctx* ctx) {
     return CT_OK;
 }
 
-int upload_seeds(ct_ctx* ctx, const ct_seed_spec* seeds, const uint32_t** ent,
-                        const uint32_t** pre) {
+int pack_seeds(const ct_seed_spec* seeds, SeedInline* out) {
     if (!seeds) return fail(CT_ERR_VALUE, "null seed spec");
     if (seeds->n_entropy < 0 || seeds->n_prefix < 0 || (seeds->n_entropy && !seeds->entropy) ||
         (seeds->n_prefix && !seeds->spawn_prefix))
         return fail(CT_ERR_VALUE, "bad seed spec");
-    size_t words = (size_t)seeds->n_entropy + seeds->n_prefix;
-    CT_CUDA(ctx->seed_words.ensure(words + 1));
-    std::vector<uint32_t> host(words + 1, 0u);
-    for (int i = 0; i < seeds->n_entropy; ++i) host[i] = seeds->entropy[i];
-    for (int i = 0; i < seeds->n_prefix; ++i) host[seeds->n_entropy + i] = seeds->spawn_prefix[i];
-    CT_CUDA(cudaMemcpyAsync(ctx->seed_words.p, host.data(), sizeof(uint32_t) * (words + 1),
-                            cudaMemcpyHostToDevice, ctx->stream));
-    *ent = ctx->seed_words.p;
-    *pre = ctx->seed_words.p + seeds->n_entropy;
-    // host vector must outlive the async copy
-    CT_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (seeds->n_entropy + seeds->n_prefix > SEED_INLINE_WORDS)
+        return fail(CT_ERR_UNSUPPORTED, "seed entropy + spawn key exceed " +
+                                            std::to_string(SEED_INLINE_WORDS) + " words");
+    std::memset(out, 0, sizeof(*out));
+    for (int i = 0; i < seeds->n_entropy; ++i) out->w[i] = seeds->entropy[i];
+    for (int i = 0; i < seeds->n_prefix; ++i) out->w[seeds->n_entropy + i] = seeds->spawn_prefix[i];
+    out->n_entropy = seeds->n_entropy;
+    out->n_prefix = seeds->n_prefix;
+    out->child_per_rep = seeds->child_per_rep;
+    out->rep_offset = seeds->rep_offset;
     return CT_OK;
 }
 
@@ -369,6 +446,7 @@ int ensure_results(ct_ctx* ctx, int64_t reps, int64_t max_steps) {
     ctx->res_reps = reps;
     ctx->res_max_steps = max_steps;
     ctx->res_valid = true;
+    ctx->agg_valid = false;
     return CT_OK;
 }
 
@@ -436,10 +514,12 @@ int ct_destroy(ct_ctx* ctx) {
     ctx->stop_bits.release(); ctx->step_index.release(); ctx->step_profiled.release();
     ctx->n_steps.release(); ctx->status.release(); ctx->rep_error.release();
     ctx->stats.release(); ctx->scratch_w.release(); ctx->scratch_e.release();
-    ctx->scratch_perm.release(); ctx->seed_words.release(); ctx->vec_a.release();
+    ctx->scratch_perm.release(); ctx->vec_a.release();
     ctx->vec_b.release(); ctx->mask_a.release(); ctx->mask_b.release(); ctx->key_a.release();
     ctx->key_b.release(); ctx->val_a.release(); ctx->val_b.release(); ctx->cub_tmp.release();
     ctx->part_d.release(); ctx->part_i.release(); ctx->tiles.release(); ctx->pick.release();
+    ctx->agg_bsf.release(); ctx->agg_times.release(); ctx->agg_vec.release();
+    ctx->agg_sampled.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     return CT_OK;
@@ -470,6 +550,22 @@ int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
     std::vector<double> colmajor((size_t)ld * c, 0.0);
     for (int64_t i = 0; i < n; ++i)
         for (int32_t j = 0; j < c; ++j) colmajor[(size_t)j * ld + i] = matrix[(size_t)i * c + j];
+    // per-column value range -> certified Eq. 16 division domain
+    uint64_t cert = 0;
+    for (int32_t j = 0; j < c && j < 64; ++j) {
+        const double* col = colmajor.data() + (size_t)j * ld;
+        double vmin = INFINITY, vpos = INFINITY, vmax = -INFINITY;
+        bool finite = true;
+        for (int64_t i = 0; i < n; ++i) {
+            const double v = col[i];
+            if (!(v == v) || std::isinf(v)) { finite = false; break; }
+            vmin = std::min(vmin, v);
+            vmax = std::max(vmax, v);
+            if (v > 0.0) vpos = std::min(vpos, v);
+        }
+        if (vpos == INFINITY) vpos = 0.0;
+        if (finite && column_certified(vmin, vpos, vmax)) cert |= 1ull << j;
+    }
     CT_CUDA(ctx->table.ensure((size_t)ld * c));
     CT_CUDA(cudaMemcpyAsync(ctx->table.p, colmajor.data(), sizeof(double) * ld * c,
                             cudaMemcpyHostToDevice, ctx->stream));
@@ -477,6 +573,7 @@ int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
     ctx->n = n;
     ctx->ld = ld;
     ctx->n_counters = c;
+    ctx->col_cert = cert;
     return CT_OK;
 }
 
@@ -688,8 +785,8 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     if (n_reps < 0) return fail(CT_ERR_VALUE, "n_reps must be >= 0");
     for (int k = 0; k < CT_N_DELTA; ++k)
         if (prm->delta_columns[k] >= ctx->n_counters) return fail(CT_ERR_VALUE, "delta column out of range");
-    const uint32_t *ent = nullptr, *pre = nullptr;
-    rc = upload_seeds(ctx, seeds, &ent, &pre); if (rc) return rc;
+    SeedInline seed_inline;
+    rc = pack_seeds(seeds, &seed_inline); if (rc) return rc;
     const int64_t n = ctx->n;
     const int64_t max_steps = (int64_t)prm->outer_iterations * (prm->inner_steps + 1);
     rc = ensure_results(ctx, std::max(n_reps, 1), max_steps); if (rc) return rc;
@@ -705,8 +802,8 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     a.inst_reaction = prm->inst_reaction; a.issue_sign = prm->issue_delta_sign; a.gamma = prm->gamma;
     a.literal_sign = prm->literal_sign; a.generation = prm->generation; a.cores = prm->cores;
     for (int k = 0; k < CT_N_DELTA; ++k) a.delta_col[k] = prm->delta_columns[k];
-    a.entropy = ent; a.n_entropy = seeds->n_entropy; a.prefix = pre; a.n_prefix = seeds->n_prefix;
-    a.child_per_rep = seeds->child_per_rep; a.rep_offset = seeds->rep_offset; a.n_reps = n_reps;
+    a.col_cert = ctx->col_cert;
+    a.seed = seed_inline; a.n_reps = n_reps;
     a.rows = rows_for(n);
     a.ntiles = (int)((n + 32LL * a.rows - 1) / (32LL * a.rows));
     a.nwords = (n + 31) / 32;
@@ -731,8 +828,8 @@ int ct_random_search_launch(ct_ctx* ctx, const ct_seed_spec* seeds, int32_t n_re
     if (!ctx->runtime.p) return fail(CT_ERR_STATE, "no replay data uploaded");
     if (use_stop && !ctx->has_stop) return fail(CT_ERR_STATE, "no stop mask uploaded");
     if (n_reps < 0) return fail(CT_ERR_VALUE, "n_reps must be >= 0");
-    const uint32_t *ent = nullptr, *pre = nullptr;
-    rc = upload_seeds(ctx, seeds, &ent, &pre); if (rc) return rc;
+    SeedInline seed_inline;
+    rc = pack_seeds(seeds, &seed_inline); if (rc) return rc;
     const int64_t n = ctx->replay_n;
     int64_t max_steps = n;
     if (max_steps_req >= 0 && max_steps_req < n) max_steps = max_steps_req;
@@ -749,8 +846,7 @@ int ct_random_search_launch(ct_ctx* ctx, const ct_seed_spec* seeds, int32_t n_re
     std::memset(&a, 0, sizeof(a));
     a.n = n; a.has_record = ctx->has_record.p; a.stop_bits = use_stop ? ctx->stop_bits.p : nullptr;
     a.max_steps_req = max_steps_req;
-    a.entropy = ent; a.n_entropy = seeds->n_entropy; a.prefix = pre; a.n_prefix = seeds->n_prefix;
-    a.child_per_rep = seeds->child_per_rep; a.rep_offset = seeds->rep_offset; a.n_reps = n_reps;
+    a.seed = seed_inline; a.n_reps = n_reps;
     a.perm_scratch = ctx->scratch_perm.p; a.n_slots = slots;
     a.step_index = ctx->step_index.p; a.step_profiled = ctx->step_profiled.p;
     a.max_steps = ctx->res_max_steps; a.n_steps = ctx->n_steps.p; a.status = ctx->status.p;
@@ -792,6 +888,86 @@ int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled, i
         stats->outer_iterations = (int64_t)st[3];
         stats->algorithmic_bytes = (int64_t)st[4];
     }
+    return CT_OK;
+}
+
+int ct_aggregate_steps(ct_ctx* ctx, double overhead, int32_t max_len, const double* sum0,
+                       const double* sq0, double* sum_out, double* sq_out, double* total_out,
+                       double* first_out) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!ctx->res_valid) return fail(CT_ERR_STATE, "no batched search launched");
+    if (!ctx->runtime.p) return fail(CT_ERR_STATE, "no replay data uploaded");
+    if (max_len < 0 || (max_len > 0 && (!sum_out || !sq_out)))
+        return fail(CT_ERR_VALUE, "bad aggregation buffers");
+    const int64_t R = ctx->res_reps, W = ctx->res_max_steps;
+    if (max_len > W) return fail(CT_ERR_VALUE, "max_len exceeds the launch's step capacity");
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(ctx->agg_bsf.ensure((size_t)std::max<int64_t>(R, 1) * W));
+    CT_CUDA(ctx->agg_times.ensure((size_t)std::max<int64_t>(R, 1) * W));
+    const size_t nv = 2 * (size_t)R + 4 * (size_t)max_len;
+    CT_CUDA(ctx->agg_vec.ensure(nv));
+    double* d_total = ctx->agg_vec.p;
+    double* d_first = d_total + R;
+    double* d_sum0 = d_first + R;
+    double* d_sq0 = d_sum0 + max_len;
+    double* d_sum = d_sq0 + max_len;
+    double* d_sq = d_sum + max_len;
+    if (R > 0) {
+        k_agg_rows<<<(int)std::min<int64_t>((R + 127) / 128, 1184), 128, 0, s>>>(
+            ctx->step_index.p, ctx->step_profiled.p, ctx->n_steps.p, (int32_t)R, W, ctx->runtime.p,
+            overhead, ctx->agg_bsf.p, ctx->agg_times.p, d_total, d_first);
+        CT_CUDA(cudaGetLastError());
+    }
+    if (max_len > 0) {
+        if (sum0) CT_CUDA(cudaMemcpyAsync(d_sum0, sum0, 8 * (size_t)max_len, cudaMemcpyHostToDevice, s));
+        if (sq0) CT_CUDA(cudaMemcpyAsync(d_sq0, sq0, 8 * (size_t)max_len, cudaMemcpyHostToDevice, s));
+        k_agg_cols<<<(max_len + 63) / 64, 64, 0, s>>>(ctx->agg_bsf.p, ctx->n_steps.p, (int32_t)R, W,
+                                                      max_len, sum0 ? d_sum0 : nullptr,
+                                                      sq0 ? d_sq0 : nullptr, d_sum, d_sq);
+        CT_CUDA(cudaGetLastError());
+        CT_CUDA(cudaMemcpyAsync(sum_out, d_sum, 8 * (size_t)max_len, cudaMemcpyDeviceToHost, s));
+        CT_CUDA(cudaMemcpyAsync(sq_out, d_sq, 8 * (size_t)max_len, cudaMemcpyDeviceToHost, s));
+    }
+    if (R > 0 && total_out)
+        CT_CUDA(cudaMemcpyAsync(total_out, d_total, 8 * (size_t)R, cudaMemcpyDeviceToHost, s));
+    if (R > 0 && first_out)
+        CT_CUDA(cudaMemcpyAsync(first_out, d_first, 8 * (size_t)R, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
+    ctx->agg_valid = true;
+    return CT_OK;
+}
+
+int ct_aggregate_time(ct_ctx* ctx, int32_t time_reps, const double* grid, int32_t n_grid,
+                      const double* sum0, const double* sq0, double* sum_out, double* sq_out) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!ctx->agg_valid) return fail(CT_ERR_STATE, "ct_aggregate_steps must run first");
+    if (n_grid < 1 || !grid || !sum_out || !sq_out) return fail(CT_ERR_VALUE, "bad grid buffers");
+    const int64_t W = ctx->res_max_steps;
+    const int32_t R = (int32_t)std::min<int64_t>(std::max(time_reps, 0), ctx->res_reps);
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(ctx->agg_sampled.ensure((size_t)std::max(R, 1) * n_grid + 5 * (size_t)n_grid));
+    double* d_grid = ctx->agg_sampled.p + (size_t)std::max(R, 1) * n_grid;
+    double* d_sum0 = d_grid + n_grid;
+    double* d_sq0 = d_sum0 + n_grid;
+    double* d_sum = d_sq0 + n_grid;
+    double* d_sq = d_sum + n_grid;
+    CT_CUDA(cudaMemcpyAsync(d_grid, grid, 8 * (size_t)n_grid, cudaMemcpyHostToDevice, s));
+    if (sum0) CT_CUDA(cudaMemcpyAsync(d_sum0, sum0, 8 * (size_t)n_grid, cudaMemcpyHostToDevice, s));
+    if (sq0) CT_CUDA(cudaMemcpyAsync(d_sq0, sq0, 8 * (size_t)n_grid, cudaMemcpyHostToDevice, s));
+    if (R > 0) {
+        const int64_t pairs = (int64_t)R * n_grid;
+        k_agg_sample<<<(int)std::min<int64_t>((pairs + 255) / 256, 2368), 256, 0, s>>>(
+            ctx->agg_bsf.p, ctx->agg_times.p, ctx->n_steps.p, R, W, d_grid, n_grid,
+            ctx->agg_sampled.p);
+        CT_CUDA(cudaGetLastError());
+    }
+    k_agg_time_sums<<<(n_grid + 63) / 64, 64, 0, s>>>(ctx->agg_sampled.p, R, n_grid,
+                                                      sum0 ? d_sum0 : nullptr,
+                                                      sq0 ? d_sq0 : nullptr, d_sum, d_sq);
+    CT_CUDA(cudaGetLastError());
+    CT_CUDA(cudaMemcpyAsync(sum_out, d_sum, 8 * (size_t)n_grid, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaMemcpyAsync(sq_out, d_sq, 8 * (size_t)n_grid, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
     return CT_OK;
 }
 

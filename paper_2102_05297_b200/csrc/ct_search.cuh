@@ -26,6 +26,29 @@ namespace ct {
 
 constexpr int MAX_ACTIVE = 18;
 
+// seed words travel inside the kernel arguments: a launch needs no copy and
+// no host synchronisation
+constexpr int SEED_INLINE_WORDS = 64;
+
+struct SeedInline {
+    uint32_t w[SEED_INLINE_WORDS];   // entropy words, then spawn-prefix words
+    int32_t n_entropy, n_prefix;
+    int32_t child_per_rep;
+    int64_t rep_offset;
+};
+
+// Shared-memory copy of the launch's seed words (all threads take part).
+__device__ __forceinline__ void load_seed_words(const SeedInline& s, uint32_t* sh) {
+    for (int i = threadIdx.x; i < s.n_entropy + s.n_prefix; i += blockDim.x) sh[i] = s.w[i];
+    __syncthreads();
+}
+
+__device__ __forceinline__ SeedWords seed_words_of(const SeedInline& s, const uint32_t* sh,
+                                                   int64_t rep) {
+    return SeedWords{sh, s.n_entropy, sh + s.n_entropy, s.n_prefix, s.child_per_rep != 0,
+                     (uint32_t)(s.rep_offset + rep)};
+}
+
 struct SearchArgs {
     // prediction table, column-major: column j of config i at table[j * ld + i]
     const double* table;
@@ -43,10 +66,8 @@ struct SearchArgs {
     int32_t literal_sign, generation;
     int64_t cores;
     int32_t delta_col[18];
-    // seeds
-    const uint32_t* entropy; int32_t n_entropy;
-    const uint32_t* prefix;  int32_t n_prefix;
-    int32_t child_per_rep;   int64_t rep_offset;
+    uint64_t col_cert;           // bit j: table column j admits raw_term_cert
+    SeedInline seed;
     int32_t n_reps;
     // tiling
     int32_t rows, ntiles;
@@ -65,11 +86,23 @@ struct SearchArgs {
     unsigned long long* stats;   // configs_scored, draws, uncertified, outer
 };
 
+__device__ __forceinline__ bool bit_get(const uint32_t* b, int64_t i) {
+    return (b[i >> 5] >> (i & 31)) & 1u;
+}
+
+struct __align__(16) RepState {
+    Pcg64 rng;
+    int64_t c_prof, ns, n_expl;
+    int st, err;
+    unsigned long long scored, draws, uncert, outers, abytes;
+};
+
 struct __align__(16) Ctl {
     u128 total;
     u128 red_tot[32];
     double red_max[32];
     double red_min[32];
+    double red_amin[32];
     int red_pos[32];
     int red_bad[32];
     ActiveTerm act[MAX_ACTIVE];
@@ -80,10 +113,74 @@ struct __align__(16) Ctl {
     int done;
     int positive;
     int nonfinite;
+    int cert_terms;
 };
 
-__device__ __forceinline__ bool bit_get(const uint32_t* b, int64_t i) {
-    return (b[i >> 5] >> (i & 31)) & 1u;
+// Eq. 16 over the whole space for one repetition's active terms: raw scores
+// into w[], pool max / min / smallest nonzero magnitude returned per thread.
+// Columns are padded to a multiple of 4*NT, so the four loads of an
+// iteration use one base pointer and immediate offsets.
+template <int NT, bool CERT>
+__device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl& ctl, const uint32_t* expl,
+                                           double* w, double& lmax, double& lmin, double& lamin) {
+    const int64_t N = a.n;
+    const int n_act = ctl.n_act;
+    for (int64_t base = threadIdx.x; base < N; base += 4LL * NT) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = 0; k < n_act; ++k) {
+            const double d = ctl.act[k].d, pv = ctl.act[k].p;
+            const double* col = a.table + (size_t)ctl.act[k].col * a.ld + base;
+            double c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c[u] = __ldg(col + u * NT);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                acc[u] = add(acc[u], CERT ? raw_term_cert(c[u], d, pv) : raw_term_nb(c[u], d, pv));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t e = base + (int64_t)u * NT;
+            if (e < N) {
+                const bool in = !bit_get(expl, e);
+                w[e] = in ? acc[u] : 0.0;
+                if (in) {
+                    lmax = nmax(lmax, acc[u]);
+                    lmin = nmin(lmin, acc[u]);
+                    const double m = fabs(acc[u]);
+                    lamin = (m != 0.0 && m < lamin) ? m : lamin;
+                }
+            }
+        }
+    }
+}
+
+// Eq. 17 weights + exact 2^-66 tile totals (one warp per tile).
+template <bool CERT>
+__device__ __forceinline__ void weight_pass(const SearchArgs& a, int NW, double smax, double smin,
+                                            const uint32_t* expl, double* w, u128* tile_tot,
+                                            u128& wtot, int& pos, int& bad) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t N = a.n;
+    const int64_t tile_len = 32LL * a.rows;
+    const double gamma = a.gamma;
+    const double y_max = rcp_nv(smax), y_min = rcp_nv(smin);
+    for (int t = warp; t < a.ntiles; t += NW) {
+        u128 sum = 0;
+        for (int j = 0; j < a.rows; ++j) {
+            int64_t e = (int64_t)t * tile_len + 32LL * j + lane;
+            if (e < N) {
+                double wt = 0.0;
+                if (!bit_get(expl, e)) wt = weight_rcp<CERT>(w[e], smax, smin, y_max, y_min, gamma);
+                w[e] = wt;
+                u128 f;
+                if (to_fx(wt, &f)) sum += f; else bad = 1;
+                pos += (wt > 0.0);
+            }
+        }
+        sum = warp_sum(sum);
+        if (lane == 0) tile_tot[t] = sum;
+        wtot += sum;
+    }
 }
 
 template <int NT>
@@ -91,9 +188,13 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ Ctl ctl;
+    __shared__ RepState rs;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t N = a.n;
     const int64_t tile_len = 32LL * a.rows;
+
+    __shared__ uint32_t seed_sh[SEED_INLINE_WORDS];
+    load_seed_words(a.seed, seed_sh);
 
     u128* tile_tot = reinterpret_cast<u128*>(smem);
     unsigned char* p = smem + sizeof(u128) * (size_t)a.ntiles;
@@ -107,18 +208,15 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
     for (int rep = blockIdx.x; rep < a.n_reps; rep += gridDim.x) {
         for (int64_t i = tid; i < a.nwords; i += NT) expl[i] = 0u;
 
-        // per-repetition serial state (thread 0 only)
-        Pcg64 rng;
-        int64_t c_prof = 0, ns = 0, n_expl = 0;
-        int st = CT_STATUS_BUDGET, err = 0;
-        unsigned long long scored = 0, draws = 0, uncert = 0, outers = 0, abytes = 0;
+        // per-repetition serial state lives in shared memory (only lane 0 of
+        // warp 0 updates it), so it costs no registers in the parallel phases
         int32_t* out_idx = a.step_index + (size_t)rep * a.max_steps;
         uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
         if (tid == 0) {
-            SeedWords sw{a.entropy, a.n_entropy, a.prefix, a.n_prefix,
-                         a.child_per_rep != 0, (uint32_t)(a.rep_offset + rep)};
-            rng.seed(seed_pool(sw));
-            c_prof = (int64_t)rng.integers((uint64_t)N);
+            rs.c_prof = 0; rs.ns = 0; rs.n_expl = 0; rs.st = CT_STATUS_BUDGET; rs.err = 0;
+            rs.scored = 0; rs.draws = 0; rs.uncert = 0; rs.outers = 0; rs.abytes = 0;
+            rs.rng.seed(seed_pool(seed_words_of(a.seed, seed_sh, rep)));
+            rs.c_prof = (int64_t)rs.rng.integers((uint64_t)N);
             ctl.done = 0;
         }
         __syncthreads();
@@ -131,7 +229,7 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
             // (the same per-component code as the scalar analyze()/react())
             // and the active terms compacted in react() order with a ballot.
             if (warp == 0) {
-                const int64_t cp = __shfl_sync(FULL, (long long)c_prof, 0);
+                const int64_t cp = rs.c_prof;
                 if (lane < N_REQ) ctl.cnt[lane] = a.counters[(size_t)cp * N_REQ + lane];
                 const int col = (lane < N_COMP) ? a.delta_col[lane] : -1;
                 const double pv = (col >= 0) ? a.table[(size_t)col * a.ld + cp] : 0.0;
@@ -154,22 +252,28 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                     // literal sign: (-d)(c - p) == d(p - c) exactly
                     ctl.act[slot].d = a.literal_sign ? -dk : dk;
                 }
+                // certified division domain for every active term
+                const double two_m200 = 6.223015277861142e-61;
+                const bool cert_ok = !act || (col < 64 && ((a.col_cert >> col) & 1ull) &&
+                                              fabs(dk) >= two_m200);
+                const bool cert_all = __all_sync(FULL, cert_ok);
                 if (lane == 0) {
                     const int na = __popc(amask);
                     ctl.n_act = na;
+                    ctl.cert_terms = cert_all ? 1 : 0;
                     if (!rec_ok) {
-                        st = CT_STATUS_ERROR; err = -4; ctl.done = 1;
-                        if (ns < a.max_steps) out_idx[ns] = (int32_t)cp;   // failing index
+                        rs.st = CT_STATUS_ERROR; rs.err = -4; ctl.done = 1;
+                        if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)cp;   // failing index
                     } else {
-                        out_idx[ns] = (int32_t)cp; out_prof[ns] = 1; ++ns;
+                        out_idx[rs.ns] = (int32_t)cp; out_prof[rs.ns] = 1; ++rs.ns;
                         uint32_t m = 1u << (cp & 31);
-                        if (!(expl[cp >> 5] & m)) { expl[cp >> 5] |= m; ++n_expl; }
-                        if (is_stop) { st = CT_STATUS_STOPPED; ctl.done = 1; }
-                        else if (n_expl >= N) { st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
+                        if (!(expl[cp >> 5] & m)) { expl[cp >> 5] |= m; ++rs.n_expl; }
+                        if (is_stop) { rs.st = CT_STATUS_STOPPED; ctl.done = 1; }
+                        else if (rs.n_expl >= N) { rs.st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
                         else {
-                            unsigned long long pool = (unsigned long long)(N - n_expl);
-                            scored += pool; ++outers;
-                            abytes += pool * (8ull * (unsigned long long)na + 16ull);
+                            unsigned long long pool = (unsigned long long)(N - rs.n_expl);
+                            rs.scored += pool; ++rs.outers;
+                            rs.abytes += pool * (8ull * (unsigned long long)na + 16ull);
                         }
                     }
                 }
@@ -178,68 +282,39 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
             if (ctl.done) break;
 
             // ---------------- Eq. 16 raw scores (all threads) ------------------
-            // Columns are padded to a multiple of 4*NT, so the four loads of an
-            // iteration use one base pointer and immediate offsets.
-            const int n_act = ctl.n_act;
-            double lmax = -INFINITY, lmin = INFINITY;
-            for (int64_t base = tid; base < N; base += 4LL * NT) {
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                for (int k = 0; k < n_act; ++k) {
-                    const double d = ctl.act[k].d, pv = ctl.act[k].p;
-                    const double* col = a.table + (size_t)ctl.act[k].col * a.ld + base;
-                    double c[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) c[u] = __ldg(col + u * NT);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) acc[u] = add(acc[u], raw_term_nb(c[u], d, pv));
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t e = base + (int64_t)u * NT;
-                    if (e < N) {
-                        const bool in = !bit_get(expl, e);
-                        w[e] = in ? acc[u] : 0.0;
-                        if (in) { lmax = nmax(lmax, acc[u]); lmin = nmin(lmin, acc[u]); }
-                    }
-                }
-            }
+            double lmax = -INFINITY, lmin = INFINITY, lamin = INFINITY;
+            if (ctl.cert_terms) score_pass<NT, true>(a, ctl, expl, w, lmax, lmin, lamin);
+            else score_pass<NT, false>(a, ctl, expl, w, lmax, lmin, lamin);
             lmax = warp_max(lmax);
             lmin = warp_min(lmin);
-            if (lane == 0) { ctl.red_max[warp] = lmax; ctl.red_min[warp] = lmin; }
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) lamin = fmin(lamin, __shfl_xor_sync(FULL, lamin, m));
+            if (lane == 0) { ctl.red_max[warp] = lmax; ctl.red_min[warp] = lmin; ctl.red_amin[warp] = lamin; }
             __syncthreads();
 
             // ---------------- Eq. 17 weights + exact tile totals ---------------
             {
-                double smax = ctl.red_max[0], smin = ctl.red_min[0];
+                double smax = ctl.red_max[0], smin = ctl.red_min[0], amin = ctl.red_amin[0];
 #pragma unroll
-                for (int i = 1; i < NW; ++i) { smax = nmax(smax, ctl.red_max[i]); smin = nmin(smin, ctl.red_min[i]); }
-                const double gamma = a.gamma;
+                for (int i = 1; i < NW; ++i) {
+                    smax = nmax(smax, ctl.red_max[i]); smin = nmin(smin, ctl.red_min[i]);
+                    amin = fmin(amin, ctl.red_amin[i]);
+                }
+                // certified Eq. 17 domain: every nonzero |s| in [2^-400, 2^400]
+                // (NaN extrema fail the comparisons)
+                const double lo = 3.872591914849318e-121, hi = 2.5822498780869086e+120;
+                const bool cert = (amin >= lo || amin == INFINITY) && smax <= hi && smin >= -hi;
                 u128 wtot = 0;
                 int pos = 0, bad = 0;
-                for (int t = warp; t < a.ntiles; t += NW) {
-                    u128 sum = 0;
-                    for (int j = 0; j < a.rows; ++j) {
-                        int64_t e = (int64_t)t * tile_len + 32LL * j + lane;
-                        if (e < N) {
-                            double wt = 0.0;
-                            if (!bit_get(expl, e)) wt = weight(w[e], smax, smin, gamma);
-                            w[e] = wt;
-                            u128 f;
-                            if (to_fx(wt, &f)) sum += f; else bad = 1;
-                            pos += (wt > 0.0);
-                        }
-                    }
-                    sum = warp_sum(sum);
-                    if (lane == 0) tile_tot[t] = sum;
-                    wtot += sum;
-                }
+                if (cert) weight_pass<true>(a, NW, smax, smin, expl, w, tile_tot, wtot, pos, bad);
+                else weight_pass<false>(a, NW, smax, smin, expl, w, tile_tot, wtot, pos, bad);
                 pos = warp_sum_i(pos);
                 bad = __any_sync(FULL, bad);
                 if (lane == 0) { ctl.red_tot[warp] = wtot; ctl.red_pos[warp] = pos; ctl.red_bad[warp] = bad; }
             }
             __syncthreads();
 
-            // ---------------- n certified draws (warp 0) ----------------------
+            // ---------------- n certified rs.draws (warp 0) ----------------------
             if (warp == 0) {
                 u128 total = 0;
                 int positive = 0, bad = 0;
@@ -247,19 +322,19 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                     total += ctl.red_tot[i]; positive += ctl.red_pos[i]; bad |= ctl.red_bad[i];
                 }
                 // each lane owns a contiguous chunk of tiles; its inclusive
-                // prefix is kept across the draws and patched after a zeroing
+                // prefix is kept across the rs.draws and patched after a zeroing
                 const int cpl = (a.ntiles + 31) >> 5;
                 const int t0 = lane * cpl, t1 = min(t0 + cpl, a.ntiles);
                 u128 mine = 0;
                 for (int t = t0; t < t1; ++t) mine += tile_tot[t];
                 u128 lane_pref = warp_incl_scan(mine, lane);
                 int done = 0;
-                if (bad) { if (lane == 0) { st = CT_STATUS_ERROR; err = -7; } done = 1; }
+                if (bad) { if (lane == 0) { rs.st = CT_STATUS_ERROR; rs.err = -7; } done = 1; }
                 double t_best = INFINITY;
                 for (int k = 0; k < a.inner && !done; ++k) {
-                    if (positive <= 0) { if (lane == 0) st = CT_STATUS_EXHAUSTED; done = 1; break; }
+                    if (positive <= 0) { if (lane == 0) rs.st = CT_STATUS_EXHAUSTED; done = 1; break; }
                     double u = 0.0;
-                    if (lane == 0) u = rng.next_double();
+                    if (lane == 0) u = rs.rng.next_double();
                     u = __shfl_sync(FULL, u, 0);
                     const double total_d = fx_to_double(total);
                     const double r = mul(u, total_d);
@@ -268,10 +343,10 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                                                   r_fx, lane);
                     int64_t chosen = pk.idx;
                     if (!certify(pk, r_fx, total_d, N)) {
-                        if (lane == 0) { chosen = sequential_select(w, N, u); ++uncert; }
+                        if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
                         chosen = __shfl_sync(FULL, (long long)chosen, 0);
                     }
-                    if (lane == 0) ++draws;
+                    if (lane == 0) ++rs.draws;
                     const bool in_range = chosen >= 0 && chosen < N;
                     const int64_t cs = in_range ? chosen : 0;
                     // the replay lookups of the draw, issued together
@@ -280,8 +355,8 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                     const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cs);
                     if (!rec_ok) {
                         if (lane == 0) {
-                            st = CT_STATUS_ERROR; err = -4;
-                            if (ns < a.max_steps) out_idx[ns] = (int32_t)chosen;
+                            rs.st = CT_STATUS_ERROR; rs.err = -4;
+                            if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)chosen;
                         }
                         done = 1; break;
                     }
@@ -299,15 +374,15 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
                     total -= f;
                     --positive;
                     if (lane == 0) {
-                        out_idx[ns] = (int32_t)chosen; out_prof[ns] = 0; ++ns;
+                        out_idx[rs.ns] = (int32_t)chosen; out_prof[rs.ns] = 0; ++rs.ns;
                         uint32_t m = 1u << (chosen & 31);
-                        if (!(expl[chosen >> 5] & m)) { expl[chosen >> 5] |= m; ++n_expl; }
+                        if (!(expl[chosen >> 5] & m)) { expl[chosen >> 5] |= m; ++rs.n_expl; }
                     }
                     if (is_stop) {
-                        if (lane == 0) st = CT_STATUS_STOPPED;
+                        if (lane == 0) rs.st = CT_STATUS_STOPPED;
                         done = 1; break;
                     }
-                    if (rt <= t_best) { t_best = rt; if (lane == 0) c_prof = chosen; }
+                    if (rt <= t_best) { t_best = rt; if (lane == 0) rs.c_prof = chosen; }
                     __syncwarp();
                 }
                 if (lane == 0) ctl.done = done;
@@ -317,14 +392,14 @@ __global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_se
         }
 
         if (tid == 0) {
-            a.n_steps[rep] = (int32_t)ns;
-            a.status[rep] = st;
-            a.rep_error[rep] = err;
-            atomicAdd(&a.stats[0], scored);
-            atomicAdd(&a.stats[1], draws);
-            atomicAdd(&a.stats[2], uncert);
-            atomicAdd(&a.stats[3], outers);
-            atomicAdd(&a.stats[4], abytes);
+            a.n_steps[rep] = (int32_t)rs.ns;
+            a.status[rep] = rs.st;
+            a.rep_error[rep] = rs.err;
+            atomicAdd(&a.stats[0], rs.scored);
+            atomicAdd(&a.stats[1], rs.draws);
+            atomicAdd(&a.stats[2], rs.uncert);
+            atomicAdd(&a.stats[3], rs.outers);
+            atomicAdd(&a.stats[4], rs.abytes);
         }
         __syncthreads();
     }
@@ -339,9 +414,7 @@ struct RandomArgs {
     const uint8_t* has_record;
     const uint32_t* stop_bits;     // nullable
     int64_t max_steps_req;         // < 0: None
-    const uint32_t* entropy; int32_t n_entropy;
-    const uint32_t* prefix;  int32_t n_prefix;
-    int32_t child_per_rep;   int64_t rep_offset;
+    SeedInline seed;
     int32_t n_reps;
     int32_t* perm_scratch;         // n_slots * n
     int32_t n_slots;
@@ -354,15 +427,15 @@ struct RandomArgs {
 };
 
 __global__ void k_random_search(const RandomArgs a) {
+    __shared__ uint32_t seed_sh[SEED_INLINE_WORDS];
+    load_seed_words(a.seed, seed_sh);
     for (int rep = blockIdx.x * blockDim.x + threadIdx.x; rep < a.n_reps;
          rep += gridDim.x * blockDim.x) {
         int slot = (blockIdx.x * blockDim.x + threadIdx.x);
         int32_t* perm = a.perm_scratch + (size_t)slot * a.n;
         const int64_t N = a.n;
-        SeedWords sw{a.entropy, a.n_entropy, a.prefix, a.n_prefix,
-                     a.child_per_rep != 0, (uint32_t)(a.rep_offset + rep)};
         Pcg64 rng;
-        rng.seed(seed_pool(sw));
+        rng.seed(seed_pool(seed_words_of(a.seed, seed_sh, rep)));
         for (int64_t i = 0; i < N; ++i) perm[i] = (int32_t)i;
         for (int64_t i = N - 1; i > 0; --i) {
             int64_t j = (int64_t)rng.interval((uint64_t)i);

@@ -180,29 +180,31 @@ def launch(ctx, spec: ExperimentSpec, params, rep_offset: int, n_reps: int):
         ctx.launch_profile(params, seeds, n_reps)
 
 
-def run_batch(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None,
-              table=None) -> Tuple[BatchResult, np.ndarray]:
-    """All repetitions of spec on the given GPUs (contiguous rep ranges)."""
-    devices = list(devices) if devices else [0]
+def _launch_all(spec: ExperimentSpec, devices: Sequence[int], table=None):
+    """Upload and launch every device's contiguous repetition range.
+
+    Returns [(context, first_rep, n_reps)] in repetition order and the
+    runtime vector; the launches are asynchronous."""
     R = spec.repetitions
     parts = np.array_split(np.arange(R), len(devices))
     if table is None and spec.searcher == SEARCHER_PROFILE:
         table = _as_table(spec.model, spec.dataset.space)
-    results = [None] * len(devices)
+    launched = [None] * len(devices)
     errors = [None] * len(devices)
     runtime = [None]
 
     def work(k):
         try:
-            ctx = _native.context(devices[k])
+            # one context per entry, so a device listed twice gets two
+            slot = devices[:k].count(devices[k])
+            ctx = _native.context(devices[k], slot)
             params, rt = prepare_device(ctx, spec, table)
             runtime[0] = rt
             idxs = parts[k]
             if idxs.size == 0:
-                results[k] = None
                 return
             launch(ctx, spec, params, int(idxs[0]), int(idxs.size))
-            results[k] = ctx.fetch(int(idxs.size))
+            launched[k] = (ctx, int(idxs[0]), int(idxs.size))
         except BaseException as exc:   # re-raised on the caller's thread
             errors[k] = exc
 
@@ -217,7 +219,16 @@ def run_batch(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None,
     for exc in errors:
         if exc is not None:
             raise exc
-    parts_ok = [r for r in results if r is not None]
+    return [x for x in launched if x is not None], runtime[0]
+
+
+def run_batch(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None,
+              table=None) -> Tuple[BatchResult, np.ndarray]:
+    """All repetitions of spec on the given GPUs (contiguous rep ranges),
+    trajectories fetched to the host."""
+    devices = list(devices) if devices else [0]
+    launched, runtime = _launch_all(spec, devices, table)
+    parts_ok = [ctx.fetch(n) for ctx, _, n in launched]
     width = max(r[0].shape[1] for r in parts_ok)
 
     def cat(j, dtype):
@@ -242,7 +253,7 @@ def run_batch(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None,
         ns = int(res.n_steps[r])
         failing = int(res.step_index[r, ns]) if ns < res.step_index.shape[1] else -1
         raise rep_error(int(err[r]), failing)
-    return res, runtime[0]
+    return res, runtime
 
 
 def aggregate(spec: ExperimentSpec, res: BatchResult, runtime: np.ndarray) -> ConvergenceReport:
@@ -305,7 +316,77 @@ def aggregate(spec: ExperimentSpec, res: BatchResult, runtime: np.ndarray) -> Co
 
 
 def simulate(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None) -> ConvergenceReport:
-    """Run the repetitions on the GPU(s) and aggregate (harness.py:175-244)."""
+    """Run the repetitions on the GPU(s) and aggregate (harness.py:175-244).
+
+    The trajectories never leave the GPU: the report's sums are taken on the
+    device in the reference's order (ct_aggregate_steps / ct_aggregate_time,
+    chained across devices in repetition order), so only O(R + steps)
+    numbers come back and the report is byte-identical to aggregate() on the
+    fetched trajectories."""
+    _worker_count()
+    devices = list(devices) if devices else [0]
+    launched, _ = _launch_all(spec, devices)
+    reps = spec.repetitions
+    nst_l, status_l, scored, uncert = [], [], 0, 0
+    for ctx, first, n in launched:
+        nst, status, err, stats = ctx.fetch_status(n)
+        bad = np.flatnonzero(status == _native.CT_STATUS_ERROR)
+        if bad.size:
+            r = int(bad[0])
+            raise rep_error(int(err[r]), ctx.failing_index(r, n))
+        nst_l.append(nst)
+        status_l.append(status)
+        scored += stats.configs_scored
+        uncert += stats.uncertified
+    nst = np.concatenate(nst_l).astype(np.int64)
+    status = np.concatenate(status_l)
+    max_len = int(nst.max())
+
+    col_sum = col_sq = None
+    totals, firsts = [], []
+    for ctx, first, n in launched:
+        col_sum, col_sq, tot, fst = ctx.aggregate_steps(spec.profiling_overhead, n, max_len,
+                                                        col_sum, col_sq)
+        totals.append(tot)
+        firsts.append(fst)
+    total_times = np.concatenate(totals)
+    first_times = np.concatenate(firsts)
+    mean = col_sum / reps
+    var = np.maximum(0.0, col_sq / reps - mean * mean)
+    step_std = np.sqrt(var)
+
+    tr = reps if spec.time_repetitions is None else min(reps, spec.time_repetitions)
+    t_start = max(float(t) for t in first_times[:tr])
+    t_end = max(float(t) for t in total_times[:tr])
+    if t_end > t_start:
+        grid = np.linspace(t_start, t_end, TIME_GRID_POINTS)
+    else:
+        grid = np.array([t_start])
+    tc_sum = tc_sq = None
+    for ctx, first, n in launched:
+        count = min(n, max(0, tr - first))
+        if count == 0:
+            continue
+        tc_sum, tc_sq = ctx.aggregate_time(count, grid, tc_sum, tc_sq)
+    tmean = tc_sum / tr
+    tvar = np.maximum(0.0, tc_sq / tr - tmean * tmean)
+    ds = spec.dataset
+    return ConvergenceReport(
+        name=spec.name, searcher=spec.searcher,
+        dataset_label=f"{ds.arch.name}/{ds.input_label}", repetitions=reps,
+        inner_steps=spec.inner_steps, outer_iterations=spec.resolved_outer_iterations(),
+        seed=spec.seed, slack=spec.slack, profiling_overhead=spec.profiling_overhead,
+        steps=nst.astype(float), censored=int(np.count_nonzero(status != _native.CT_STATUS_STOPPED)),
+        mean_time_seconds=float(np.mean(total_times)) / 1e6,
+        step_curve_mean=mean, step_curve_std=step_std, time_grid_seconds=grid / 1e6,
+        time_curve_mean=tmean, time_curve_std=np.sqrt(tvar),
+        configs_scored=int(scored), uncertified_draws=int(uncert))
+
+
+def simulate_host_aggregate(spec: ExperimentSpec,
+                            devices: Optional[Sequence[int]] = None) -> ConvergenceReport:
+    """simulate() with the trajectories fetched and aggregated on the host
+    (aggregate()); the device-aggregation path is checked against it."""
     _worker_count()
     res, runtime = run_batch(spec, devices)
     return aggregate(spec, res, runtime)

@@ -232,3 +232,25 @@ def test_inline_division_is_ddiv_rn():
     from paper_2102_05297_b200 import _native
     ctx = _native.context(0)
     assert ctx.check_division(1 << 28, seed=12345) == 0
+
+
+@pytest.mark.parametrize("name", ["gradient", "transpose"])
+def test_device_aggregation_matches_host_aggregate(name):
+    """simulate() sums on the device; aggregate() on fetched trajectories is
+    the reference's harness.py:187-244 arithmetic.  Both must agree bit for bit,
+    also with the repetitions split over two contexts (chained partial sums)."""
+    from paper_2102_05297_b200 import ExactModelSet, ExperimentSpec, harness
+    ds = dataset_from_golden(name)
+    for searcher, tr in (("profile", None), ("profile", 7), ("random", 13)):
+        spec = ExperimentSpec(dataset=ds, searcher=searcher,
+                              model=ExactModelSet(ds) if searcher == "profile" else None,
+                              name="x", repetitions=40, seed=3, time_repetitions=tr,
+                              profiling_overhead=2.5)
+        want = harness.simulate_host_aggregate(spec)
+        for devices in ([0], [0, 0]):
+            got = harness.simulate(spec, devices=devices)
+            for f in ("steps", "step_curve_mean", "step_curve_std", "time_grid_seconds",
+                      "time_curve_mean", "time_curve_std"):
+                np.testing.assert_array_equal(getattr(got, f), getattr(want, f), err_msg=f)
+            assert got.censored == want.censored
+            assert got.mean_time_seconds == want.mean_time_seconds
