@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -811,15 +812,30 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     a.max_steps = max_steps; a.n_steps = ctx->n_steps.p; a.status = ctx->status.p;
     a.rep_error = ctx->rep_error.p; a.stats = ctx->stats.p;
 
+    // threads per repetition: the serial phases (expert system, draws) run on
+    // one warp, so small spaces use small CTAs (many repetitions per SM, no
+    // idle warps at the CTA barrier); CT_SEARCH_NT overrides (benchmarking)
+    int nt = n <= 8192 ? 32 : (n <= 65536 ? 256 : 512);
+    if (const char* env = std::getenv("CT_SEARCH_NT")) nt = std::atoi(env);
+    // weights + explored bits go to shared memory when that still lets all
+    // repetitions be resident at once (one wave); otherwise to a per-CTA
+    // slice of global scratch (L2-resident)
     const size_t budget = 200 * 1024;
     size_t tiles_b = 16 * (size_t)a.ntiles, w_b = 8 * (size_t)n, e_b = 4 * (size_t)a.nwords;
-    a.w_in_smem = (tiles_b + w_b + e_b <= budget) ? 1 : 0;
+    if (tiles_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the tile index");
+    const int64_t want_per_sm = std::min<int64_t>(std::min<int64_t>(
+        (n_reps + ctx->sm_count - 1) / ctx->sm_count, 32), 2048 / nt);
+    const size_t per_cta_cap = std::min<size_t>(budget, (size_t)(227 * 1024 / std::max<int64_t>(want_per_sm, 1)) - 4096);
+    a.w_in_smem = (tiles_b + w_b + e_b <= per_cta_cap) ? 1 : 0;
     a.e_in_smem = (tiles_b + (a.w_in_smem ? w_b : 0) + e_b <= budget) ? 1 : 0;
     size_t smem = tiles_b + (a.w_in_smem ? w_b : 0) + (a.e_in_smem ? e_b : 0);
-    if (tiles_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the tile index");
-    if (n <= 4096) return launch_profile<128>(ctx, a, smem, n_reps);
-    if (n <= 65536) return launch_profile<256>(ctx, a, smem, n_reps);
-    return launch_profile<512>(ctx, a, smem, n_reps);
+    switch (nt) {
+    case 32: return launch_profile<32>(ctx, a, smem, n_reps);
+    case 64: return launch_profile<64>(ctx, a, smem, n_reps);
+    case 128: return launch_profile<128>(ctx, a, smem, n_reps);
+    case 256: return launch_profile<256>(ctx, a, smem, n_reps);
+    default: return launch_profile<512>(ctx, a, smem, n_reps);
+    }
 }
 
 int ct_random_search_launch(ct_ctx* ctx, const ct_seed_spec* seeds, int32_t n_reps,

@@ -184,7 +184,8 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int NW, double 
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, (NT == 128) ? 7 : (896 / NT)) k_profile_search(const SearchArgs a) {
+__global__ void __launch_bounds__(NT, (NT <= 64) ? 8 : ((NT == 128) ? 7 : (896 / NT)))
+k_profile_search(const SearchArgs a) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ Ctl ctl;

@@ -1,0 +1,62 @@
+"""Time the batched search kernel on every synthetic space for several CTA
+sizes (CT_SEARCH_NT).  GPU only; CUDA events on the context's stream.
+
+    python scripts/search_sweep.py [--nt 32,64,128] [--spaces coulomb,transpose]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nt", default="32,64,128,256")
+    ap.add_argument("--spaces", default="coulomb,transpose,nbody,conv,gemm")
+    ap.add_argument("--reps", type=int, default=1000)
+    ap.add_argument("--outer", type=int, default=40)
+    ap.add_argument("--runs", type=int, default=5)
+    a = ap.parse_args()
+    import torch
+    from paper_2102_05297_b200 import ExactModelSet, harness, spaces
+    from paper_2102_05297_b200 import _native
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = _native.context(0)
+    ctx.set_stream(stream.cuda_stream)
+    for name in a.spaces.split(","):
+        ds = spaces.SPACES[name]()
+        spec = harness.ExperimentSpec(dataset=ds, searcher="profile", model=ExactModelSet(ds),
+                                      repetitions=a.reps, outer_iterations=a.outer, seed=42,
+                                      stop_at_well_performing=False)
+        params, _ = harness.prepare_device(ctx, spec)
+        ref = None
+        for nt in a.nt.split(","):
+            os.environ["CT_SEARCH_NT"] = nt
+            harness.launch(ctx, spec, params, 0, a.reps)   # warm-up
+            times = []
+            for _ in range(a.runs):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                harness.launch(ctx, spec, params, 0, a.reps)
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+            idx, _, nst, _, _, stats = ctx.fetch(a.reps, want_profiled=False)
+            same = None
+            if ref is None:
+                ref = (idx.copy(), nst.copy())
+            else:
+                same = bool((ref[1] == nst).all() and (ref[0] == idx).all())
+            ms = sorted(times)[len(times) // 2]
+            print(json.dumps({"space": name, "n": len(ds.space), "nt": int(nt), "ms": ms,
+                              "configs_per_s": stats.configs_scored / (ms / 1e3),
+                              "same_as_first": same}), flush=True)
+    os.environ.pop("CT_SEARCH_NT", None)
+
+
+if __name__ == "__main__":
+    main()
