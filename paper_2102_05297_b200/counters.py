@@ -82,6 +82,22 @@ VOLTA_METRICS: Dict[str, Tuple[str, float]] = {
 }
 _BY_VOLTA = {name: (abbr, scale) for abbr, (name, scale) in VOLTA_METRICS.items()}
 
+# Pre-Volta (nvprof event/metric) names; readings are canonical as they come.
+PRE_VOLTA_NAMES: Dict[str, str] = {
+    "DRAM_RT": "dram_read_transactions", "DRAM_WT": "dram_write_transactions",
+    "L2_RT": "l2_read_transactions", "L2_WT": "l2_write_transactions",
+    "TEX_RWT": "tex_cache_transactions", "LOC_O": "local_memory_overhead",
+    "SHR_LT": "shared_load_transactions", "SHR_WT": "shared_store_transactions",
+    "INST_F32": "inst_fp_32", "INST_F64": "inst_fp_64", "INST_INT": "inst_integer",
+    "INST_MISC": "inst_misc", "INST_LDST": "inst_compute_ld_st", "INST_CONT": "inst_control",
+    "INST_BCONV": "inst_bit_convert", "INST_EXE": "inst_executed",
+    "INST_ISSUE_U": "issue_slot_utilization", "DRAM_U": "dram_utilization",
+    "L2_U": "l2_utilization", "TEX_U": "tex_utilization", "SHR_U": "shared_utilization",
+    "SM_E": "sm_efficiency", "WARP_E": "warp_execution_efficiency",
+    "WARP_NP_E": "warp_nonpred_execution_efficiency",
+}
+_BY_PRE_VOLTA = {name: abbr for abbr, name in PRE_VOLTA_NAMES.items()}
+
 
 @dataclass(frozen=True)
 class ArchProfile:
@@ -107,8 +123,8 @@ def generation_code(arch) -> int:
 def canonicalize(raw_name: str, value: float, arch) -> Tuple[str, float]:
     """Raw counter reading -> (abbreviation, canonical value) (counters.py:161-180).
 
-    Pre-Volta event names are not carried (the device path targets B200);
-    arch overrides, Volta+ metric names and canonical abbreviations are.
+    Order: arch overrides, then the generation's catalog names, then the
+    canonical abbreviations verbatim.
     """
     overrides = getattr(arch, "overrides", {}) or {}
     if raw_name in overrides:
@@ -119,6 +135,8 @@ def canonicalize(raw_name: str, value: float, arch) -> Tuple[str, float]:
     if arch.generation == VOLTA_PLUS and raw_name in _BY_VOLTA:
         abbr, scale = _BY_VOLTA[raw_name]
         return abbr, value * scale
+    if arch.generation == PRE_VOLTA and raw_name in _BY_PRE_VOLTA:
+        return _BY_PRE_VOLTA[raw_name], value
     if raw_name in KIND:
         return raw_name, value
     raise KeyError(f"counter name {raw_name!r} is not known for generation {arch.generation}")
