@@ -86,8 +86,7 @@ struct ct_ctx {
     int64_t res_reps = 0, res_max_steps = 0;
     bool res_valid = false;
     // scratch
-    DevBuf<double> scratch_w;
-    DevBuf<uint32_t> scratch_e;
+    DevBuf<u128> scratch_pref;
     DevBuf<int32_t> scratch_perm;
     // single-call buffers
     DevBuf<double> vec_a, vec_b;
@@ -451,26 +450,28 @@ int ensure_results(ct_ctx* ctx, int64_t reps, int64_t max_steps) {
     return CT_OK;
 }
 
-template <int NT>
-int launch_profile(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
-    auto kern = k_profile_search<NT>;
+template <int NT, bool SMEM>
+int launch_profile_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
+    auto kern = k_profile_search<NT, SMEM>;
     if (smem > 48 * 1024)
         CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
     if (occ < 1) return fail(CT_ERR_CUDA, "search kernel does not fit on an SM");
     int grid = std::min(n_reps, occ * ctx->sm_count);
-    if (!a.w_in_smem) {
-        CT_CUDA(ctx->scratch_w.ensure((size_t)grid * a.n));
-        a.scratch_w = ctx->scratch_w.p;
-    }
-    if (!a.e_in_smem) {
-        CT_CUDA(ctx->scratch_e.ensure((size_t)grid * a.nwords));
-        a.scratch_e = ctx->scratch_e.p;
+    if (!SMEM) {
+        CT_CUDA(ctx->scratch_pref.ensure((size_t)grid * 32 * (size_t)a.nrows));
+        a.scratch_pref = ctx->scratch_pref.p;
     }
     kern<<<grid, NT, smem, ctx->stream>>>(a);
     CT_CUDA(cudaGetLastError());
     return CT_OK;
+}
+
+template <int NT>
+int launch_profile(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int n_reps) {
+    return in_smem ? launch_profile_t<NT, true>(ctx, a, smem, n_reps)
+                   : launch_profile_t<NT, false>(ctx, a, smem, n_reps);
 }
 
 }  // namespace
@@ -514,7 +515,7 @@ int ct_destroy(ct_ctx* ctx) {
     ctx->threads.release(); ctx->counters.release(); ctx->has_record.release();
     ctx->stop_bits.release(); ctx->step_index.release(); ctx->step_profiled.release();
     ctx->n_steps.release(); ctx->status.release(); ctx->rep_error.release();
-    ctx->stats.release(); ctx->scratch_w.release(); ctx->scratch_e.release();
+    ctx->stats.release(); ctx->scratch_pref.release();
     ctx->scratch_perm.release(); ctx->vec_a.release();
     ctx->vec_b.release(); ctx->mask_a.release(); ctx->mask_b.release(); ctx->key_a.release();
     ctx->key_b.release(); ctx->val_a.release(); ctx->val_b.release(); ctx->cub_tmp.release();
@@ -805,9 +806,9 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     for (int k = 0; k < CT_N_DELTA; ++k) a.delta_col[k] = prm->delta_columns[k];
     a.col_cert = ctx->col_cert;
     a.seed = seed_inline; a.n_reps = n_reps;
-    a.rows = rows_for(n);
-    a.ntiles = (int)((n + 32LL * a.rows - 1) / (32LL * a.rows));
+    a.nrows = (int32_t)((n + 31) / 32);
     a.nwords = (n + 31) / 32;
+    if (const char* env = std::getenv("CT_SEARCH_FORCE_SEQUENTIAL")) a.force_sequential = std::atoi(env);
     a.step_index = ctx->step_index.p; a.step_profiled = ctx->step_profiled.p;
     a.max_steps = max_steps; a.n_steps = ctx->n_steps.p; a.status = ctx->status.p;
     a.rep_error = ctx->rep_error.p; a.stats = ctx->stats.p;
@@ -815,26 +816,29 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     // threads per repetition: the serial phases (expert system, draws) run on
     // one warp, so small spaces use small CTAs (many repetitions per SM, no
     // idle warps at the CTA barrier); CT_SEARCH_NT overrides (benchmarking)
-    int nt = n <= 8192 ? 32 : (n <= 65536 ? 256 : 512);
+    int nt = n <= 8192 ? 128 : (n <= 65536 ? 256 : 512);
     if (const char* env = std::getenv("CT_SEARCH_NT")) nt = std::atoi(env);
-    // weights + explored bits go to shared memory when that still lets all
-    // repetitions be resident at once (one wave); otherwise to a per-CTA
-    // slice of global scratch (L2-resident)
+    // row totals + explored bits always in shared memory; the per-
+    // configuration prefixes too when that still lets all repetitions be
+    // resident at once (one wave), otherwise a per-CTA slice of global
+    // scratch (L2-resident)
     const size_t budget = 200 * 1024;
-    size_t tiles_b = 16 * (size_t)a.ntiles, w_b = 8 * (size_t)n, e_b = 4 * (size_t)a.nwords;
-    if (tiles_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the tile index");
+    const size_t head_b = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+    const size_t pref_b = 16 * 32 * (size_t)a.nrows;
+    if (head_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the row index");
     const int64_t want_per_sm = std::min<int64_t>(std::min<int64_t>(
         (n_reps + ctx->sm_count - 1) / ctx->sm_count, 32), 2048 / nt);
-    const size_t per_cta_cap = std::min<size_t>(budget, (size_t)(227 * 1024 / std::max<int64_t>(want_per_sm, 1)) - 4096);
-    a.w_in_smem = (tiles_b + w_b + e_b <= per_cta_cap) ? 1 : 0;
-    a.e_in_smem = (tiles_b + (a.w_in_smem ? w_b : 0) + e_b <= budget) ? 1 : 0;
-    size_t smem = tiles_b + (a.w_in_smem ? w_b : 0) + (a.e_in_smem ? e_b : 0);
+    const size_t per_cta_cap = std::min<size_t>(
+        budget, (size_t)(228 * 1024 / std::max<int64_t>(want_per_sm, 1)) - 3 * 1024);
+    bool in_smem = head_b + pref_b <= per_cta_cap;
+    if (const char* env = std::getenv("CT_SEARCH_SMEM")) in_smem = std::atoi(env) != 0 && head_b + pref_b <= budget;
+    const size_t smem = head_b + (in_smem ? pref_b : 0);
     switch (nt) {
-    case 32: return launch_profile<32>(ctx, a, smem, n_reps);
-    case 64: return launch_profile<64>(ctx, a, smem, n_reps);
-    case 128: return launch_profile<128>(ctx, a, smem, n_reps);
-    case 256: return launch_profile<256>(ctx, a, smem, n_reps);
-    default: return launch_profile<512>(ctx, a, smem, n_reps);
+    case 32: return launch_profile<32>(ctx, a, in_smem, smem, n_reps);
+    case 64: return launch_profile<64>(ctx, a, in_smem, smem, n_reps);
+    case 128: return launch_profile<128>(ctx, a, in_smem, smem, n_reps);
+    case 256: return launch_profile<256>(ctx, a, in_smem, smem, n_reps);
+    default: return launch_profile<512>(ctx, a, in_smem, smem, n_reps);
     }
 }
 

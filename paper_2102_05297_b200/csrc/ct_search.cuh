@@ -4,18 +4,27 @@
 // end and then takes the next repetition (persistent grid sized to the
 // resident-CTA capacity).  Per outer iteration, inside the CTA:
 //
-//   thread 0   record the profiled step, replay its counters, analyze() +
-//              react() (Eqs. 6-15), build the active-term list        [serial]
+//   warp 0     record the profiled step, replay its counters, analyze() +
+//              react() (Eqs. 6-15) on 18 lanes, ballot-compact the active
+//              terms                                                   [serial]
 //   all warps  Eq. 16 raw score of every unexplored configuration,
 //              coalesced column reads of the column-major table, pool
-//              max/min                                                 [parallel]
-//   all warps  Eq. 17 weights + exact 2^-66 fixed-point tile totals    [parallel]
-//   warp 0     n certified inverse-CDF draws with progressive zeroing,
-//              replay lookups, stop test, argmin with later ties      [serial]
+//              max / min / smallest magnitude                          [parallel]
+//   all warps  Eq. 17 weights, exact 2^-66 fixed point, one exact warp
+//              scan per 32-configuration row: every configuration's
+//              in-row inclusive prefix and every row's total are stored [parallel]
+//   warp 0     n certified inverse-CDF draws: a ballot over per-lane row
+//              chunks, one 128-bit load per lane and a ballot inside the
+//              row; the drawn weight is subtracted from the stored
+//              prefixes (exact), replay lookups, stop test, argmin with
+//              later ties                                              [serial]
 //
-// Weights live in shared memory when the space fits (N <~ 20k), otherwise in
-// a per-CTA-slot global scratch slice.  The numpy Generator stream of the
-// repetition is regenerated on the device (ct_rng.cuh).
+// The serial phases run on one warp while the others wait, so they are kept
+// to a few hundred instructions per draw: no scans, no float<->fixed
+// conversions of whole rows.  The per-configuration prefixes (16 B) live in
+// shared memory when all repetitions still fit on the GPU at once, otherwise
+// in a per-CTA slice of global scratch (L2-resident).  The numpy Generator
+// stream of the repetition is regenerated on the device (ct_rng.cuh).
 #pragma once
 #include "ct_select.cuh"
 #include "ct_expert.cuh"
@@ -69,13 +78,13 @@ struct SearchArgs {
     uint64_t col_cert;           // bit j: table column j admits raw_term_cert
     SeedInline seed;
     int32_t n_reps;
-    // tiling
-    int32_t rows, ntiles;
-    // storage
-    int32_t w_in_smem, e_in_smem;
-    double* scratch_w;           // gridDim.x * n doubles (if !w_in_smem)
-    uint32_t* scratch_e;         // gridDim.x * nwords   (if !e_in_smem)
+    // rows of 32 configurations
+    int32_t nrows;
     int64_t nwords;
+    int32_t force_sequential;    // test hook: decide every draw sequentially
+    // storage: per-configuration prefixes (16 B each, nrows * 32) in shared
+    // memory or a per-CTA slice of scratch_pref
+    u128* scratch_pref;
     // outputs
     int32_t* step_index;
     uint8_t* step_profiled;
@@ -83,7 +92,7 @@ struct SearchArgs {
     int32_t* n_steps;
     int32_t* status;
     int32_t* rep_error;
-    unsigned long long* stats;   // configs_scored, draws, uncertified, outer
+    unsigned long long* stats;   // configs_scored, draws, uncertified, outer, bytes
 };
 
 __device__ __forceinline__ bool bit_get(const uint32_t* b, int64_t i) {
@@ -97,32 +106,30 @@ struct __align__(16) RepState {
     unsigned long long scored, draws, uncert, outers, abytes;
 };
 
+template <int NW>
 struct __align__(16) Ctl {
-    u128 total;
-    u128 red_tot[32];
-    double red_max[32];
-    double red_min[32];
-    double red_amin[32];
-    int red_pos[32];
-    int red_bad[32];
+    u128 red_tot[NW];
+    double red_max[NW];
+    double red_min[NW];
+    double red_amin[NW];
+    int red_pos[NW];
+    int red_bad[NW];
     ActiveTerm act[MAX_ACTIVE];
     double cnt[N_REQ];
-    double pv[N_COMP];
-    double s_max, s_min;
     int n_act;
     int done;
-    int positive;
-    int nonfinite;
     int cert_terms;
 };
 
-// Eq. 16 over the whole space for one repetition's active terms: raw scores
-// into w[], pool max / min / smallest nonzero magnitude returned per thread.
-// Columns are padded to a multiple of 4*NT, so the four loads of an
-// iteration use one base pointer and immediate offsets.
-template <int NT, bool CERT>
-__device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl& ctl, const uint32_t* expl,
-                                           double* w, double& lmax, double& lmin, double& lamin) {
+// Eq. 16 over the whole space for one repetition's active terms: raw score of
+// configuration e into raw[2e] (the low half of its prefix slot), pool max /
+// min / smallest nonzero magnitude returned per thread.  Columns are padded
+// to a multiple of 4*NT, so the four loads of an iteration use one base
+// pointer and immediate offsets.
+template <int NT, bool CERT, int NW>
+__device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& ctl,
+                                           const uint32_t* expl, double* raw, double& lmax,
+                                           double& lmin, double& lamin) {
     const int64_t N = a.n;
     const int n_act = ctl.n_act;
     for (int64_t base = threadIdx.x; base < N; base += 4LL * NT) {
@@ -142,7 +149,7 @@ __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl& ctl, 
             const int64_t e = base + (int64_t)u * NT;
             if (e < N) {
                 const bool in = !bit_get(expl, e);
-                w[e] = in ? acc[u] : 0.0;
+                raw[2 * e] = in ? acc[u] : 0.0;
                 if (in) {
                     lmax = nmax(lmax, acc[u]);
                     lmin = nmin(lmin, acc[u]);
@@ -154,57 +161,87 @@ __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl& ctl, 
     }
 }
 
-// Eq. 17 weights + exact 2^-66 tile totals (one warp per tile).
+// Eq. 17 weights and the exact in-row prefixes: warp w takes rows w, w+NW, ...
+// lane l converts configuration 32 t + l to fixed point, an exact warp scan
+// gives its inclusive in-row prefix (stored over its raw score) and lane 31
+// holds the row total.
 template <bool CERT>
 __device__ __forceinline__ void weight_pass(const SearchArgs& a, int NW, double smax, double smin,
-                                            const uint32_t* expl, double* w, u128* tile_tot,
+                                            const uint32_t* expl, u128* pref, u128* row_tot,
                                             u128& wtot, int& pos, int& bad) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t N = a.n;
-    const int64_t tile_len = 32LL * a.rows;
     const double gamma = a.gamma;
     const double y_max = rcp_nv(smax), y_min = rcp_nv(smin);
-    for (int t = warp; t < a.ntiles; t += NW) {
-        u128 sum = 0;
-        for (int j = 0; j < a.rows; ++j) {
-            int64_t e = (int64_t)t * tile_len + 32LL * j + lane;
-            if (e < N) {
-                double wt = 0.0;
-                if (!bit_get(expl, e)) wt = weight_rcp<CERT>(w[e], smax, smin, y_max, y_min, gamma);
-                w[e] = wt;
-                u128 f;
-                if (to_fx(wt, &f)) sum += f; else bad = 1;
-                pos += (wt > 0.0);
-            }
+    const double* raw = reinterpret_cast<const double*>(pref);
+    for (int t = warp; t < a.nrows; t += NW) {
+        const int64_t e = 32LL * t + lane;
+        u128 f = 0;
+        if (e < N) {
+            double wt = 0.0;
+            if (!bit_get(expl, e)) wt = weight_rcp<CERT>(raw[2 * e], smax, smin, y_max, y_min, gamma);
+            if (!to_fx(wt, &f)) bad = 1;
+            pos += (wt > 0.0);
         }
-        sum = warp_sum(sum);
-        if (lane == 0) tile_tot[t] = sum;
-        wtot += sum;
+        const u128 incl = warp_incl_scan(f, lane);
+        pref[e] = incl;
+        const u128 tot = shfl_u128(incl, 31);
+        if (lane == 0) row_tot[t] = tot;
+        wtot += tot;
     }
 }
 
-template <int NT>
+// Sequential float64 re-decision of an uncertified draw (np.cumsum +
+// searchsorted 'right'), one thread, over the weights recovered exactly from
+// the stored prefixes.  Returns n when r reaches the total.
+__device__ __noinline__ int64_t sequential_select_pref(const u128* pref, int64_t n, double u) {
+    double c = 0.0;
+    for (int64_t e = 0; e < n; ++e) {
+        const u128 prev = (e & 31) ? pref[e - 1] : (u128)0;
+        c = add(c, fx_to_double(pref[e] - prev));
+    }
+    const double r = mul(u, c);
+    double s = 0.0;
+    for (int64_t e = 0; e < n; ++e) {
+        const u128 prev = (e & 31) ? pref[e - 1] : (u128)0;
+        s = add(s, fx_to_double(pref[e] - prev));
+        if (s > r) return e;
+    }
+    return n;
+}
+
+// v * 2^-66 for the draw's r = u * T: within 1 ulp of T (one hardware
+// rounding of hi 2^64 + double(lo)); the certificate charges the error.
+__device__ __forceinline__ double fx_total_to_double(u128 v) {
+    const double hi = (double)(unsigned long long)(v >> 64);
+    const double lo = (double)(unsigned long long)v;
+    return __fma_rn(hi, 18446744073709551616.0, lo) * 1.3552527156068805e-20;   // 2^64, 2^-66
+}
+
+template <int NT, bool SMEM>
 __global__ void __launch_bounds__(NT, (NT <= 64) ? 8 : ((NT == 128) ? 7 : (896 / NT)))
 k_profile_search(const SearchArgs a) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ Ctl ctl;
+    __shared__ Ctl<NW> ctl;
     __shared__ RepState rs;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t N = a.n;
-    const int64_t tile_len = 32LL * a.rows;
 
     __shared__ uint32_t seed_sh[SEED_INLINE_WORDS];
     load_seed_words(a.seed, seed_sh);
 
-    u128* tile_tot = reinterpret_cast<u128*>(smem);
-    unsigned char* p = smem + sizeof(u128) * (size_t)a.ntiles;
-    double* w;
-    if (a.w_in_smem) { w = reinterpret_cast<double*>(p); p += sizeof(double) * (size_t)N; }
-    else { w = a.scratch_w + (size_t)blockIdx.x * (size_t)N; }
-    uint32_t* expl;
-    if (a.e_in_smem) { expl = reinterpret_cast<uint32_t*>(p); }
-    else { expl = a.scratch_e + (size_t)blockIdx.x * (size_t)a.nwords; }
+    // dynamic shared memory: row totals | explored bits | [prefixes]
+    u128* row_tot = reinterpret_cast<u128*>(smem);
+    uint32_t* expl = reinterpret_cast<uint32_t*>(smem + sizeof(u128) * (size_t)a.nrows);
+    u128* pref;
+    if (SMEM) {
+        const size_t off = (sizeof(u128) * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+        pref = reinterpret_cast<u128*>(smem + off);
+    } else {
+        pref = a.scratch_pref + (size_t)blockIdx.x * 32 * (size_t)a.nrows;
+    }
+    double* raw = reinterpret_cast<double*>(pref);
 
     for (int rep = blockIdx.x; rep < a.n_reps; rep += gridDim.x) {
         for (int64_t i = tid; i < a.nwords; i += NT) expl[i] = 0u;
@@ -284,8 +321,8 @@ k_profile_search(const SearchArgs a) {
 
             // ---------------- Eq. 16 raw scores (all threads) ------------------
             double lmax = -INFINITY, lmin = INFINITY, lamin = INFINITY;
-            if (ctl.cert_terms) score_pass<NT, true>(a, ctl, expl, w, lmax, lmin, lamin);
-            else score_pass<NT, false>(a, ctl, expl, w, lmax, lmin, lamin);
+            if (ctl.cert_terms) score_pass<NT, true>(a, ctl, expl, raw, lmax, lmin, lamin);
+            else score_pass<NT, false>(a, ctl, expl, raw, lmax, lmin, lamin);
             lmax = warp_max(lmax);
             lmin = warp_min(lmin);
 #pragma unroll
@@ -293,7 +330,7 @@ k_profile_search(const SearchArgs a) {
             if (lane == 0) { ctl.red_max[warp] = lmax; ctl.red_min[warp] = lmin; ctl.red_amin[warp] = lamin; }
             __syncthreads();
 
-            // ---------------- Eq. 17 weights + exact tile totals ---------------
+            // ---------------- Eq. 17 weights + exact in-row prefixes -----------
             {
                 double smax = ctl.red_max[0], smin = ctl.red_min[0], amin = ctl.red_amin[0];
 #pragma unroll
@@ -307,28 +344,35 @@ k_profile_search(const SearchArgs a) {
                 const bool cert = (amin >= lo || amin == INFINITY) && smax <= hi && smin >= -hi;
                 u128 wtot = 0;
                 int pos = 0, bad = 0;
-                if (cert) weight_pass<true>(a, NW, smax, smin, expl, w, tile_tot, wtot, pos, bad);
-                else weight_pass<false>(a, NW, smax, smin, expl, w, tile_tot, wtot, pos, bad);
+                if (cert) weight_pass<true>(a, NW, smax, smin, expl, pref, row_tot, wtot, pos, bad);
+                else weight_pass<false>(a, NW, smax, smin, expl, pref, row_tot, wtot, pos, bad);
                 pos = warp_sum_i(pos);
                 bad = __any_sync(FULL, bad);
                 if (lane == 0) { ctl.red_tot[warp] = wtot; ctl.red_pos[warp] = pos; ctl.red_bad[warp] = bad; }
             }
             __syncthreads();
 
-            // ---------------- n certified rs.draws (warp 0) ----------------------
+            // ---------------- n certified draws (warp 0) ----------------------
             if (warp == 0) {
                 u128 total = 0;
                 int positive = 0, bad = 0;
+#pragma unroll
                 for (int i = 0; i < NW; ++i) {
                     total += ctl.red_tot[i]; positive += ctl.red_pos[i]; bad |= ctl.red_bad[i];
                 }
-                // each lane owns a contiguous chunk of tiles; its inclusive
-                // prefix is kept across the rs.draws and patched after a zeroing
-                const int cpl = (a.ntiles + 31) >> 5;
-                const int t0 = lane * cpl, t1 = min(t0 + cpl, a.ntiles);
+                // each lane owns a contiguous chunk of rows; its inclusive
+                // prefix is kept across the draws and patched after a zeroing
+                const int cpl = (a.nrows + 31) >> 5;
+                const int t0 = lane * cpl, t1 = min(t0 + cpl, a.nrows);
                 u128 mine = 0;
-                for (int t = t0; t < t1; ++t) mine += tile_tot[t];
+                for (int t = t0; t < t1; ++t) mine += row_tot[t];
                 u128 lane_pref = warp_incl_scan(mine, lane);
+                // certificate half-width (SURVEY hard part 3): sequential
+                // float prefix vs exact prefix, weights within 1 ulp, T within
+                // 1 ulp; taken at the iteration's largest total
+                const double bound = (double)(2 * N + 32) * 1.1102230246251565e-16 *
+                                     fx_total_to_double(total);
+                const u128 b_fx = floor_fx(bound) + 1;
                 int done = 0;
                 if (bad) { if (lane == 0) { rs.st = CT_STATUS_ERROR; rs.err = -7; } done = 1; }
                 double t_best = INFINITY;
@@ -337,15 +381,48 @@ k_profile_search(const SearchArgs a) {
                     double u = 0.0;
                     if (lane == 0) u = rs.rng.next_double();
                     u = __shfl_sync(FULL, u, 0);
-                    const double total_d = fx_to_double(total);
-                    const double r = mul(u, total_d);
+                    const double r = mul(u, fx_total_to_double(total));
                     const u128 r_fx = floor_fx(r);
-                    Located pk = warp_locate_pref(tile_tot, t0, t1, lane_pref, mine, w, N, a.rows,
-                                                  r_fx, lane);
-                    int64_t chosen = pk.idx;
-                    if (!certify(pk, r_fx, total_d, N)) {
-                        if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
+                    // the lane whose row chunk holds r, then the row, then the
+                    // configuration: one ballot each
+                    int64_t chosen = -1;
+                    bool ok = false;
+                    u128 wfx = 0;
+                    int row = -1, l2 = 0;
+                    const unsigned bal = __ballot_sync(FULL, lane_pref > r_fx);
+                    if (bal) {
+                        const int L = __ffs(bal) - 1;
+                        u128 carry = lane_pref - mine;
+                        if (lane == L) {
+                            for (int t = t0; t < t1; ++t) {
+                                const u128 nxt = carry + row_tot[t];
+                                if (nxt > r_fx) { row = t; break; }
+                                carry = nxt;
+                            }
+                        }
+                        row = __shfl_sync(FULL, row, L);
+                        carry = shfl_u128(carry, L);
+                        const u128 p = pref[32LL * row + lane];
+                        l2 = __ffs(__ballot_sync(FULL, carry + p > r_fx)) - 1;
+                        const u128 prev = shfl_u128(p, l2 > 0 ? l2 - 1 : 0);
+                        const u128 before = carry + (l2 > 0 ? prev : (u128)0);
+                        wfx = carry + shfl_u128(p, l2) - before;
+                        chosen = 32LL * row + l2;
+                        // r far enough from both boundaries of the chosen
+                        // configuration: the reference's sequential cumsum
+                        // picks it too
+                        ok = l2 >= 0 && (r_fx - before > b_fx) && (before + wfx - r_fx - 1 > b_fx);
+                        ok = ok && !a.force_sequential;
+                    }
+                    if (!ok) {
+                        if (lane == 0) { chosen = sequential_select_pref(pref, N, u); ++rs.uncert; }
                         chosen = __shfl_sync(FULL, (long long)chosen, 0);
+                        // weight of the re-decided configuration, from its prefixes
+                        if (chosen >= 0 && chosen < N) {
+                            row = (int)(chosen >> 5); l2 = (int)(chosen & 31);
+                            const u128 pc = pref[chosen];
+                            wfx = pc - (l2 > 0 ? pref[chosen - 1] : (u128)0);
+                        }
                     }
                     if (lane == 0) ++rs.draws;
                     const bool in_range = chosen >= 0 && chosen < N;
@@ -361,18 +438,14 @@ k_profile_search(const SearchArgs a) {
                         }
                         done = 1; break;
                     }
-                    // zero the drawn weight: the exact prefix stays exact
-                    u128 f = 0;
-                    to_fx(w[chosen], &f);
-                    const int tc = (int)(chosen / tile_len);
+                    // zero the drawn weight: its own and every later in-row
+                    // prefix, its row total and the lane prefixes drop by wfx
                     __syncwarp();
-                    if (lane == 0) {
-                        w[chosen] = 0.0;
-                        tile_tot[tc] -= f;
-                    }
-                    if (tc >= t0 && tc < t1) mine -= f;
-                    if (tc < t1) lane_pref -= f;
-                    total -= f;
+                    if (lane >= l2) pref[32LL * row + lane] -= wfx;
+                    if (lane == 0) row_tot[row] -= wfx;
+                    if (row >= t0 && row < t1) mine -= wfx;
+                    if (row < t1) lane_pref -= wfx;
+                    total -= wfx;
                     --positive;
                     if (lane == 0) {
                         out_idx[rs.ns] = (int32_t)chosen; out_prof[rs.ns] = 0; ++rs.ns;

@@ -254,3 +254,30 @@ def test_device_aggregation_matches_host_aggregate(name):
                 np.testing.assert_array_equal(getattr(got, f), getattr(want, f), err_msg=f)
             assert got.censored == want.censored
             assert got.mean_time_seconds == want.mean_time_seconds
+
+
+def test_sequential_redecision_path_matches_reference(monkeypatch):
+    """Every draw forced through the uncertified path (sequential float
+    cumsum over the weights recovered from the exact prefixes): the
+    trajectories must still be the reference's."""
+    from paper_2102_05297_b200 import _native
+    from paper_2102_05297_b200.search import search_params
+    from paper_2102_05297_b200.space import replay_arrays
+    monkeypatch.setenv("CT_SEARCH_FORCE_SEQUENTIAL", "1")
+    traj = golden("traj_gradient.npz")
+    reps, i = 8, int(traj["i"])
+    ds, table = _table("gradient", "exact")
+    rt, th, req, hr = replay_arrays(ds)
+    stop = np.zeros(len(ds.space), dtype=np.uint8)
+    stop[traj["well"]] = 1
+    ctx = _native.context(0)
+    ctx.upload_table(table.matrix)
+    ctx.upload_replay(rt, th, req, hr, stop)
+    params = search_params(table, ds.arch, i=i, n=5, inst_reaction=0.7, literal_sign=False,
+                           score_top_k=None, use_stop=True)
+    ctx.launch_profile(params, _native.SeedWords(42, child_per_rep=True), reps)
+    idx, _, nst, _, _, stats = ctx.fetch(reps)
+    want = ragged(traj, "exact_stop")
+    for r in range(reps):
+        assert idx[r, :nst[r]].tolist() == want[r]
+    assert stats.uncertified == stats.draws > 0
