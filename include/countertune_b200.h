@@ -196,6 +196,42 @@ int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled,
 int ct_result_device_ptrs(ct_ctx* ctx, void** step_index, void** step_profiled,
                           void** n_steps, void** status);
 
+/* ---- batched model inference (search.py:54-63 over models.py:310-333) ---
+ * A trained ModelSet flattened by paper_2102_05297_b200.models.
+ * compile_model_program: trees as node arrays (feature -1 = leaf), per
+ * column either a tree root or a key-sorted list of binary-subspace
+ * regression models (key bits = binary parameters in declared order, first
+ * parameter most significant), each a list of terms (kind 0 intercept,
+ * 1 lin, 2 quad, 3 cross; p1/p2 parameter positions; coefficient). */
+typedef struct {
+    int32_t n_cols, n_nodes, n_models, n_terms, n_binary;
+    const int32_t* node_feature;
+    const int32_t* node_left;
+    const int32_t* node_right;
+    const double*  node_threshold;
+    const double*  node_value;
+    const int32_t* col_root;
+    const int32_t* col_model_first;
+    const int32_t* col_model_count;
+    const uint64_t* model_key;
+    const int32_t* model_term_first;
+    const int32_t* model_term_count;
+    const int32_t* term_kind;
+    const int32_t* term_p1;
+    const int32_t* term_p2;
+    const double*  term_coef;
+    const int32_t* binary_pos;
+} ct_model_program;
+
+/* PredictionTable.from_model_set for a whole space on the GPU: every
+ * configuration's predicted counters, clamped at 0, 0 where the reference
+ * omits a counter (no model for the subspace) -- bit-identical to the
+ * reference.  The result also becomes the context's resident prediction
+ * table (as ct_table_upload would make it); out_rowmajor (nullable,
+ * n x n_cols) receives a host copy. */
+int ct_model_predict(ct_ctx* ctx, const ct_model_program* prog, const double* assign_rowmajor,
+                     int64_t n_configs, int32_t n_params, double* out_rowmajor);
+
 /* ---- on-device aggregation of the last launch (harness.py:187-244) ------
  * The ConvergenceReport statistics computed where the trajectories live, with
  * the reference's float operations in its order (sequential sums over

@@ -83,6 +83,19 @@ class BatchStats(ctypes.Structure):
     ]
 
 
+class ModelProgramC(ctypes.Structure):
+    """ct_model_program"""
+    _fields_ = [
+        ("n_cols", _i32), ("n_nodes", _i32), ("n_models", _i32), ("n_terms", _i32),
+        ("n_binary", _i32),
+        ("node_feature", _vp), ("node_left", _vp), ("node_right", _vp),
+        ("node_threshold", _vp), ("node_value", _vp), ("col_root", _vp),
+        ("col_model_first", _vp), ("col_model_count", _vp), ("model_key", _vp),
+        ("model_term_first", _vp), ("model_term_count", _vp), ("term_kind", _vp),
+        ("term_p1", _vp), ("term_p2", _vp), ("term_coef", _vp), ("binary_pos", _vp),
+    ]
+
+
 # name -> (restype, argtypes); the exported surface of include/countertune_b200.h
 SIGNATURES = {
     "ct_abi_version": (ctypes.c_int, []),
@@ -106,6 +119,7 @@ SIGNATURES = {
     "ct_result_device_ptrs": (ctypes.c_int, [_vp, _P(_vp), _P(_vp), _P(_vp), _P(_vp)]),
     "ct_analyze_react": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64, _dbl, _dbl, _vp]),
     "ct_check_division": (ctypes.c_int, [_vp, _i64, ctypes.c_uint64, _P(_i64), _vp]),
+    "ct_model_predict": (ctypes.c_int, [_vp, _P(ModelProgramC), _vp, _i64, _i32, _vp]),
     "ct_aggregate_steps": (ctypes.c_int, [_vp, _dbl, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ct_aggregate_time": (ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
 }
@@ -289,6 +303,26 @@ class Context:
         check(library().ct_fetch_results(self.handle, ptr(idx), ptr(prof), ptr(nst),
                                          ptr(status), ptr(err), ctypes.byref(stats)))
         return idx, prof, nst, status, err, stats
+
+    def model_predict(self, prog, assignments: np.ndarray) -> np.ndarray:
+        """ct_model_predict: the n x n_cols table (also left resident on the
+        device as the context's prediction table)."""
+        a = np.ascontiguousarray(assignments, dtype=np.float64)
+        arrays = {f: np.ascontiguousarray(getattr(prog, f)) for f in (
+            "node_feature", "node_left", "node_right", "node_threshold", "node_value",
+            "col_root", "col_model_first", "col_model_count", "model_key", "model_term_first",
+            "model_term_count", "term_kind", "term_p1", "term_p2", "term_coef", "binary_pos")}
+        c = ModelProgramC()
+        c.n_cols, c.n_nodes = prog.n_cols, arrays["node_feature"].size
+        c.n_models, c.n_terms = arrays["model_key"].size, arrays["term_kind"].size
+        c.n_binary = arrays["binary_pos"].size
+        for f, arr in arrays.items():
+            setattr(c, f, arr.ctypes.data if arr.size else None)
+        out = np.empty((a.shape[0], prog.n_cols), dtype=np.float64)
+        check(library().ct_model_predict(self.handle, ctypes.byref(c), ptr(a), a.shape[0],
+                                         a.shape[1], ptr(out)))
+        self._table_key = None
+        return out
 
     def fetch_status(self, n_reps: int):
         """n_steps, status, rep_error and stats of the last launch (no trajectories)."""

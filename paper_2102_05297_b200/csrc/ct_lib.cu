@@ -18,6 +18,7 @@
 
 #include "countertune_b200.h"
 #include "ct_search.cuh"
+#include "ct_models.cuh"
 
 using namespace ct;
 
@@ -100,6 +101,9 @@ struct ct_ctx {
     DevBuf<long long> pick;
     // on-device aggregation
     DevBuf<double> agg_bsf, agg_times, agg_vec, agg_sampled;
+    // model inference
+    DevBuf<unsigned char> model_blob;
+    DevBuf<double> model_out;
     bool agg_valid = false;
     double agg_overhead = 1.0;
 };
@@ -400,6 +404,26 @@ __global__ void k_agg_time_sums(const double* sampled, int32_t reps, int32_t n_g
     }
 }
 
+// Per-column value range of a row-major n x c table -> bit j set when column
+// j is inside raw_term_cert's certified division domain.
+uint64_t certified_columns(const double* m, int64_t n, int32_t c) {
+    uint64_t cert = 0;
+    for (int32_t j = 0; j < c && j < 64; ++j) {
+        double vmin = INFINITY, vpos = INFINITY, vmax = -INFINITY;
+        bool finite = true;
+        for (int64_t i = 0; i < n; ++i) {
+            const double v = m[(size_t)i * c + j];
+            if (!(v == v) || std::isinf(v)) { finite = false; break; }
+            vmin = std::min(vmin, v);
+            vmax = std::max(vmax, v);
+            if (v > 0.0) vpos = std::min(vpos, v);
+        }
+        if (vpos == INFINITY) vpos = 0.0;
+        if (finite && column_certified(vmin, vpos, vmax)) cert |= 1ull << j;
+    }
+    return cert;
+}
+
 int rows_for(int64_t n) {
     // ~sqrt(N)/32 rows balances the two scans of a draw; at least 2 rows so
     // that each lane sums two weights per tile before the warp reduction
@@ -521,7 +545,7 @@ int ct_destroy(ct_ctx* ctx) {
     ctx->key_b.release(); ctx->val_a.release(); ctx->val_b.release(); ctx->cub_tmp.release();
     ctx->part_d.release(); ctx->part_i.release(); ctx->tiles.release(); ctx->pick.release();
     ctx->agg_bsf.release(); ctx->agg_times.release(); ctx->agg_vec.release();
-    ctx->agg_sampled.release();
+    ctx->agg_sampled.release(); ctx->model_blob.release(); ctx->model_out.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     return CT_OK;
@@ -552,22 +576,7 @@ int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
     std::vector<double> colmajor((size_t)ld * c, 0.0);
     for (int64_t i = 0; i < n; ++i)
         for (int32_t j = 0; j < c; ++j) colmajor[(size_t)j * ld + i] = matrix[(size_t)i * c + j];
-    // per-column value range -> certified Eq. 16 division domain
-    uint64_t cert = 0;
-    for (int32_t j = 0; j < c && j < 64; ++j) {
-        const double* col = colmajor.data() + (size_t)j * ld;
-        double vmin = INFINITY, vpos = INFINITY, vmax = -INFINITY;
-        bool finite = true;
-        for (int64_t i = 0; i < n; ++i) {
-            const double v = col[i];
-            if (!(v == v) || std::isinf(v)) { finite = false; break; }
-            vmin = std::min(vmin, v);
-            vmax = std::max(vmax, v);
-            if (v > 0.0) vpos = std::min(vpos, v);
-        }
-        if (vpos == INFINITY) vpos = 0.0;
-        if (finite && column_certified(vmin, vpos, vmax)) cert |= 1ull << j;
-    }
+    const uint64_t cert = certified_columns(matrix, n, c);
     CT_CUDA(ctx->table.ensure((size_t)ld * c));
     CT_CUDA(cudaMemcpyAsync(ctx->table.p, colmajor.data(), sizeof(double) * ld * c,
                             cudaMemcpyHostToDevice, ctx->stream));
@@ -576,6 +585,71 @@ int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
     ctx->ld = ld;
     ctx->n_counters = c;
     ctx->col_cert = cert;
+    return CT_OK;
+}
+
+int ct_model_predict(ct_ctx* ctx, const ct_model_program* pg, const double* assign, int64_t n,
+                     int32_t p, double* out_rowmajor) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!pg || !assign || n < 1 || p < 1 || pg->n_cols < 1)
+        return fail(CT_ERR_VALUE, "model inference needs a programme, n >= 1 and params >= 1");
+    if (n > INT32_MAX) return fail(CT_ERR_VALUE, "spaces above 2^31-1 configurations are not supported");
+    if (pg->n_binary < 0 || pg->n_binary > 63) return fail(CT_ERR_VALUE, "bad binary parameter count");
+    for (int b = 0; b < pg->n_binary; ++b)
+        if (pg->binary_pos[b] < 0 || pg->binary_pos[b] >= p) return fail(CT_ERR_VALUE, "binary position out of range");
+    for (int i = 0; i < pg->n_nodes; ++i)
+        if (pg->node_feature[i] >= p) return fail(CT_ERR_MISMATCH, "tree feature outside the parameter list");
+    for (int i = 0; i < pg->n_terms; ++i)
+        if (pg->term_p1[i] >= p || pg->term_p2[i] >= p) return fail(CT_ERR_MISMATCH, "regression term outside the parameter list");
+    // one blob: [assignments | program arrays], 16-byte aligned pieces
+    std::vector<std::pair<const void*, size_t>> parts = {
+        {assign, sizeof(double) * (size_t)n * p},
+        {pg->node_feature, 4 * (size_t)pg->n_nodes}, {pg->node_left, 4 * (size_t)pg->n_nodes},
+        {pg->node_right, 4 * (size_t)pg->n_nodes}, {pg->node_threshold, 8 * (size_t)pg->n_nodes},
+        {pg->node_value, 8 * (size_t)pg->n_nodes}, {pg->col_root, 4 * (size_t)pg->n_cols},
+        {pg->col_model_first, 4 * (size_t)pg->n_cols}, {pg->col_model_count, 4 * (size_t)pg->n_cols},
+        {pg->model_key, 8 * (size_t)pg->n_models}, {pg->model_term_first, 4 * (size_t)pg->n_models},
+        {pg->model_term_count, 4 * (size_t)pg->n_models}, {pg->term_kind, 4 * (size_t)pg->n_terms},
+        {pg->term_p1, 4 * (size_t)pg->n_terms}, {pg->term_p2, 4 * (size_t)pg->n_terms},
+        {pg->term_coef, 8 * (size_t)pg->n_terms}, {pg->binary_pos, 4 * (size_t)pg->n_binary}};
+    std::vector<size_t> off(parts.size());
+    size_t total = 0;
+    for (size_t k = 0; k < parts.size(); ++k) { off[k] = total; total += (parts[k].second + 15) & ~(size_t)15; }
+    std::vector<unsigned char> blob(std::max<size_t>(total, 16), 0);
+    for (size_t k = 0; k < parts.size(); ++k)
+        if (parts[k].second) std::memcpy(blob.data() + off[k], parts[k].first, parts[k].second);
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(ctx->model_blob.ensure(blob.size()));
+    CT_CUDA(cudaMemcpyAsync(ctx->model_blob.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+    unsigned char* d = ctx->model_blob.p;
+    ModelProgramDev m;
+    m.n_cols = pg->n_cols; m.n_params = p; m.n_binary = pg->n_binary;
+    m.node_feature = (const int32_t*)(d + off[1]); m.node_left = (const int32_t*)(d + off[2]);
+    m.node_right = (const int32_t*)(d + off[3]); m.node_threshold = (const double*)(d + off[4]);
+    m.node_value = (const double*)(d + off[5]); m.col_root = (const int32_t*)(d + off[6]);
+    m.col_model_first = (const int32_t*)(d + off[7]); m.col_model_count = (const int32_t*)(d + off[8]);
+    m.model_key = (const uint64_t*)(d + off[9]); m.model_term_first = (const int32_t*)(d + off[10]);
+    m.model_term_count = (const int32_t*)(d + off[11]); m.term_kind = (const int32_t*)(d + off[12]);
+    m.term_p1 = (const int32_t*)(d + off[13]); m.term_p2 = (const int32_t*)(d + off[14]);
+    m.term_coef = (const double*)(d + off[15]); m.binary_pos = (const int32_t*)(d + off[16]);
+    const int64_t ld = (n + 2047) / 2048 * 2048;
+    CT_CUDA(ctx->table.ensure((size_t)ld * pg->n_cols));
+    CT_CUDA(cudaMemsetAsync(ctx->table.p, 0, sizeof(double) * (size_t)ld * pg->n_cols, s));
+    CT_CUDA(ctx->model_out.ensure((size_t)n * pg->n_cols));
+    const int64_t work = n * pg->n_cols;
+    k_model_predict<<<(int)std::min<int64_t>((work + 255) / 256, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+        m, (const double*)(d + off[0]), n, ctx->model_out.p, ctx->table.p, ld);
+    CT_CUDA(cudaGetLastError());
+    std::vector<double> host;
+    double* dst = out_rowmajor;
+    if (!dst) { host.resize((size_t)n * pg->n_cols); dst = host.data(); }
+    CT_CUDA(cudaMemcpyAsync(dst, ctx->model_out.p, sizeof(double) * (size_t)n * pg->n_cols,
+                            cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
+    ctx->n = n;
+    ctx->ld = ld;
+    ctx->n_counters = pg->n_cols;
+    ctx->col_cert = certified_columns(dst, n, pg->n_cols);
     return CT_OK;
 }
 

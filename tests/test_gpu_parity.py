@@ -281,3 +281,19 @@ def test_sequential_redecision_path_matches_reference(monkeypatch):
     for r in range(reps):
         assert idx[r, :nst[r]].tolist() == want[r]
     assert stats.uncertified == stats.draws > 0
+
+
+@pytest.mark.parametrize("name,family", [("gradient", "tree"), ("coulomb", "tree"),
+                                         ("gradient", "regression"),
+                                         ("coulomb", "regression"), ("conv", "regression")])
+def test_gpu_model_inference_matches_reference_table(name, family):
+    """ct_model_predict == the reference's PredictionTable.from_model_set."""
+    import os
+    from conftest import GOLDEN
+    from paper_2102_05297_b200 import models, spaces
+    from paper_2102_05297_b200.search import PredictionTable
+    ms = models.load_model_set(os.path.join(GOLDEN, "models", f"{name}_{family}.json"))
+    want = np.load(os.path.join(GOLDEN, "models", "tables.npz"))[f"{name}_{family}_matrix"]
+    ds = dataset_from_golden("gradient") if name == "gradient" else spaces.SPACES[name]()
+    table = PredictionTable.from_model_set(ms, ds.space)
+    np.testing.assert_array_equal(table.matrix.view(np.uint64), want.view(np.uint64))
