@@ -87,7 +87,7 @@ struct ct_ctx {
     int64_t res_reps = 0, res_max_steps = 0;
     bool res_valid = false;
     // scratch
-    DevBuf<u128> scratch_pref;
+    DevBuf<double> scratch_w;
     DevBuf<int32_t> scratch_perm;
     // single-call buffers
     DevBuf<double> vec_a, vec_b;
@@ -484,8 +484,8 @@ int launch_profile_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
     if (occ < 1) return fail(CT_ERR_CUDA, "search kernel does not fit on an SM");
     int grid = std::min(n_reps, occ * ctx->sm_count);
     if (!SMEM) {
-        CT_CUDA(ctx->scratch_pref.ensure((size_t)grid * 32 * (size_t)a.nrows));
-        a.scratch_pref = ctx->scratch_pref.p;
+        CT_CUDA(ctx->scratch_w.ensure((size_t)grid * 32 * (size_t)a.nrows));
+        a.scratch_w = ctx->scratch_w.p;
     }
     kern<<<grid, NT, smem, ctx->stream>>>(a);
     CT_CUDA(cudaGetLastError());
@@ -539,7 +539,7 @@ int ct_destroy(ct_ctx* ctx) {
     ctx->threads.release(); ctx->counters.release(); ctx->has_record.release();
     ctx->stop_bits.release(); ctx->step_index.release(); ctx->step_profiled.release();
     ctx->n_steps.release(); ctx->status.release(); ctx->rep_error.release();
-    ctx->stats.release(); ctx->scratch_pref.release();
+    ctx->stats.release(); ctx->scratch_w.release();
     ctx->scratch_perm.release(); ctx->vec_a.release();
     ctx->vec_b.release(); ctx->mask_a.release(); ctx->mask_b.release(); ctx->key_a.release();
     ctx->key_b.release(); ctx->val_a.release(); ctx->val_b.release(); ctx->cub_tmp.release();
@@ -892,13 +892,12 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     // idle warps at the CTA barrier); CT_SEARCH_NT overrides (benchmarking)
     int nt = n <= 8192 ? 128 : (n <= 65536 ? 256 : 512);
     if (const char* env = std::getenv("CT_SEARCH_NT")) nt = std::atoi(env);
-    // row totals + explored bits always in shared memory; the per-
-    // configuration prefixes too when that still lets all repetitions be
-    // resident at once (one wave), otherwise a per-CTA slice of global
-    // scratch (L2-resident)
+    // row totals + explored bits always in shared memory; the weights too
+    // when that still lets all repetitions be resident at once (one wave),
+    // otherwise a per-CTA slice of global scratch (L2-resident)
     const size_t budget = 200 * 1024;
     const size_t head_b = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
-    const size_t pref_b = 16 * 32 * (size_t)a.nrows;
+    const size_t pref_b = 8 * 32 * (size_t)a.nrows;
     if (head_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the row index");
     const int64_t want_per_sm = std::min<int64_t>(std::min<int64_t>(
         (n_reps + ctx->sm_count - 1) / ctx->sm_count, 32), 2048 / nt);

@@ -10,21 +10,20 @@
 //   all warps  Eq. 16 raw score of every unexplored configuration,
 //              coalesced column reads of the column-major table, pool
 //              max / min / smallest magnitude                          [parallel]
-//   all warps  Eq. 17 weights, exact 2^-66 fixed point, one exact warp
-//              scan per 32-configuration row: every configuration's
-//              in-row inclusive prefix and every row's total are stored [parallel]
+//   all warps  Eq. 17 weights (stored over the raw scores); each 32-
+//              configuration row's exact 2^-66 fixed-point total from
+//              three 32-bit limb reductions (REDUX)                    [parallel]
 //   warp 0     n certified inverse-CDF draws: a ballot over per-lane row
-//              chunks, one 128-bit load per lane and a ballot inside the
-//              row; the drawn weight is subtracted from the stored
-//              prefixes (exact), replay lookups, stop test, argmin with
-//              later ties                                              [serial]
+//              chunks finds the row, one limb scan of that row and a
+//              ballot the configuration; zeroing a drawn weight patches
+//              its row total and the lane prefixes (exact), then replay
+//              lookups, stop test, argmin with later ties              [serial]
 //
 // The serial phases run on one warp while the others wait, so they are kept
-// to a few hundred instructions per draw: no scans, no float<->fixed
-// conversions of whole rows.  The per-configuration prefixes (16 B) live in
-// shared memory when all repetitions still fit on the GPU at once, otherwise
-// in a per-CTA slice of global scratch (L2-resident).  The numpy Generator
-// stream of the repetition is regenerated on the device (ct_rng.cuh).
+// to a few hundred instructions per draw.  The weights live in shared memory
+// when all repetitions still fit on the GPU at once, otherwise in a per-CTA
+// slice of global scratch (L2-resident).  The numpy Generator stream of the
+// repetition is regenerated on the device (ct_rng.cuh).
 #pragma once
 #include "ct_select.cuh"
 #include "ct_expert.cuh"
@@ -82,9 +81,9 @@ struct SearchArgs {
     int32_t nrows;
     int64_t nwords;
     int32_t force_sequential;    // test hook: decide every draw sequentially
-    // storage: per-configuration prefixes (16 B each, nrows * 32) in shared
-    // memory or a per-CTA slice of scratch_pref
-    u128* scratch_pref;
+    // storage: weights (8 B each, nrows * 32) in shared memory or a per-CTA
+    // slice of scratch_w
+    double* scratch_w;
     // outputs
     int32_t* step_index;
     uint8_t* step_profiled;
@@ -122,13 +121,12 @@ struct __align__(16) Ctl {
 };
 
 // Eq. 16 over the whole space for one repetition's active terms: raw score of
-// configuration e into raw[2e] (the low half of its prefix slot), pool max /
-// min / smallest nonzero magnitude returned per thread.  Columns are padded
-// to a multiple of 4*NT, so the four loads of an iteration use one base
-// pointer and immediate offsets.
+// configuration e into w[e], pool max / min / smallest nonzero magnitude
+// returned per thread.  Columns are padded to a multiple of 4*NT, so the four
+// loads of an iteration use one base pointer and immediate offsets.
 template <int NT, bool CERT, int NW>
 __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& ctl,
-                                           const uint32_t* expl, double* raw, double& lmax,
+                                           const uint32_t* expl, double* w, double& lmax,
                                            double& lmin, double& lamin) {
     const int64_t N = a.n;
     const int n_act = ctl.n_act;
@@ -149,7 +147,7 @@ __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& c
             const int64_t e = base + (int64_t)u * NT;
             if (e < N) {
                 const bool in = !bit_get(expl, e);
-                raw[2 * e] = in ? acc[u] : 0.0;
+                w[e] = in ? acc[u] : 0.0;
                 if (in) {
                     lmax = nmax(lmax, acc[u]);
                     lmin = nmin(lmin, acc[u]);
@@ -161,53 +159,29 @@ __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& c
     }
 }
 
-// Eq. 17 weights and the exact in-row prefixes: warp w takes rows w, w+NW, ...
-// lane l converts configuration 32 t + l to fixed point, an exact warp scan
-// gives its inclusive in-row prefix (stored over its raw score) and lane 31
-// holds the row total.
+// Eq. 17 weights over the raw scores and each row's exact total: warp wp
+// takes rows wp, wp+NW, ...; lane l owns configuration 32 t + l (padding
+// lanes write weight 0).
 template <bool CERT>
 __device__ __forceinline__ void weight_pass(const SearchArgs& a, int NW, double smax, double smin,
-                                            const uint32_t* expl, u128* pref, u128* row_tot,
+                                            const uint32_t* expl, double* w, u128* row_tot,
                                             u128& wtot, int& pos, int& bad) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t N = a.n;
     const double gamma = a.gamma;
     const double y_max = rcp_nv(smax), y_min = rcp_nv(smin);
-    const double* raw = reinterpret_cast<const double*>(pref);
     for (int t = warp; t < a.nrows; t += NW) {
         const int64_t e = 32LL * t + lane;
-        u128 f = 0;
-        if (e < N) {
-            double wt = 0.0;
-            if (!bit_get(expl, e)) wt = weight_rcp<CERT>(raw[2 * e], smax, smin, y_max, y_min, gamma);
-            if (!to_fx(wt, &f)) bad = 1;
-            pos += (wt > 0.0);
-        }
-        const u128 incl = warp_incl_scan(f, lane);
-        pref[e] = incl;
-        const u128 tot = shfl_u128(incl, 31);
+        double wt = 0.0;
+        if (e < N && !bit_get(expl, e)) wt = weight_rcp<CERT>(w[e], smax, smin, y_max, y_min, gamma);
+        w[e] = wt;
+        Limbs f;
+        if (!weight_limbs(wt, &f)) bad = 1;
+        pos += (wt > 0.0);
+        const u128 tot = warp_sum_limbs(f);
         if (lane == 0) row_tot[t] = tot;
         wtot += tot;
     }
-}
-
-// Sequential float64 re-decision of an uncertified draw (np.cumsum +
-// searchsorted 'right'), one thread, over the weights recovered exactly from
-// the stored prefixes.  Returns n when r reaches the total.
-__device__ __noinline__ int64_t sequential_select_pref(const u128* pref, int64_t n, double u) {
-    double c = 0.0;
-    for (int64_t e = 0; e < n; ++e) {
-        const u128 prev = (e & 31) ? pref[e - 1] : (u128)0;
-        c = add(c, fx_to_double(pref[e] - prev));
-    }
-    const double r = mul(u, c);
-    double s = 0.0;
-    for (int64_t e = 0; e < n; ++e) {
-        const u128 prev = (e & 31) ? pref[e - 1] : (u128)0;
-        s = add(s, fx_to_double(pref[e] - prev));
-        if (s > r) return e;
-    }
-    return n;
 }
 
 // v * 2^-66 for the draw's r = u * T: within 1 ulp of T (one hardware
@@ -231,17 +205,16 @@ k_profile_search(const SearchArgs a) {
     __shared__ uint32_t seed_sh[SEED_INLINE_WORDS];
     load_seed_words(a.seed, seed_sh);
 
-    // dynamic shared memory: row totals | explored bits | [prefixes]
+    // dynamic shared memory: row totals | explored bits | [weights]
     u128* row_tot = reinterpret_cast<u128*>(smem);
     uint32_t* expl = reinterpret_cast<uint32_t*>(smem + sizeof(u128) * (size_t)a.nrows);
-    u128* pref;
+    double* w;
     if (SMEM) {
         const size_t off = (sizeof(u128) * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
-        pref = reinterpret_cast<u128*>(smem + off);
+        w = reinterpret_cast<double*>(smem + off);
     } else {
-        pref = a.scratch_pref + (size_t)blockIdx.x * 32 * (size_t)a.nrows;
+        w = a.scratch_w + (size_t)blockIdx.x * 32 * (size_t)a.nrows;
     }
-    double* raw = reinterpret_cast<double*>(pref);
 
     for (int rep = blockIdx.x; rep < a.n_reps; rep += gridDim.x) {
         for (int64_t i = tid; i < a.nwords; i += NT) expl[i] = 0u;
@@ -321,8 +294,8 @@ k_profile_search(const SearchArgs a) {
 
             // ---------------- Eq. 16 raw scores (all threads) ------------------
             double lmax = -INFINITY, lmin = INFINITY, lamin = INFINITY;
-            if (ctl.cert_terms) score_pass<NT, true>(a, ctl, expl, raw, lmax, lmin, lamin);
-            else score_pass<NT, false>(a, ctl, expl, raw, lmax, lmin, lamin);
+            if (ctl.cert_terms) score_pass<NT, true>(a, ctl, expl, w, lmax, lmin, lamin);
+            else score_pass<NT, false>(a, ctl, expl, w, lmax, lmin, lamin);
             lmax = warp_max(lmax);
             lmin = warp_min(lmin);
 #pragma unroll
@@ -330,7 +303,7 @@ k_profile_search(const SearchArgs a) {
             if (lane == 0) { ctl.red_max[warp] = lmax; ctl.red_min[warp] = lmin; ctl.red_amin[warp] = lamin; }
             __syncthreads();
 
-            // ---------------- Eq. 17 weights + exact in-row prefixes -----------
+            // ---------------- Eq. 17 weights + exact row totals ----------------
             {
                 double smax = ctl.red_max[0], smin = ctl.red_min[0], amin = ctl.red_amin[0];
 #pragma unroll
@@ -344,8 +317,8 @@ k_profile_search(const SearchArgs a) {
                 const bool cert = (amin >= lo || amin == INFINITY) && smax <= hi && smin >= -hi;
                 u128 wtot = 0;
                 int pos = 0, bad = 0;
-                if (cert) weight_pass<true>(a, NW, smax, smin, expl, pref, row_tot, wtot, pos, bad);
-                else weight_pass<false>(a, NW, smax, smin, expl, pref, row_tot, wtot, pos, bad);
+                if (cert) weight_pass<true>(a, NW, smax, smin, expl, w, row_tot, wtot, pos, bad);
+                else weight_pass<false>(a, NW, smax, smin, expl, w, row_tot, wtot, pos, bad);
                 pos = warp_sum_i(pos);
                 bad = __any_sync(FULL, bad);
                 if (lane == 0) { ctl.red_tot[warp] = wtot; ctl.red_pos[warp] = pos; ctl.red_bad[warp] = bad; }
@@ -402,11 +375,14 @@ k_profile_search(const SearchArgs a) {
                         }
                         row = __shfl_sync(FULL, row, L);
                         carry = shfl_u128(carry, L);
-                        const u128 p = pref[32LL * row + lane];
-                        l2 = __ffs(__ballot_sync(FULL, carry + p > r_fx)) - 1;
-                        const u128 prev = shfl_u128(p, l2 > 0 ? l2 - 1 : 0);
-                        const u128 before = carry + (l2 > 0 ? prev : (u128)0);
-                        wfx = carry + shfl_u128(p, l2) - before;
+                        // exact in-row prefix of the row holding r
+                        Limbs f;
+                        weight_limbs(w[32LL * row + lane], &f);
+                        const u128 incl = warp_incl_scan_limbs(f, lane);
+                        l2 = __ffs(__ballot_sync(FULL, carry + incl > r_fx)) - 1;
+                        const int src = l2 < 0 ? 0 : l2;
+                        wfx = shfl_u128(limbs_value(f.l0, f.l1, f.l2), src);
+                        const u128 before = carry + shfl_u128(incl, src) - wfx;
                         chosen = 32LL * row + l2;
                         // r far enough from both boundaries of the chosen
                         // configuration: the reference's sequential cumsum
@@ -415,13 +391,11 @@ k_profile_search(const SearchArgs a) {
                         ok = ok && !a.force_sequential;
                     }
                     if (!ok) {
-                        if (lane == 0) { chosen = sequential_select_pref(pref, N, u); ++rs.uncert; }
+                        if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
                         chosen = __shfl_sync(FULL, (long long)chosen, 0);
-                        // weight of the re-decided configuration, from its prefixes
                         if (chosen >= 0 && chosen < N) {
                             row = (int)(chosen >> 5); l2 = (int)(chosen & 31);
-                            const u128 pc = pref[chosen];
-                            wfx = pc - (l2 > 0 ? pref[chosen - 1] : (u128)0);
+                            to_fx(w[chosen], &wfx);
                         }
                     }
                     if (lane == 0) ++rs.draws;
@@ -438,11 +412,10 @@ k_profile_search(const SearchArgs a) {
                         }
                         done = 1; break;
                     }
-                    // zero the drawn weight: its own and every later in-row
-                    // prefix, its row total and the lane prefixes drop by wfx
+                    // zero the drawn weight: its row total and the lane
+                    // prefixes drop by wfx (exact)
                     __syncwarp();
-                    if (lane >= l2) pref[32LL * row + lane] -= wfx;
-                    if (lane == 0) row_tot[row] -= wfx;
+                    if (lane == 0) { w[chosen] = 0.0; row_tot[row] -= wfx; }
                     if (row >= t0 && row < t1) mine -= wfx;
                     if (row < t1) lane_pref -= wfx;
                     total -= wfx;
