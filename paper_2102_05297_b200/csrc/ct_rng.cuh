@@ -118,13 +118,30 @@ struct Pcg64 {
         u32 = 0;
     }
 
-    CT_HD uint64_t next64() {
-        step();
-        uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+    // XSL-RR output of a state
+    CT_HD static uint64_t output(u128 s) {
+        uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
         uint64_t x = hi ^ lo;
         unsigned rot = (unsigned)(hi >> 58);
         return (x >> rot) | (x << ((64u - rot) & 63u));
     }
+
+    CT_HD uint64_t next64() {
+        step();
+        return output(state);
+    }
+
+    // Jump-ahead: k steps map state s to A_k s + C_k inc with A_k = M^k,
+    // C_k = M^(k-1) + ... + 1 (mod 2^128); jump_tables fills k = 0..kmax.
+    CT_HD static void jump_tables(u128* A, u128* C, int kmax) {
+        A[0] = 1; C[0] = 0;
+        for (int k = 0; k < kmax; ++k) { A[k + 1] = A[k] * mult(); C[k + 1] = C[k] * mult() + 1; }
+    }
+    // Generator.random() that the (k)th next call would return, k = 1, 2, ...
+    CT_HD double double_after(u128 Ak, u128 Ck) const {
+        return (double)(output(Ak * state + Ck * inc) >> 11) * (1.0 / 9007199254740992.0);
+    }
+    CT_HD void advance(u128 Ak, u128 Ck) { state = Ak * state + Ck * inc; }
 
     CT_HD uint32_t next32() {
         if (has32) { has32 = 0; return u32; }

@@ -203,6 +203,9 @@ k_profile_search(const SearchArgs a) {
     const int64_t N = a.n;
 
     __shared__ uint32_t seed_sh[SEED_INLINE_WORDS];
+    // PCG64 jump-ahead tables: k steps = (A_k, C_k), k = 0..32
+    __shared__ u128 jA[33], jC[33];
+    if (tid == 0) Pcg64::jump_tables(jA, jC, 32);
     load_seed_words(a.seed, seed_sh);
 
     // dynamic shared memory: row totals | explored bits | [weights]
@@ -349,89 +352,121 @@ k_profile_search(const SearchArgs a) {
                 int done = 0;
                 if (bad) { if (lane == 0) { rs.st = CT_STATUS_ERROR; rs.err = -7; } done = 1; }
                 double t_best = INFINITY;
-                for (int k = 0; k < a.inner && !done; ++k) {
-                    if (positive <= 0) { if (lane == 0) rs.st = CT_STATUS_EXHAUSTED; done = 1; break; }
-                    double u = 0.0;
-                    if (lane == 0) u = rs.rng.next_double();
-                    u = __shfl_sync(FULL, u, 0);
-                    const double r = mul(u, fx_total_to_double(total));
-                    const u128 r_fx = floor_fx(r);
-                    // the lane whose row chunk holds r, then the row, then the
-                    // configuration: one ballot each
-                    int64_t chosen = -1;
-                    bool ok = false;
-                    u128 wfx = 0;
-                    int row = -1, l2 = 0;
-                    const unsigned bal = __ballot_sync(FULL, lane_pref > r_fx);
-                    if (bal) {
-                        const int L = __ffs(bal) - 1;
-                        u128 carry = lane_pref - mine;
-                        if (lane == L) {
-                            for (int t = t0; t < t1; ++t) {
-                                const u128 nxt = carry + row_tot[t];
-                                if (nxt > r_fx) { row = t; break; }
-                                carry = nxt;
+                // The iteration's uniforms come 32 at a time from the
+                // repetition's PCG64 by jump-ahead (lane j: the (j+1)-th next
+                // Generator.random()), the draws of a chunk touch shared
+                // memory only, and their replay lookups are issued together
+                // afterwards: one L2 round trip per chunk instead of one per
+                // draw.  Draws past a stop / error are discarded (the
+                // repetition ends there, as the reference's loop does).
+                Pcg64 g;
+                g.state = rs.rng.state;
+                g.inc = rs.rng.inc;
+                int k = 0;
+                bool exhausted = false;
+                while (k < a.inner && !done) {
+                    const int k0 = k;
+                    const int cnt = min(32, a.inner - k0);
+                    const double u_lane = (lane < cnt) ? g.double_after(jA[lane + 1], jC[lane + 1]) : 0.0;
+                    int64_t my_choice = -1;
+                    for (; k < k0 + cnt; ++k) {
+                        if (positive <= 0) { exhausted = true; break; }
+                        const double u = __shfl_sync(FULL, u_lane, k - k0);
+                        const double r = mul(u, fx_total_to_double(total));
+                        const u128 r_fx = floor_fx(r);
+                        // the lane whose row chunk holds r, then the row, then
+                        // the configuration: one ballot each
+                        int64_t chosen = -1;
+                        bool ok = false;
+                        u128 wfx = 0;
+                        int row = -1, l2 = 0;
+                        const unsigned bal = __ballot_sync(FULL, lane_pref > r_fx);
+                        if (bal) {
+                            const int L = __ffs(bal) - 1;
+                            u128 carry = lane_pref - mine;
+                            if (lane == L) {
+                                for (int t = t0; t < t1; ++t) {
+                                    const u128 nxt = carry + row_tot[t];
+                                    if (nxt > r_fx) { row = t; break; }
+                                    carry = nxt;
+                                }
+                            }
+                            row = __shfl_sync(FULL, row, L);
+                            carry = shfl_u128(carry, L);
+                            // exact in-row prefix of the row holding r
+                            Limbs f;
+                            weight_limbs(w[32LL * row + lane], &f);
+                            const u128 incl = warp_incl_scan_limbs(f, lane);
+                            l2 = __ffs(__ballot_sync(FULL, carry + incl > r_fx)) - 1;
+                            const int src = l2 < 0 ? 0 : l2;
+                            wfx = shfl_u128(limbs_value(f.l0, f.l1, f.l2), src);
+                            const u128 before = carry + shfl_u128(incl, src) - wfx;
+                            chosen = 32LL * row + l2;
+                            // r far enough from both boundaries of the chosen
+                            // configuration: the reference's sequential cumsum
+                            // picks it too
+                            ok = l2 >= 0 && (r_fx - before > b_fx) && (before + wfx - r_fx - 1 > b_fx);
+                            ok = ok && !a.force_sequential;
+                        }
+                        if (!ok) {
+                            if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
+                            chosen = __shfl_sync(FULL, (long long)chosen, 0);
+                            if (chosen >= 0 && chosen < N) {
+                                row = (int)(chosen >> 5); l2 = (int)(chosen & 31);
+                                to_fx(w[chosen], &wfx);
                             }
                         }
-                        row = __shfl_sync(FULL, row, L);
-                        carry = shfl_u128(carry, L);
-                        // exact in-row prefix of the row holding r
-                        Limbs f;
-                        weight_limbs(w[32LL * row + lane], &f);
-                        const u128 incl = warp_incl_scan_limbs(f, lane);
-                        l2 = __ffs(__ballot_sync(FULL, carry + incl > r_fx)) - 1;
-                        const int src = l2 < 0 ? 0 : l2;
-                        wfx = shfl_u128(limbs_value(f.l0, f.l1, f.l2), src);
-                        const u128 before = carry + shfl_u128(incl, src) - wfx;
-                        chosen = 32LL * row + l2;
-                        // r far enough from both boundaries of the chosen
-                        // configuration: the reference's sequential cumsum
-                        // picks it too
-                        ok = l2 >= 0 && (r_fx - before > b_fx) && (before + wfx - r_fx - 1 > b_fx);
-                        ok = ok && !a.force_sequential;
+                        if (lane == 0) ++rs.draws;
+                        if (lane == k - k0) my_choice = chosen;
+                        if (!(chosen >= 0 && chosen < N)) { ++k; break; }   // recorded as an error below
+                        // zero the drawn weight: its row total and the lane
+                        // prefixes drop by wfx (exact)
+                        __syncwarp();
+                        if (lane == 0) { w[chosen] = 0.0; row_tot[row] -= wfx; }
+                        if (row >= t0 && row < t1) mine -= wfx;
+                        if (row < t1) lane_pref -= wfx;
+                        total -= wfx;
+                        --positive;
+                        __syncwarp();
                     }
-                    if (!ok) {
-                        if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
-                        chosen = __shfl_sync(FULL, (long long)chosen, 0);
-                        if (chosen >= 0 && chosen < N) {
-                            row = (int)(chosen >> 5); l2 = (int)(chosen & 31);
-                            to_fx(w[chosen], &wfx);
-                        }
-                    }
-                    if (lane == 0) ++rs.draws;
-                    const bool in_range = chosen >= 0 && chosen < N;
-                    const int64_t cs = in_range ? chosen : 0;
-                    // the replay lookups of the draw, issued together
-                    const bool rec_ok = in_range && a.has_record[cs];
+                    const int made = k - k0;
+                    g.advance(jA[made], jC[made]);
+                    // replay lookups of the chunk's draws, one per lane
+                    const bool mine_in = lane < made && my_choice >= 0 && my_choice < N;
+                    const int64_t cs = mine_in ? my_choice : 0;
+                    const bool rec_ok = mine_in && a.has_record[cs];
                     const double rt = a.runtime[cs];
                     const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cs);
-                    if (!rec_ok) {
-                        if (lane == 0) {
-                            rs.st = CT_STATUS_ERROR; rs.err = -4;
-                            if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)chosen;
+                    // the reference's bookkeeping, draw by draw
+                    for (int j = 0; j < made; ++j) {
+                        const int64_t cj = __shfl_sync(FULL, (long long)my_choice, j);
+                        const bool okj = __shfl_sync(FULL, rec_ok, j);
+                        const double rtj = __shfl_sync(FULL, rt, j);
+                        const bool stj = __shfl_sync(FULL, is_stop, j);
+                        if (!okj) {
+                            if (lane == 0) {
+                                rs.st = CT_STATUS_ERROR; rs.err = -4;
+                                if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)cj;
+                            }
+                            done = 1; break;
                         }
-                        done = 1; break;
+                        if (lane == 0) {
+                            out_idx[rs.ns] = (int32_t)cj; out_prof[rs.ns] = 0; ++rs.ns;
+                            uint32_t m = 1u << (cj & 31);
+                            if (!(expl[cj >> 5] & m)) { expl[cj >> 5] |= m; ++rs.n_expl; }
+                        }
+                        if (stj) {
+                            if (lane == 0) rs.st = CT_STATUS_STOPPED;
+                            done = 1; break;
+                        }
+                        if (rtj <= t_best) { t_best = rtj; if (lane == 0) rs.c_prof = cj; }
                     }
-                    // zero the drawn weight: its row total and the lane
-                    // prefixes drop by wfx (exact)
-                    __syncwarp();
-                    if (lane == 0) { w[chosen] = 0.0; row_tot[row] -= wfx; }
-                    if (row >= t0 && row < t1) mine -= wfx;
-                    if (row < t1) lane_pref -= wfx;
-                    total -= wfx;
-                    --positive;
-                    if (lane == 0) {
-                        out_idx[rs.ns] = (int32_t)chosen; out_prof[rs.ns] = 0; ++rs.ns;
-                        uint32_t m = 1u << (chosen & 31);
-                        if (!(expl[chosen >> 5] & m)) { expl[chosen >> 5] |= m; ++rs.n_expl; }
+                    if (!done && exhausted) {
+                        if (lane == 0) rs.st = CT_STATUS_EXHAUSTED;
+                        done = 1;
                     }
-                    if (is_stop) {
-                        if (lane == 0) rs.st = CT_STATUS_STOPPED;
-                        done = 1; break;
-                    }
-                    if (rt <= t_best) { t_best = rt; if (lane == 0) rs.c_prof = chosen; }
-                    __syncwarp();
                 }
+                if (lane == 0) rs.rng.state = g.state;
                 if (lane == 0) ctl.done = done;
             }
             __syncthreads();
