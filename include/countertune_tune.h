@@ -51,6 +51,17 @@ int ct_tuner_device_info(ct_tuner* t, char* arch, int32_t arch_cap, int32_t* sm_
 int ct_tuner_compile(ct_tuner* t, const char* source, const char* kernel_name,
                      const char* const* options, int32_t n_options, int32_t* variant,
                      char* log, int64_t log_cap);
+/* Compile n_variants variants of one source concurrently on `threads` host
+ * threads (0 = all cores).  Variant i's options are options_flat[
+ * sum(n_options[:i]) .. +n_options[i]).  variants[i] receives the handle (or
+ * -1), status[i] CT_TUNE_OK or the variant's error (a configuration NVRTC
+ * rejects is CT_TUNE_ERR_COMPILE, like an invalid configuration in the
+ * reference's runner protocol, search.py:241-253).  Returns CT_TUNE_OK when
+ * the batch itself ran; ct_tune_last_error() holds the first variant error. */
+int ct_tuner_compile_batch(ct_tuner* t, const char* source, const char* kernel_name,
+                           const char* const* options_flat, const int32_t* n_options,
+                           int32_t n_variants, int32_t threads, int32_t* variants,
+                           int32_t* status);
 /* registers / static smem / max threads per block of a loaded variant */
 int ct_tuner_variant_info(ct_tuner* t, int32_t variant, int32_t* regs, int32_t* static_smem,
                           int32_t* max_threads);

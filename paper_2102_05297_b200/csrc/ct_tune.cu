@@ -21,6 +21,8 @@
 #include <cupti_target.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -28,6 +30,43 @@
 #include "countertune_tune.h"
 
 namespace {
+
+// Driver API through the runtime's entry-point table: the library links
+// only cudart/NVRTC/CUPTI, so it loads (and reports "no CUDA device") on a
+// host without the driver, like libct_b200.so.
+struct DriverTable {
+#define CT_DRV(fn) decltype(&::fn) fn = nullptr;
+    CT_DRV(cuInit) CT_DRV(cuDeviceGet) CT_DRV(cuDevicePrimaryCtxRetain)
+    CT_DRV(cuDevicePrimaryCtxRelease) CT_DRV(cuCtxSetCurrent) CT_DRV(cuGetErrorString)
+    CT_DRV(cuModuleLoadData) CT_DRV(cuModuleGetFunction) CT_DRV(cuModuleUnload)
+    CT_DRV(cuFuncGetAttribute) CT_DRV(cuFuncSetAttribute) CT_DRV(cuLaunchKernel)
+#undef CT_DRV
+    bool ready = false;
+};
+DriverTable D;
+
+bool load_driver() {
+    if (D.ready) return true;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) return false;
+    bool ok = true;
+#define CT_DRV(fn)                                                                           \
+    {                                                                                        \
+        void* p_ = nullptr;                                                                  \
+        cudaDriverEntryPointQueryResult q_;                                                  \
+        if (cudaGetDriverEntryPoint(#fn, &p_, cudaEnableDefault, &q_) != cudaSuccess ||      \
+            q_ != cudaDriverEntryPointSuccess || !p_)                                        \
+            ok = false;                                                                      \
+        D.fn = reinterpret_cast<decltype(D.fn)>(p_);                                         \
+    }
+    CT_DRV(cuInit) CT_DRV(cuDeviceGet) CT_DRV(cuDevicePrimaryCtxRetain)
+    CT_DRV(cuDevicePrimaryCtxRelease) CT_DRV(cuCtxSetCurrent) CT_DRV(cuGetErrorString)
+    CT_DRV(cuModuleLoadData) CT_DRV(cuModuleGetFunction) CT_DRV(cuModuleUnload)
+    CT_DRV(cuFuncGetAttribute) CT_DRV(cuFuncSetAttribute) CT_DRV(cuLaunchKernel)
+#undef CT_DRV
+    D.ready = ok;
+    return ok;
+}
 
 thread_local std::string g_err;
 
@@ -38,7 +77,7 @@ int fail(int code, const std::string& msg) {
 
 std::string cu_msg(CUresult r) {
     const char* s = nullptr;
-    cuGetErrorString(r, &s);
+    if (D.cuGetErrorString) D.cuGetErrorString(r, &s);
     return s ? s : "unknown CUDA driver error";
 }
 
@@ -97,7 +136,7 @@ namespace {
 int activate(ct_tuner* t) {
     if (!t) return fail(CT_TUNE_ERR_VALUE, "null tuner");
     TU_RT(cudaSetDevice(t->device));
-    TU_CU(cuCtxSetCurrent(t->ctx));
+    TU_CU(D.cuCtxSetCurrent(t->ctx));
     return CT_TUNE_OK;
 }
 
@@ -108,16 +147,60 @@ int get_variant(ct_tuner* t, int32_t v, Variant** out) {
     return CT_TUNE_OK;
 }
 
+// NVRTC: source + -D options -> cubin for this device (thread-safe).
+bool compile_cubin(const std::string& arch, const char* source, const char* const* options,
+                   int32_t n_options, std::vector<char>* cubin, std::string* log) {
+    nvrtcProgram prog;
+    nvrtcResult nr = nvrtcCreateProgram(&prog, source, "variant.cu", 0, nullptr, nullptr);
+    if (nr != NVRTC_SUCCESS) { *log = nvrtcGetErrorString(nr); return false; }
+    std::vector<std::string> opts = {"--gpu-architecture=" + arch, "--std=c++17",
+                                     "--device-as-default-execution-space", "-lineinfo"};
+    for (int i = 0; i < n_options; ++i) opts.emplace_back(options[i]);
+    std::vector<const char*> optp;
+    for (auto& o : opts) optp.push_back(o.c_str());
+    nr = nvrtcCompileProgram(prog, (int)optp.size(), optp.data());
+    size_t log_size = 0;
+    nvrtcGetProgramLogSize(prog, &log_size);
+    log->assign(log_size, '\0');
+    if (log_size) nvrtcGetProgramLog(prog, &(*log)[0]);
+    if (!log->empty() && log->back() == '\0') log->pop_back();
+    if (nr != NVRTC_SUCCESS) {
+        *log = std::string(nvrtcGetErrorString(nr)) + "\n" + *log;
+        nvrtcDestroyProgram(&prog);
+        return false;
+    }
+    size_t cubin_size = 0;
+    nvrtcGetCUBINSize(prog, &cubin_size);
+    cubin->resize(cubin_size);
+    nvrtcGetCUBIN(prog, cubin->data());
+    nvrtcDestroyProgram(&prog);
+    return true;
+}
+
+int load_variant(ct_tuner* t, const std::vector<char>& cubin, const char* name, int32_t* variant) {
+    Variant v;
+    CUresult r = D.cuModuleLoadData(&v.mod, cubin.data());
+    if (r != CUDA_SUCCESS) return fail(CT_TUNE_ERR_COMPILE, "cuModuleLoadData: " + cu_msg(r));
+    r = D.cuModuleGetFunction(&v.fn, v.mod, name);
+    if (r != CUDA_SUCCESS) {
+        D.cuModuleUnload(v.mod);
+        return fail(CT_TUNE_ERR_COMPILE, std::string("kernel ") + name + " not found: " + cu_msg(r));
+    }
+    t->variants.push_back(v);
+    *variant = (int32_t)t->variants.size() - 1;
+    return CT_TUNE_OK;
+}
+
 int launch_once(ct_tuner* t, Variant* var, const ct_launch* l) {
     std::vector<void*> params((size_t)std::max(l->n_args, 0));
     for (int i = 0; i < l->n_args; ++i)
         params[i] = const_cast<char*>(static_cast<const char*>(l->args) + l->arg_offsets[i]);
     if (l->dynamic_smem > var->smem_attr && l->dynamic_smem > 48 * 1024) {
-        TU_CU(cuFuncSetAttribute(var->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+        TU_CU(D.cuFuncSetAttribute(var->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                                  (int)l->dynamic_smem));
         var->smem_attr = l->dynamic_smem;
     }
-    CUresult r = cuLaunchKernel(var->fn, l->grid[0], l->grid[1], l->grid[2], l->block[0],
+    CUresult r = D.cuLaunchKernel(var->fn, l->grid[0], l->grid[1], l->grid[2], l->block[0],
                                 l->block[1], l->block[2], l->dynamic_smem, (CUstream)t->stream,
                                 params.data(), nullptr);
     if (r != CUDA_SUCCESS) return fail(CT_TUNE_ERR_LAUNCH, "cuLaunchKernel: " + cu_msg(r));
@@ -200,11 +283,12 @@ const char* ct_tune_last_error(void) { return g_err.c_str(); }
 int ct_tuner_create(int device, ct_tuner** out) {
     if (!out) return fail(CT_TUNE_ERR_VALUE, "null output");
     *out = nullptr;
-    TU_CU(cuInit(0));
+    if (!load_driver()) return fail(CT_TUNE_ERR_CUDA, "no CUDA device");
+    TU_CU(D.cuInit(0));
     ct_tuner* t = new ct_tuner();
     t->device = device;
-    CUresult r = cuDeviceGet(&t->dev, device);
-    if (r == CUDA_SUCCESS) r = cuDevicePrimaryCtxRetain(&t->ctx, t->dev);
+    CUresult r = D.cuDeviceGet(&t->dev, device);
+    if (r == CUDA_SUCCESS) r = D.cuDevicePrimaryCtxRetain(&t->ctx, t->dev);
     if (r != CUDA_SUCCESS) { delete t; return fail(CT_TUNE_ERR_CUDA, cu_msg(r)); }
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaFree(nullptr);   // bind the runtime to the primary context
@@ -228,7 +312,7 @@ int ct_tuner_create(int device, ct_tuner** out) {
 int ct_tuner_destroy(ct_tuner* t) {
     if (!t) return CT_TUNE_OK;
     cudaSetDevice(t->device);
-    cuCtxSetCurrent(t->ctx);
+    D.cuCtxSetCurrent(t->ctx);
     cudaStreamSynchronize(t->stream);
     if (t->rp) {
         CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
@@ -236,13 +320,13 @@ int ct_tuner_destroy(ct_tuner* t) {
         cuptiRangeProfilerDisable(&dp);
     }
     for (auto& v : t->variants)
-        if (v.mod) cuModuleUnload(v.mod);
+        if (v.mod) D.cuModuleUnload(v.mod);
     for (void* p : t->allocs) cudaFree(p);
     if (t->flush) cudaFree(t->flush);
     cudaEventDestroy(t->e0);
     cudaEventDestroy(t->e1);
     cudaStreamDestroy(t->stream);
-    cuDevicePrimaryCtxRelease(t->dev);
+    D.cuDevicePrimaryCtxRelease(t->dev);
     delete t;
     return CT_TUNE_OK;
 }
@@ -264,42 +348,58 @@ int ct_tuner_compile(ct_tuner* t, const char* source, const char* name, const ch
     int rc = activate(t); if (rc) return rc;
     if (!source || !name || !variant || n_options < 0 || (n_options && !options))
         return fail(CT_TUNE_ERR_VALUE, "bad compile arguments");
-    nvrtcProgram prog;
-    nvrtcResult nr = nvrtcCreateProgram(&prog, source, "variant.cu", 0, nullptr, nullptr);
-    if (nr != NVRTC_SUCCESS) return fail(CT_TUNE_ERR_COMPILE, nvrtcGetErrorString(nr));
-    std::vector<std::string> opts = {"--gpu-architecture=" + t->arch, "--std=c++17",
-                                     "--device-as-default-execution-space"};
-    for (int i = 0; i < n_options; ++i) opts.emplace_back(options[i]);
-    std::vector<const char*> optp;
-    for (auto& o : opts) optp.push_back(o.c_str());
-    nr = nvrtcCompileProgram(prog, (int)optp.size(), optp.data());
-    size_t log_size = 0;
-    nvrtcGetProgramLogSize(prog, &log_size);
-    std::string plog(log_size, '\0');
-    if (log_size) nvrtcGetProgramLog(prog, &plog[0]);
+    std::vector<char> cubin;
+    std::string plog;
+    bool ok = compile_cubin(t->arch, source, options, n_options, &cubin, &plog);
     if (log && log_cap > 0) {
         std::strncpy(log, plog.c_str(), (size_t)log_cap - 1);
         log[log_cap - 1] = 0;
     }
-    if (nr != NVRTC_SUCCESS) {
-        nvrtcDestroyProgram(&prog);
-        return fail(CT_TUNE_ERR_COMPILE, std::string(nvrtcGetErrorString(nr)) + "\n" + plog);
+    if (!ok) return fail(CT_TUNE_ERR_COMPILE, plog);
+    return load_variant(t, cubin, name, variant);
+}
+
+int ct_tuner_compile_batch(ct_tuner* t, const char* source, const char* name,
+                           const char* const* options_flat, const int32_t* n_options,
+                           int32_t n_variants, int32_t threads, int32_t* variants,
+                           int32_t* status) {
+    int rc = activate(t); if (rc) return rc;
+    if (!source || !name || n_variants < 0 || (n_variants && (!n_options || !variants || !status)))
+        return fail(CT_TUNE_ERR_VALUE, "bad compile_batch arguments");
+    std::vector<int64_t> first(n_variants + 1, 0);
+    for (int i = 0; i < n_variants; ++i) {
+        if (n_options[i] < 0) return fail(CT_TUNE_ERR_VALUE, "negative option count");
+        first[i + 1] = first[i] + n_options[i];
     }
-    size_t cubin_size = 0;
-    nvrtcGetCUBINSize(prog, &cubin_size);
-    std::vector<char> cubin(cubin_size);
-    nvrtcGetCUBIN(prog, cubin.data());
-    nvrtcDestroyProgram(&prog);
-    Variant v;
-    CUresult r = cuModuleLoadData(&v.mod, cubin.data());
-    if (r != CUDA_SUCCESS) return fail(CT_TUNE_ERR_COMPILE, "cuModuleLoadData: " + cu_msg(r));
-    r = cuModuleGetFunction(&v.fn, v.mod, name);
-    if (r != CUDA_SUCCESS) {
-        cuModuleUnload(v.mod);
-        return fail(CT_TUNE_ERR_COMPILE, std::string("kernel ") + name + " not found: " + cu_msg(r));
+    if (first[n_variants] && !options_flat) return fail(CT_TUNE_ERR_VALUE, "null options");
+    std::vector<std::vector<char>> cubins(n_variants);
+    std::vector<std::string> logs(n_variants);
+    std::vector<char> ok(n_variants, 0);
+    int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    nt = std::min(nt, std::max(n_variants, 1));
+    std::atomic<int> next{0};
+    auto worker = [&]() {
+        for (int i = next++; i < n_variants; i = next++)
+            ok[i] = compile_cubin(t->arch, source, options_flat + first[i], n_options[i],
+                                  &cubins[i], &logs[i]);
+    };
+    std::vector<std::thread> pool;
+    for (int k = 1; k < nt; ++k) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    // modules are loaded on the calling thread, into the tuner's context
+    std::string first_err;
+    for (int i = 0; i < n_variants; ++i) {
+        variants[i] = -1;
+        if (!ok[i]) {
+            status[i] = CT_TUNE_ERR_COMPILE;
+            if (first_err.empty()) first_err = logs[i];
+            continue;
+        }
+        status[i] = load_variant(t, cubins[i], name, &variants[i]);
+        if (status[i] && first_err.empty()) first_err = g_err;
     }
-    t->variants.push_back(v);
-    *variant = (int32_t)t->variants.size() - 1;
+    g_err = first_err;
     return CT_TUNE_OK;
 }
 
@@ -309,10 +409,10 @@ int ct_tuner_variant_info(ct_tuner* t, int32_t variant, int32_t* regs, int32_t* 
     Variant* v = nullptr;
     rc = get_variant(t, variant, &v); if (rc) return rc;
     int a = 0;
-    if (regs) { TU_CU(cuFuncGetAttribute(&a, CU_FUNC_ATTRIBUTE_NUM_REGS, v->fn)); *regs = a; }
-    if (smem) { TU_CU(cuFuncGetAttribute(&a, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, v->fn)); *smem = a; }
+    if (regs) { TU_CU(D.cuFuncGetAttribute(&a, CU_FUNC_ATTRIBUTE_NUM_REGS, v->fn)); *regs = a; }
+    if (smem) { TU_CU(D.cuFuncGetAttribute(&a, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, v->fn)); *smem = a; }
     if (max_threads) {
-        TU_CU(cuFuncGetAttribute(&a, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, v->fn));
+        TU_CU(D.cuFuncGetAttribute(&a, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, v->fn));
         *max_threads = a;
     }
     return CT_TUNE_OK;
@@ -322,7 +422,7 @@ int ct_tuner_unload(ct_tuner* t, int32_t variant) {
     int rc = activate(t); if (rc) return rc;
     Variant* v = nullptr;
     rc = get_variant(t, variant, &v); if (rc) return rc;
-    TU_CU(cuModuleUnload(v->mod));
+    TU_CU(D.cuModuleUnload(v->mod));
     v->mod = nullptr;
     v->fn = nullptr;
     return CT_TUNE_OK;

@@ -9,21 +9,32 @@ import pytest
 from conftest import ROOT, have_gpu
 
 
-def declared_symbols():
-    names = set()
-    inc = os.path.join(ROOT, "include")
-    for fn in os.listdir(inc):
-        if fn.endswith(".h"):
-            text = open(os.path.join(inc, fn)).read()
-            text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-            names.update(re.findall(r"\b(ct_[a-z0-9_]+)\s*\(", text))
-    return names
+def declared_symbols(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(ct_[a-z0-9_]+)\s*\(", text))
+
+
+def test_every_header_is_checked():
+    assert sorted(f for f in os.listdir(os.path.join(ROOT, "include")) if f.endswith(".h")) == \
+        ["countertune_b200.h", "countertune_tune.h"]
+
+
+def test_tuner_library_exports_every_declared_symbol():
+    from paper_2102_05297_b200 import tuner
+    lib = tuner.library()
+    declared = declared_symbols("countertune_tune.h")
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(tuner.SIGNATURES), "ctypes binding and header disagree"
+    assert lib.ct_tune_abi_version() == 1
 
 
 def test_library_exports_every_declared_symbol():
     from paper_2102_05297_b200 import _native
     lib = _native.library()
-    declared = declared_symbols()
+    declared = declared_symbols("countertune_b200.h")
     assert len(declared) >= 18
     for name in declared:
         assert hasattr(lib, name), name
