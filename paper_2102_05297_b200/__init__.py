@@ -13,7 +13,7 @@ from .errors import (AnalysisError, CounterTuneError, ParameterMismatchError,
 from .harness import (ConvergenceReport, ExperimentSpec, pair_with_baseline, report,
                       simulate)
 from .search import (DatasetReplaySource, ExactModelSet, Measurement, PredictionTable,
-                     ScoreVector, SearchTrace, SubprocessMeasurementSource, TraceStep,
+                     ProfileSearcher, ScoreVector, SearchTrace, SubprocessMeasurementSource, TraceStep,
                      normalize_scores, run_profile_search, run_random_search,
                      score_configurations, weighted_select)
 from .space import (Dataset, MeasurementRecord, TuningConfiguration, TuningParameter,

@@ -21,6 +21,8 @@
 #include <cupti_target.h>
 
 #include <algorithm>
+#include <map>
+#include <memory>
 #include <atomic>
 #include <thread>
 #include <cstring>
@@ -112,6 +114,24 @@ struct Variant {
 
 }  // namespace
 
+namespace {
+// Host configuration of a metric set: config image + pass count.
+struct HostConfig {
+    CUpti_Profiler_Host_Object* host = nullptr;
+    std::vector<uint8_t> image;
+    size_t passes = 0;
+    std::vector<uint8_t> counter_data;   // one-range counter data image
+    ~HostConfig() {
+        if (host) {
+            CUpti_Profiler_Host_Deinitialize_Params dp = {sizeof(CUpti_Profiler_Host_Deinitialize_Params)};
+            dp.pHostObject = host;
+            cuptiProfilerHostDeinitialize(&dp);
+        }
+    }
+};
+
+}  // namespace
+
 struct ct_tuner {
     int device = 0;
     CUdevice dev = 0;
@@ -129,6 +149,8 @@ struct ct_tuner {
     std::string chip;
     std::vector<uint8_t> avail;
     CUpti_RangeProfiler_Object* rp = nullptr;
+    // host configurations by metric set (building one costs milliseconds)
+    std::map<std::string, std::unique_ptr<HostConfig>> configs;
 };
 
 namespace {
@@ -229,20 +251,6 @@ int cupti_init(ct_tuner* t) {
     return CT_TUNE_OK;
 }
 
-// Host configuration of a metric set: config image + pass count.
-struct HostConfig {
-    CUpti_Profiler_Host_Object* host = nullptr;
-    std::vector<uint8_t> image;
-    size_t passes = 0;
-    ~HostConfig() {
-        if (host) {
-            CUpti_Profiler_Host_Deinitialize_Params dp = {sizeof(CUpti_Profiler_Host_Deinitialize_Params)};
-            dp.pHostObject = host;
-            cuptiProfilerHostDeinitialize(&dp);
-        }
-    }
-};
-
 int host_config(ct_tuner* t, const char* const* metrics, int32_t n, HostConfig* hc) {
     CUpti_Profiler_Host_Initialize_Params hp = {sizeof(CUpti_Profiler_Host_Initialize_Params)};
     hp.profilerType = CUPTI_PROFILER_TYPE_RANGE_PROFILER;
@@ -269,6 +277,20 @@ int host_config(ct_tuner* t, const char* const* metrics, int32_t n, HostConfig* 
     np.pConfigImage = hc->image.data();
     TU_CUPTI(cuptiProfilerHostGetNumOfPasses(&np));
     hc->passes = np.numOfPasses;
+    return CT_TUNE_OK;
+}
+
+// cached host configuration of a metric set
+int host_config_cached(ct_tuner* t, const char* const* metrics, int32_t n, HostConfig** out) {
+    std::string key;
+    for (int i = 0; i < n; ++i) { key += metrics[i]; key += '\n'; }
+    auto it = t->configs.find(key);
+    if (it == t->configs.end()) {
+        std::unique_ptr<HostConfig> hc(new HostConfig());
+        int rc = host_config(t, metrics, n, hc.get()); if (rc) return rc;
+        it = t->configs.emplace(key, std::move(hc)).first;
+    }
+    *out = it->second.get();
     return CT_TUNE_OK;
 }
 
@@ -314,6 +336,7 @@ int ct_tuner_destroy(ct_tuner* t) {
     cudaSetDevice(t->device);
     D.cuCtxSetCurrent(t->ctx);
     cudaStreamSynchronize(t->stream);
+    t->configs.clear();
     if (t->rp) {
         CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
         dp.pRangeProfilerObject = t->rp;
@@ -497,9 +520,9 @@ int ct_tuner_profile_passes(ct_tuner* t, const char* const* metrics, int32_t n, 
     int rc = activate(t); if (rc) return rc;
     if (!metrics || n < 1 || !passes) return fail(CT_TUNE_ERR_VALUE, "bad metric list");
     rc = cupti_init(t); if (rc) return rc;
-    HostConfig hc;
-    rc = host_config(t, metrics, n, &hc); if (rc) return rc;
-    *passes = (int32_t)hc.passes;
+    HostConfig* hc = nullptr;
+    rc = host_config_cached(t, metrics, n, &hc); if (rc) return rc;
+    *passes = (int32_t)hc->passes;
     return CT_TUNE_OK;
 }
 
@@ -510,17 +533,20 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     Variant* v = nullptr;
     rc = get_variant(t, variant, &v); if (rc) return rc;
     rc = cupti_init(t); if (rc) return rc;
-    HostConfig hc;
-    rc = host_config(t, metrics, n, &hc); if (rc) return rc;
-    // counter data image for one range
-    CUpti_RangeProfiler_GetCounterDataSize_Params cs = {CUpti_RangeProfiler_GetCounterDataSize_Params_STRUCT_SIZE};
-    cs.pRangeProfilerObject = t->rp;
-    cs.pMetricNames = const_cast<const char**>(metrics);
-    cs.numMetrics = (size_t)n;
-    cs.maxNumOfRanges = 1;
-    cs.maxNumRangeTreeNodes = 1;
-    TU_CUPTI(cuptiRangeProfilerGetCounterDataSize(&cs));
-    std::vector<uint8_t> data(cs.counterDataSize, 0);
+    HostConfig* hc = nullptr;
+    rc = host_config_cached(t, metrics, n, &hc); if (rc) return rc;
+    // counter data image for one range (re-initialised per collection)
+    if (hc->counter_data.empty()) {
+        CUpti_RangeProfiler_GetCounterDataSize_Params cs = {CUpti_RangeProfiler_GetCounterDataSize_Params_STRUCT_SIZE};
+        cs.pRangeProfilerObject = t->rp;
+        cs.pMetricNames = const_cast<const char**>(metrics);
+        cs.numMetrics = (size_t)n;
+        cs.maxNumOfRanges = 1;
+        cs.maxNumRangeTreeNodes = 1;
+        TU_CUPTI(cuptiRangeProfilerGetCounterDataSize(&cs));
+        hc->counter_data.assign(cs.counterDataSize, 0);
+    }
+    std::vector<uint8_t>& data = hc->counter_data;
     CUpti_RangeProfiler_CounterDataImage_Initialize_Params ci = {CUpti_RangeProfiler_CounterDataImage_Initialize_Params_STRUCT_SIZE};
     ci.pRangeProfilerObject = t->rp;
     ci.counterDataSize = data.size();
@@ -528,8 +554,8 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     TU_CUPTI(cuptiRangeProfilerCounterDataImageInitialize(&ci));
     CUpti_RangeProfiler_SetConfig_Params sc = {CUpti_RangeProfiler_SetConfig_Params_STRUCT_SIZE};
     sc.pRangeProfilerObject = t->rp;
-    sc.configSize = hc.image.size();
-    sc.pConfig = hc.image.data();
+    sc.configSize = hc->image.size();
+    sc.pConfig = hc->image.data();
     sc.counterDataImageSize = data.size();
     sc.pCounterDataImage = data.data();
     sc.range = CUPTI_UserRange;
@@ -566,7 +592,7 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     dd.pRangeProfilerObject = t->rp;
     TU_CUPTI(cuptiRangeProfilerDecodeData(&dd));
     CUpti_Profiler_Host_EvaluateToGpuValues_Params ev = {sizeof(CUpti_Profiler_Host_EvaluateToGpuValues_Params)};
-    ev.pHostObject = hc.host;
+    ev.pHostObject = hc->host;
     ev.pCounterDataImage = data.data();
     ev.counterDataImageSize = data.size();
     ev.rangeIndex = 0;

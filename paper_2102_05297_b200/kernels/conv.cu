@@ -1,0 +1,160 @@
+// Tunable 2D convolution (FILTER x FILTER taps, zero padding), fp32:
+//   out[y][x] = sum_{fy, fx} in[y + fy - R][x + fx - R] * filt[fy][fx]
+// NVRTC source; tuning parameters arrive as -D<NAME>=<v>.
+//
+//   TBX, TBY    threads per block in x / y
+//   WPTX, WPTY  outputs per thread in x (contiguous) / y (strided by TBY)
+//   VW          floats per output store (WPTX % VW == 0)
+//   LOCAL       0: input straight from global memory
+//               1: block's input tile (+ halo) staged in shared memory
+//               2: as 1, plus a per-thread register window of each input
+//                  row (WPTX + FILTER - 1 values reused by FILTER taps)
+//   PAD         +1 float per shared-memory tile row (LOCAL > 0)
+//   UNROLL_F    fully unroll the filter loops
+//   CACHE_F     filter staged in shared memory (else read through L1)
+//   REVERSE     filter traversal order (fx outer instead of fy outer)
+//
+// The tile lives in dynamic shared memory: the host passes
+// smem_bytes() = 4 * ((TH + F - 1) * (TW + F - 1 + PAD) + CACHE_F * F * F).
+#ifndef TBX
+#define TBX 32
+#endif
+#ifndef TBY
+#define TBY 8
+#endif
+#ifndef WPTX
+#define WPTX 2
+#endif
+#ifndef WPTY
+#define WPTY 2
+#endif
+#ifndef VW
+#define VW 2
+#endif
+#ifndef LOCAL
+#define LOCAL 1
+#endif
+#ifndef PAD
+#define PAD 0
+#endif
+#ifndef UNROLL_F
+#define UNROLL_F 1
+#endif
+#ifndef CACHE_F
+#define CACHE_F 1
+#endif
+#ifndef REVERSE
+#define REVERSE 0
+#endif
+#ifndef FILTER
+#define FILTER 7
+#endif
+
+constexpr int F = FILTER, R = FILTER / 2;
+constexpr int TW = TBX * WPTX, TH = TBY * WPTY;
+constexpr int LW = TW + F - 1, LH = TH + F - 1;   // tile incl. halo
+constexpr int SW = LW + PAD;                      // shared row stride
+constexpr int NT = TBX * TBY;
+constexpr int kUnrollF = UNROLL_F ? F : 1;
+
+template <int V> struct vec_t;
+template <> struct vec_t<1> { typedef float T; };
+template <> struct vec_t<2> { typedef float2 T; };
+template <> struct vec_t<4> { typedef float4 T; };
+typedef vec_t<VW>::T vec;
+
+__device__ __forceinline__ float load_global(const float* __restrict__ in, int width, int height,
+                                             int gx, int gy) {
+    return (gx >= 0 && gx < width && gy >= 0 && gy < height) ? __ldg(in + (size_t)gy * width + gx)
+                                                             : 0.0f;
+}
+
+extern "C" __global__ void __launch_bounds__(NT)
+conv(const float* __restrict__ in, const float* __restrict__ filt, float* __restrict__ out,
+     int width, int height) {
+    extern __shared__ __align__(16) float dsm[];
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TBX + tx;
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+#if CACHE_F
+    float* sf = dsm + (LOCAL ? LH * SW : 0);
+    for (int i = tid; i < F * F; i += NT) sf[i] = filt[i];
+#define FILT(fy, fx) sf[(fy) * F + (fx)]
+#else
+#define FILT(fy, fx) __ldg(filt + (fy) * F + (fx))
+#endif
+#if LOCAL
+    float* tile = dsm;
+    for (int i = tid; i < LH * LW; i += NT) {
+        const int ry = i / LW, rx = i - ry * LW;
+        const int gx = x0 + rx - R, gy = y0 + ry - R;
+        tile[ry * SW + rx] = (gx >= 0 && gx < width && gy >= 0 && gy < height)
+                                 ? __ldg(in + (size_t)gy * width + gx) : 0.0f;
+    }
+#define INPUT(ly, lx) tile[(ly) * SW + (lx)]
+#else
+#define INPUT(ly, lx) load_global(in, width, height, x0 - R + (lx), y0 - R + (ly))
+#endif
+#if CACHE_F || LOCAL
+    __syncthreads();
+#endif
+    float acc[WPTY][WPTX];
+#pragma unroll
+    for (int wy = 0; wy < WPTY; ++wy)
+#pragma unroll
+        for (int i = 0; i < WPTX; ++i) acc[wy][i] = 0.0f;
+
+#pragma unroll
+    for (int wy = 0; wy < WPTY; ++wy) {
+        const int ly = wy * TBY + ty;      // output row inside the tile
+        const int lx = tx * WPTX;          // first output column inside the tile
+#if LOCAL == 2
+#pragma unroll kUnrollF
+        for (int fy = 0; fy < F; ++fy) {
+            float win[WPTX + F - 1];
+#pragma unroll
+            for (int k = 0; k < WPTX + F - 1; ++k) win[k] = INPUT(ly + fy, lx + k);
+#if REVERSE
+#pragma unroll
+            for (int i = 0; i < WPTX; ++i)
+#pragma unroll kUnrollF
+                for (int fx = 0; fx < F; ++fx) acc[wy][i] += win[i + fx] * FILT(fy, fx);
+#else
+#pragma unroll kUnrollF
+            for (int fx = 0; fx < F; ++fx) {
+                const float f = FILT(fy, fx);
+#pragma unroll
+                for (int i = 0; i < WPTX; ++i) acc[wy][i] += win[i + fx] * f;
+            }
+#endif
+        }
+#else
+#if REVERSE
+#pragma unroll kUnrollF
+        for (int fx = 0; fx < F; ++fx)
+#pragma unroll kUnrollF
+            for (int fy = 0; fy < F; ++fy) {
+#else
+#pragma unroll kUnrollF
+        for (int fy = 0; fy < F; ++fy)
+#pragma unroll kUnrollF
+            for (int fx = 0; fx < F; ++fx) {
+#endif
+                const float f = FILT(fy, fx);
+#pragma unroll
+                for (int i = 0; i < WPTX; ++i) acc[wy][i] += INPUT(ly + fy, lx + i + fx) * f;
+            }
+#endif
+    }
+#pragma unroll
+    for (int wy = 0; wy < WPTY; ++wy) {
+        const int y = y0 + wy * TBY + ty;
+        float* row = out + (size_t)y * width + x0 + tx * WPTX;
+#pragma unroll
+        for (int i = 0; i < WPTX; i += VW) {
+            vec v;
+#pragma unroll
+            for (int k = 0; k < VW; ++k) reinterpret_cast<float*>(&v)[k] = acc[wy][i + k];
+            *reinterpret_cast<vec*>(row + i) = v;
+        }
+    }
+}

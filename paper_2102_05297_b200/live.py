@@ -1,0 +1,453 @@
+"""Live measurement path: the five tunable benchmark kernels of the paper
+(Table 2), compiled per configuration with NVRTC for the
+B200, timed with CUDA events and profiled with the CUPTI range profiler.
+
+This is the in-process B200 runner behind the reference's measurement plug
+point (the ``MeasurementSource`` duck type, search.py:188-217; its
+out-of-process form is the line protocol of search.py:220-275):
+
+    src = CudaMeasurementSource(benchmark("transpose"))
+    trace = run_profile_search(src, models, i=40)        # live Alg. 1
+    ds = sweep(src)                                       # exhaustive B200 dataset
+
+* ``src.space`` is the same configuration set as the synthetic stand-in of the
+  same name (``spaces.space_of``), so models, datasets and traces line up.
+* ``measure(idx, profiled=False)`` compiles the variant on first use (cached),
+  times it (median of ``reps`` launches, L2 flushed between them) and returns
+  ``Measurement(runtime_us)``; ``profiled=True`` also collects the paper's
+  counter set (Table 1; ``counters.VOLTA_METRICS``, 24 metrics, 5 replay passes
+  on GB100) and canonicalises it (``counters.canonicalize``,
+  counters.py:161-180) as the reference's runner protocol does
+  (search.py:262).
+* Benchmark inputs are deterministic functions of ``seed``; outputs can be
+  fetched for checking against the numpy oracles (tests only).
+"""
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import counters as cc
+from . import spaces
+from .counters import ArchProfile
+from .errors import CounterTuneError
+from .search import Measurement
+from .space import Dataset
+from .tuner import CompileError, Launch, LaunchError, Tuner
+
+_KDIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "kernels")
+
+# Table-1 metric names in catalog order (the counters the profiled step reports)
+TABLE1_ABBRS: Sequence[str] = tuple(a for a in cc.ABBREVIATIONS if a in cc.VOLTA_METRICS)
+TABLE1_METRICS: Sequence[str] = tuple(cc.VOLTA_METRICS[a][0] for a in TABLE1_ABBRS)
+
+_u64 = ctypes.c_uint64
+_i32 = ctypes.c_int32
+_f32 = ctypes.c_float
+
+
+def b200_arch(sm_count: int = spaces.B200_SMS) -> ArchProfile:
+    """ArchProfile of the device: Volta+ counter dialect, 128 FP32 cores/SM
+    (the b_paral saturation rule of bottlenecks.py:172-173 counts cores)."""
+    return ArchProfile(name="b200", generation=cc.VOLTA_PLUS, cores=int(sm_count) * 128)
+
+
+class Benchmark:
+    """One tunable kernel: its space, NVRTC source, inputs and launch geometry."""
+
+    name = ""
+    kernel = ""
+    bound = ""        # roofline the kernel is judged against
+    unit = ""
+
+    def __init__(self, seed: int = 0):
+        self.seed = seed
+        with open(os.path.join(_KDIR, self.kernel + ".cu")) as f:
+            self.source = f.read()
+        self._space = None
+
+    @property
+    def space(self):
+        if self._space is None:
+            self._space = spaces.space_of(self.name)
+        return self._space
+
+    def values(self, config_index: int) -> Dict[str, int]:
+        row = self.space.assignments[config_index]
+        return {p.name: int(v) for p, v in zip(self.space.parameters, row)}
+
+    def options(self, values: Dict[str, int]) -> List[str]:
+        return [f"-D{k}={v}" for k, v in values.items()] + self.extra_options()
+
+    def extra_options(self) -> List[str]:
+        return []
+
+    # per subclass -----------------------------------------------------------
+    def host_inputs(self) -> Dict[str, np.ndarray]:
+        raise NotImplementedError
+
+    def setup(self, tuner: Tuner) -> Dict[str, int]:
+        """Device buffers (inputs uploaded, outputs allocated)."""
+        raise NotImplementedError
+
+    def launch(self, values: Dict[str, int], bufs: Dict[str, int]) -> Launch:
+        raise NotImplementedError
+
+    def output(self, tuner: Tuner, bufs: Dict[str, int]) -> np.ndarray:
+        raise NotImplementedError
+
+    def work(self) -> float:
+        """Algorithmic bytes (HBM-bound) or flops / interactions per launch."""
+        raise NotImplementedError
+
+
+class TransposeBenchmark(Benchmark):
+    name, kernel, bound, unit = "transpose", "transpose", "hbm", "bytes"
+
+    def __init__(self, width: int = 8192, height: int = 8192, seed: int = 0):
+        super().__init__(seed)
+        if width % 128 or height % 64:
+            raise ValueError("transpose sizes must be multiples of 128 (width) and 64 (height)")
+        self.width, self.height = width, height
+
+    def host_inputs(self):
+        rng = np.random.default_rng(self.seed)
+        return {"in": rng.standard_normal((self.height, self.width), dtype=np.float32)}
+
+    def setup(self, tuner):
+        x = self.host_inputs()["in"]
+        return {"in": tuner.upload(x), "out": tuner.alloc(x.nbytes)}
+
+    def launch(self, v, bufs):
+        tile, work_x = v["TILE"], v["WORK_X"]
+        return Launch((self.width // (tile * work_x), self.height // tile),
+                      (tile // v["VEC"], v["BLOCK_Y"]),
+                      [_u64(bufs["in"]), _u64(bufs["out"]), _i32(self.width), _i32(self.height)])
+
+    def output(self, tuner, bufs):
+        return tuner.d2h(bufs["out"], np.empty((self.width, self.height), np.float32))
+
+    def work(self):
+        return 2.0 * 4.0 * self.width * self.height
+
+
+class CoulombBenchmark(Benchmark):
+    name, kernel, bound, unit = "coulomb", "coulomb", "mufu", "interactions"
+
+    def __init__(self, grid: int = 256, atoms: int = 256, spacing: float = 0.5, seed: int = 0):
+        super().__init__(seed)
+        if grid % 32 or atoms % 256:
+            raise ValueError("coulomb needs grid % 32 == 0 and atoms % 256 == 0")
+        self.grid, self.atoms, self.spacing = grid, atoms, float(np.float32(spacing))
+
+    def host_inputs(self):
+        rng = np.random.default_rng(self.seed)
+        extent = self.grid * self.spacing
+        a = np.empty((self.atoms, 4), np.float32)
+        # atoms between grid planes (never on a grid point)
+        a[:, :3] = (rng.integers(0, self.grid, (self.atoms, 3)) + rng.uniform(0.2, 0.8, (self.atoms, 3))
+                    ) * self.spacing
+        a[:, :3] = np.minimum(a[:, :3], extent)
+        a[:, 3] = rng.uniform(-1.0, 1.0, self.atoms)
+        return {"atoms": a}
+
+    def setup(self, tuner):
+        a = self.host_inputs()["atoms"]
+        soa = np.ascontiguousarray(a.T)
+        out = {"atoms": tuner.upload(a)}
+        for k, name in enumerate("xyzw"):
+            out[name] = tuner.upload(soa[k])
+        out["energy"] = tuner.alloc(4 * self.grid ** 3)
+        return out
+
+    def launch(self, v, bufs):
+        by = v["BLOCK"] // 32
+        z = v["Z_ITERATIONS"]
+        return Launch((self.grid // 32, self.grid // by, -(-self.grid // z)), (32, by),
+                      [_u64(bufs["atoms"]), _u64(bufs["x"]), _u64(bufs["y"]), _u64(bufs["z"]),
+                       _u64(bufs["w"]), _i32(self.atoms), _f32(self.spacing), _i32(self.grid),
+                       _u64(bufs["energy"])])
+
+    def output(self, tuner, bufs):
+        g = self.grid
+        return tuner.d2h(bufs["energy"], np.empty((g, g, g), np.float32))
+
+    def work(self):
+        return float(self.grid) ** 3 * self.atoms
+
+
+class NBodyBenchmark(Benchmark):
+    name, kernel, bound, unit = "nbody", "nbody", "fp32", "interactions"
+
+    def __init__(self, bodies: int = 16384, eps2: float = 0.01, seed: int = 0):
+        super().__init__(seed)
+        if bodies % 1024:
+            raise ValueError("nbody needs bodies % 1024 == 0")
+        self.bodies, self.eps2 = bodies, float(np.float32(eps2))
+
+    def host_inputs(self):
+        rng = np.random.default_rng(self.seed)
+        pm = np.empty((self.bodies, 4), np.float32)
+        pm[:, :3] = rng.standard_normal((self.bodies, 3))
+        pm[:, 3] = rng.uniform(0.5, 1.5, self.bodies)
+        return {"pm": pm}
+
+    def setup(self, tuner):
+        pm = self.host_inputs()["pm"]
+        soa = np.ascontiguousarray(pm.T)
+        out = {"pm": tuner.upload(pm)}
+        for k, name in enumerate(("x", "y", "z", "m")):
+            out[name] = tuner.upload(soa[k])
+        out["acc"] = tuner.alloc(16 * self.bodies)
+        return out
+
+    def launch(self, v, bufs):
+        per_block = v["BLOCK"] * v["OUTER"]
+        return Launch((-(-self.bodies // per_block),), (v["BLOCK"],),
+                      [_u64(bufs["pm"]), _u64(bufs["x"]), _u64(bufs["y"]), _u64(bufs["z"]),
+                       _u64(bufs["m"]), _i32(self.bodies), _f32(self.eps2), _u64(bufs["acc"])])
+
+    def output(self, tuner, bufs):
+        return tuner.d2h(bufs["acc"], np.empty((self.bodies, 4), np.float32))[:, :3]
+
+    def work(self):
+        return float(self.bodies) ** 2
+
+
+class ConvBenchmark(Benchmark):
+    name, kernel, bound, unit = "conv", "conv", "fp32", "flops"
+
+    def __init__(self, width: int = 4096, height: int = 4096, filt: int = 7, seed: int = 0):
+        super().__init__(seed)
+        if width % 512 or height % 128:
+            raise ValueError("conv sizes must be multiples of 512 (width) and 128 (height)")
+        self.width, self.height, self.filt = width, height, filt
+
+    def extra_options(self):
+        return [f"-DFILTER={self.filt}"]
+
+    def host_inputs(self):
+        rng = np.random.default_rng(self.seed)
+        return {"in": rng.standard_normal((self.height, self.width), dtype=np.float32),
+                "filt": rng.uniform(-1, 1, (self.filt, self.filt)).astype(np.float32)}
+
+    def setup(self, tuner):
+        h = self.host_inputs()
+        return {"in": tuner.upload(h["in"]), "filt": tuner.upload(h["filt"]),
+                "out": tuner.alloc(h["in"].nbytes)}
+
+    def smem_bytes(self, v) -> int:
+        f = self.filt
+        tw, th = v["TBX"] * v["WPTX"], v["TBY"] * v["WPTY"]
+        tile = (th + f - 1) * (tw + f - 1 + v["PAD"]) if v["LOCAL"] else 0
+        return 4 * (tile + (f * f if v["CACHE_F"] else 0))
+
+    def launch(self, v, bufs):
+        tw, th = v["TBX"] * v["WPTX"], v["TBY"] * v["WPTY"]
+        return Launch((self.width // tw, self.height // th), (v["TBX"], v["TBY"]),
+                      [_u64(bufs["in"]), _u64(bufs["filt"]), _u64(bufs["out"]),
+                       _i32(self.width), _i32(self.height)], dynamic_smem=self.smem_bytes(v))
+
+    def output(self, tuner, bufs):
+        return tuner.d2h(bufs["out"], np.empty((self.height, self.width), np.float32))
+
+    def work(self):
+        return 2.0 * self.filt ** 2 * self.width * self.height
+
+
+class GemmBenchmark(Benchmark):
+    name, kernel, bound, unit = "gemm", "gemm", "fp32", "flops"
+
+    def __init__(self, m: int = 2048, n: int = 2048, k: int = 2048, seed: int = 0):
+        super().__init__(seed)
+        if m % 128 or n % 128 or k % 32:
+            raise ValueError("gemm sizes must be multiples of 128 (m, n) and 32 (k)")
+        self.m, self.n, self.k = m, n, k
+
+    def host_inputs(self):
+        rng = np.random.default_rng(self.seed)
+        return {"at": rng.uniform(-1, 1, (self.k, self.m)).astype(np.float32),
+                "b": rng.uniform(-1, 1, (self.k, self.n)).astype(np.float32)}
+
+    def setup(self, tuner):
+        h = self.host_inputs()
+        return {"at": tuner.upload(h["at"]), "b": tuner.upload(h["b"]),
+                "c": tuner.alloc(4 * self.m * self.n)}
+
+    def launch(self, v, bufs):
+        return Launch((self.m // v["MWG"], self.n // v["NWG"]), (v["MDIMC"] * v["NDIMC"],),
+                      [_u64(bufs["at"]), _u64(bufs["b"]), _u64(bufs["c"]), _i32(self.m),
+                       _i32(self.n), _i32(self.k)])
+
+    def output(self, tuner, bufs):
+        return tuner.d2h(bufs["c"], np.empty((self.m, self.n), np.float32))
+
+    def work(self):
+        return 2.0 * self.m * self.n * self.k
+
+
+BENCHMARKS = {
+    "transpose": TransposeBenchmark,
+    "coulomb": CoulombBenchmark,
+    "nbody": NBodyBenchmark,
+    "conv": ConvBenchmark,
+    "gemm": GemmBenchmark,
+}
+
+
+def benchmark(name: str, **sizes) -> Benchmark:
+    try:
+        return BENCHMARKS[name](**sizes)
+    except KeyError:
+        raise ValueError(f"unknown benchmark {name!r}; known: {sorted(BENCHMARKS)}")
+
+
+class CudaMeasurementSource:
+    """MeasurementSource over one GPU (search.py:188-217 duck type)."""
+
+    def __init__(self, bench: Benchmark, device: int = 0, tuner: Optional[Tuner] = None,
+                 warmup: int = 1, reps: int = 3, flush_l2: bool = True,
+                 metrics: Sequence[str] = TABLE1_METRICS):
+        self.bench = bench
+        self.tuner = tuner if tuner is not None else Tuner(device)
+        self._own_tuner = tuner is None
+        self.space = bench.space
+        self.arch = b200_arch(self.tuner.sm_count)
+        self.warmup, self.reps, self.flush_l2 = warmup, reps, flush_l2
+        self.metrics = tuple(metrics)
+        self._bufs = bench.setup(self.tuner)
+        self._variants: Dict[int, int] = {}
+        self.profile_passes = 0
+        self.compile_failures: Dict[int, str] = {}
+
+    # -- variants ---------------------------------------------------------
+    def compile_all(self, indices: Optional[Sequence[int]] = None, threads: int = 0) -> int:
+        """Compile the variants of `indices` (default: the whole space)
+        concurrently on host threads; returns how many failed."""
+        idx = [i for i in (range(len(self.space)) if indices is None else indices)
+               if i not in self._variants]
+        if not idx:
+            return 0
+        opts = [self.bench.options(self.bench.values(i)) for i in idx]
+        handles, status = self.tuner.compile_batch(self.bench.source, self.bench.kernel, opts,
+                                                   threads)
+        bad = 0
+        for i, h, st in zip(idx, handles, status):
+            if st == 0:
+                self._variants[i] = int(h)
+            else:
+                self.compile_failures[i] = f"status {int(st)}"
+                bad += 1
+        return bad
+
+    def variant(self, config_index: int) -> int:
+        v = self._variants.get(config_index)
+        if v is None:
+            try:
+                v = self.tuner.compile(self.bench.source, self.bench.kernel,
+                                       self.bench.options(self.bench.values(config_index)))
+            except CompileError as e:
+                raise CounterTuneError(f"configuration {config_index} does not compile: {e}")
+            self._variants[config_index] = v
+        return v
+
+    def launch_of(self, config_index: int) -> Launch:
+        return self.bench.launch(self.bench.values(config_index), self._bufs)
+
+    # -- MeasurementSource ------------------------------------------------
+    def measure(self, config_index: int, profiled: bool) -> Measurement:
+        v = self.variant(config_index)
+        launch = self.launch_of(config_index)
+        try:
+            times = self.tuner.time(v, launch, warmup=self.warmup, reps=self.reps,
+                                    flush_l2=self.flush_l2)
+        except LaunchError as e:
+            raise CounterTuneError(f"configuration {config_index} failed to launch: {e}")
+        runtime = float(np.median(times))
+        if not profiled:
+            return Measurement(runtime_us=runtime)
+        vals, passes = self.tuner.profile(v, launch, self.metrics)
+        self.profile_passes = passes
+        counter_map: Dict[str, float] = {}
+        for name, value in zip(self.metrics, vals):
+            abbr, canonical = cc.canonicalize(name, float(value), self.arch)
+            counter_map[abbr] = canonical
+        return Measurement(runtime_us=runtime, global_threads=launch.threads,
+                           counters=counter_map)
+
+    def output(self, config_index: int) -> np.ndarray:
+        """Run the variant once and fetch its output (for oracle checks)."""
+        v = self.variant(config_index)
+        self.tuner.time(v, self.launch_of(config_index), warmup=1, reps=0, flush_l2=False)
+        return self.bench.output(self.tuner, self._bufs)
+
+    def close(self) -> None:
+        if self._own_tuner and self.tuner is not None:
+            self.tuner.close()
+        self.tuner = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+@dataclass
+class SweepResult:
+    dataset: Dataset
+    failures: Dict[int, str]
+    seconds_compile: float
+    seconds_measure: float
+
+
+def sweep(source: CudaMeasurementSource, profiled: bool = True, checkpoint: Optional[str] = None,
+          compile_threads: int = 0, progress=None) -> SweepResult:
+    """Exhaustive sweep of the source's space -> a replay Dataset in the
+    reference's layout (runtime, threads, the Table-1 counters canonicalised).
+
+    With ``checkpoint`` the partial results are kept in an .npz after every
+    configuration and a rerun resumes from it (config_index order)."""
+    import time
+    n = len(source.space)
+    names = TABLE1_ABBRS
+    runtime = np.full(n, np.nan)
+    threads = np.zeros(n, dtype=np.int64)
+    cm = np.full((n, len(names)), np.nan)
+    done = np.zeros(n, dtype=bool)
+    if checkpoint and os.path.exists(checkpoint):
+        z = np.load(checkpoint)
+        runtime, threads, cm, done = z["runtime"], z["threads"], z["counters"], z["done"]
+    t0 = time.perf_counter()
+    source.compile_all([i for i in range(n) if not done[i]], threads=compile_threads)
+    t1 = time.perf_counter()
+    failures = dict(source.compile_failures)
+    for i in range(n):
+        if done[i] or i in failures:
+            continue
+        try:
+            m = source.measure(i, profiled=profiled)
+        except CounterTuneError as e:
+            failures[i] = str(e)
+            continue
+        runtime[i] = m.runtime_us
+        if profiled:
+            threads[i] = m.global_threads
+            cm[i] = [m.counters[a] for a in names]
+        done[i] = True
+        if checkpoint:
+            np.savez(checkpoint, runtime=runtime, threads=threads, counters=cm, done=done)
+        if progress:
+            progress(i, n)
+    t2 = time.perf_counter()
+    # configurations that failed to build or launch carry no record: replaying
+    # them raises, as the reference's replay source does (search.py:205-214)
+    ds = Dataset(source.space, source.arch, f"{source.bench.name}-b200",
+                 runtime_us=np.where(done, runtime, 1.0), global_threads=np.maximum(1, threads),
+                 counter_names=names if profiled else (),
+                 counter_matrix=np.where(done[:, None], cm, 0.0) if profiled
+                 else np.zeros((n, 0)), has_record=done)
+    return SweepResult(ds, failures, t1 - t0, t2 - t1)

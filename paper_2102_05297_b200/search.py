@@ -479,13 +479,30 @@ def _profile_search_host_driven(source, table, total, *, i, n, seed, inst_reacti
                                 literal_sign, stop_indices, score_top_k) -> SearchTrace:
     """Live sources: the host owns measurement and the numpy Generator; the
     device runs the expert system, scoring, normalisation and every draw."""
-    space = source.space
+    steps = _profile_search_steps(source.space, source.arch, table, total, i=i, n=n, seed=seed,
+                                  inst_reaction=inst_reaction, literal_sign=literal_sign,
+                                  stop_indices=stop_indices, score_top_k=score_top_k)
+    try:
+        request = next(steps)
+        while True:
+            request = steps.send(source.measure(*request))
+    except StopIteration as done:
+        return done.value
+
+
+def _profile_search_steps(space, arch, table, total, *, i, n, seed, inst_reaction,
+                          literal_sign, stop_indices, score_top_k):
+    """run_profile_search (search.py:338-399) as a generator: it yields each
+    empirical test as (config_index, profiled), is sent the Measurement, and
+    returns the SearchTrace.  The RNG is consumed exactly as the reference's
+    loop consumes it, so driving it with source.measure IS the reference's
+    control flow."""
     rng = np.random.default_rng(seed)
     explored = np.zeros(total, dtype=bool)
     steps: List[TraceStep] = []
     c_profile = space.configurations[int(rng.integers(0, total))]
     ctx = _ctx()
-    gen = cc.generation_code(source.arch)
+    gen = cc.generation_code(arch)
 
     def record(idx: int, runtime: float, profiled: bool) -> bool:
         steps.append(TraceStep(step=len(steps) + 1, config_index=idx, runtime_us=runtime,
@@ -494,11 +511,11 @@ def _profile_search_host_driven(source, table, total, *, i, n, seed, inst_reacti
         return stop_indices is not None and idx in stop_indices
 
     for _ in range(i):
-        m = source.measure(c_profile.index, profiled=True)
+        m = yield (c_profile.index, True)
         if record(c_profile.index, m.runtime_us, True):
             return SearchTrace(steps=steps, seed=seed, status=STATUS_STOPPED)
         _check_inst_reaction(inst_reaction)
-        _, deltas, _ = ctx.analyze_react(_counters23(m), gen, source.arch.cores,
+        _, deltas, _ = ctx.analyze_react(_counters23(m), gen, arch.cores,
                                          m.global_threads, inst_reaction)
         delta = dict(zip(cc.DELTA_KEYS, map(float, deltas)))
         if not (~explored).any():
@@ -514,7 +531,7 @@ def _profile_search_host_driven(source, table, total, *, i, n, seed, inst_reacti
                 chosen = weighted_select(scores, rng)
             except SpaceExhaustedError:
                 return SearchTrace(steps=steps, seed=seed, status=STATUS_EXHAUSTED)
-            runtime = source.measure(chosen, profiled=False).runtime_us
+            runtime = (yield (chosen, False)).runtime_us
             scores.norm[chosen] = 0.0
             if record(chosen, runtime, False):
                 return SearchTrace(steps=steps, seed=seed, status=STATUS_STOPPED)
@@ -522,3 +539,67 @@ def _profile_search_host_driven(source, table, total, *, i, n, seed, inst_reacti
                 t_best = runtime
                 c_profile = space.configurations[chosen]
     return SearchTrace(steps=steps, seed=seed, status=STATUS_BUDGET)
+
+
+class ProfileSearcher:
+    """Ask/tell form of the profile searcher (north_star's
+    ``searcher.next_config`` / ``add_result``) for callers that own the
+    measurement loop -- e.g. a tuner that times candidates itself, or the
+    original KTT stub that talked "via files and sockets".
+
+        s = ProfileSearcher(models, space, arch, i=40)
+        while (req := s.next_config()) is not None:
+            idx, profiled = req
+            s.add_result(measure(idx, profiled))
+        trace = s.trace
+
+    It is the inversion of control of run_profile_search (same arguments,
+    same RNG consumption, same trajectory); every numeric step runs on the
+    GPU through libct_b200.so.
+    """
+
+    def __init__(self, models, space, arch, *, i: int, n: int = DEFAULT_INNER_STEPS, seed=0,
+                 inst_reaction: float = DEFAULT_INST_REACTION, literal_sign: bool = False,
+                 stop_indices: Optional[Set[int]] = None, score_top_k: Optional[int] = None):
+        if i < 1:
+            raise ValueError(f"need at least one outer iteration, got i={i}")
+        if n < 0:
+            raise ValueError(f"inner step count must be >= 0, got n={n}")
+        self.space = space
+        self.arch = arch
+        table = _as_table(models, space)
+        self._gen = _profile_search_steps(space, arch, table, len(space), i=i, n=n, seed=seed,
+                                          inst_reaction=inst_reaction, literal_sign=literal_sign,
+                                          stop_indices=stop_indices, score_top_k=score_top_k)
+        self._pending = None
+        self._trace: Optional[SearchTrace] = None
+        self._advance(None, first=True)
+
+    def _advance(self, value, first=False):
+        try:
+            self._pending = next(self._gen) if first else self._gen.send(value)
+        except StopIteration as done:
+            self._pending = None
+            self._trace = done.value
+
+    def next_config(self):
+        """(config_index, profiled) of the next empirical test, or None when
+        the search has finished (budget, stop set or exhausted space)."""
+        return self._pending
+
+    def add_result(self, measurement: Measurement) -> None:
+        """Report the measurement of the configuration next_config() named.
+        A profiled request needs runtime_us, global_threads and counters."""
+        if self._pending is None:
+            raise CounterTuneError("the search has finished; no measurement is pending")
+        self._advance(measurement)
+
+    @property
+    def finished(self) -> bool:
+        return self._pending is None
+
+    @property
+    def trace(self) -> SearchTrace:
+        if self._trace is None:
+            raise CounterTuneError("the search has not finished yet")
+        return self._trace

@@ -115,17 +115,20 @@ def _dataset(name, tps, grid, runtime_us, counters, threads) -> Dataset:
                    counter_names=COUNTER_NAMES, counter_matrix=cm)
 
 
-def transpose(size: int = 8192, target: int = 1784) -> Dataset:
-    params = [("TILE", [8, 16, 32, 64]), ("VEC", [1, 2, 4]), ("PAD", [0, 1]),
-              ("BLOCK_Y", [1, 2, 4, 8, 16, 32]), ("USE_SMEM", [0, 1]), ("DIAG", [0, 1]),
-              ("UNROLL", [1, 2, 4, 8]), ("WORK_X", [1, 2])]
+def _transpose_valid(p):
+    tx = p["TILE"] / p["VEC"]
+    threads = tx * p["BLOCK_Y"]
+    return ((p["BLOCK_Y"] <= p["TILE"]) & (threads >= 32) & (threads <= 1024)
+            & (tx >= 2) & ((p["USE_SMEM"] == 1) | (p["PAD"] == 0)))
 
-    def valid(p):
-        tx = p["TILE"] / p["VEC"]
-        threads = tx * p["BLOCK_Y"]
-        return ((p["BLOCK_Y"] <= p["TILE"]) & (threads >= 32) & (threads <= 1024)
-                & (tx >= 2) & ((p["USE_SMEM"] == 1) | (p["PAD"] == 0)))
-    tps, g = _enumerate(params, valid, target, seed=1784)
+
+TRANSPOSE_PARAMS = [("TILE", [8, 16, 32, 64]), ("VEC", [1, 2, 4]), ("PAD", [0, 1]),
+                    ("BLOCK_Y", [1, 2, 4, 8, 16, 32]), ("USE_SMEM", [0, 1]), ("DIAG", [0, 1]),
+                    ("UNROLL", [1, 2, 4, 8]), ("WORK_X", [1, 2])]
+
+
+def transpose(size: int = 8192, target: int = 1784) -> Dataset:
+    tps, g = _enumerate(TRANSPOSE_PARAMS, _transpose_valid, target, seed=1784)
     T, V, PAD, BY, SM, DG, UN, WX = (g[:, j] for j in range(8))
     n = g.shape[0]
     elems = float(size) * size
@@ -167,30 +170,35 @@ def transpose(size: int = 8192, target: int = 1784) -> Dataset:
     return _dataset("transpose-8192", tps, g, runtime, c, threads)
 
 
-def gemm(m: int = 2048, target: int = 5788, full: bool = False) -> Dataset:
-    params = [("MWG", [16, 32, 64, 128]), ("NWG", [16, 32, 64, 128]), ("KWG", [16, 32]),
-              ("MDIMC", [8, 16, 32]), ("NDIMC", [8, 16, 32]), ("VWM", [1, 2, 4, 8]),
-              ("VWN", [1, 2, 4, 8]), ("SA", [0, 1]), ("SB", [0, 1]), ("TC", [0, 1])]
-    if full:
-        params = [("MWG", [16, 32, 64, 128]), ("NWG", [16, 32, 64, 128]), ("KWG", [16, 32]),
-                  ("MDIMC", [8, 16, 32]), ("NDIMC", [8, 16, 32]), ("MDIMA", [8, 16, 32]),
-                  ("NDIMB", [8, 16, 32]), ("KWI", [2, 8]), ("VWM", [1, 2, 4, 8]),
-                  ("VWN", [1, 2, 4, 8]), ("STRM", [0, 1]), ("STRN", [0, 1]), ("SA", [0, 1]),
-                  ("SB", [0, 1])]
-        target = 205216
+GEMM_PARAMS = [("MWG", [16, 32, 64, 128]), ("NWG", [16, 32, 64, 128]), ("KWG", [16, 32]),
+               ("MDIMC", [8, 16, 32]), ("NDIMC", [8, 16, 32]), ("VWM", [1, 2, 4, 8]),
+               ("VWN", [1, 2, 4, 8]), ("SA", [0, 1]), ("SB", [0, 1]), ("TC", [0, 1])]
+GEMM_FULL_PARAMS = [("MWG", [16, 32, 64, 128]), ("NWG", [16, 32, 64, 128]), ("KWG", [16, 32]),
+                    ("MDIMC", [8, 16, 32]), ("NDIMC", [8, 16, 32]), ("MDIMA", [8, 16, 32]),
+                    ("NDIMB", [8, 16, 32]), ("KWI", [2, 8]), ("VWM", [1, 2, 4, 8]),
+                    ("VWN", [1, 2, 4, 8]), ("STRM", [0, 1]), ("STRN", [0, 1]), ("SA", [0, 1]),
+                    ("SB", [0, 1])]
 
-    def valid(p):
-        ok = ((p["MWG"] % (p["MDIMC"] * p["VWM"]) == 0) & (p["NWG"] % (p["NDIMC"] * p["VWN"]) == 0)
-              & (p["MDIMC"] * p["NDIMC"] >= 64) & (p["MDIMC"] * p["NDIMC"] <= 1024))
-        if full:
-            ok &= ((p["MWG"] % (p["MDIMA"] * p["VWM"]) == 0)
-                   & (p["NWG"] % (p["NDIMB"] * p["VWN"]) == 0)
-                   & ((p["MDIMC"] * p["NDIMC"]) % p["MDIMA"] == 0)
-                   & ((p["MDIMC"] * p["NDIMC"]) % p["NDIMB"] == 0))
-        else:
-            ok &= (p["TC"] == 0) | ((p["SA"] == 1) & (p["SB"] == 1))
-        return ok
-    tps, g = _enumerate(params, valid, target, seed=5788 if not full else 205216)
+
+def _gemm_valid(p, full=False):
+    ok = ((p["MWG"] % (p["MDIMC"] * p["VWM"]) == 0) & (p["NWG"] % (p["NDIMC"] * p["VWN"]) == 0)
+          & (p["MDIMC"] * p["NDIMC"] >= 64) & (p["MDIMC"] * p["NDIMC"] <= 1024))
+    if full:
+        ok &= ((p["MWG"] % (p["MDIMA"] * p["VWM"]) == 0)
+               & (p["NWG"] % (p["NDIMB"] * p["VWN"]) == 0)
+               & ((p["MDIMC"] * p["NDIMC"]) % p["MDIMA"] == 0)
+               & ((p["MDIMC"] * p["NDIMC"]) % p["NDIMB"] == 0))
+    else:
+        ok &= (p["TC"] == 0) | ((p["SA"] == 1) & (p["SB"] == 1))
+    return ok
+
+
+def gemm(m: int = 2048, target: int = 5788, full: bool = False) -> Dataset:
+    if full:
+        target = 205216
+    tps, g = _enumerate(GEMM_FULL_PARAMS if full else GEMM_PARAMS,
+                        lambda p: _gemm_valid(p, full), target,
+                        seed=5788 if not full else 205216)
     col = {p.name: g[:, j] for j, p in enumerate(tps)}
     n = g.shape[0]
     MWG, NWG, KWG = col["MWG"], col["NWG"], col["KWG"]
@@ -277,25 +285,33 @@ def _pairwise(name, label, target, seed, n_bodies, params, valid, per_pair_flops
     return _dataset(label, tps, g, runtime, c, threads)
 
 
+NBODY_PARAMS = [("BLOCK", [32, 64, 128, 256, 512, 1024]), ("OUTER", [1, 2, 4, 8, 16]),
+                ("UNROLL", [1, 2, 4, 8, 16, 32]), ("USE_SMEM", [0, 1]), ("VEC", [1, 2, 4]),
+                ("FAST_RSQRT", [0, 1]), ("SOA", [0, 1])]
+
+
+def _nbody_valid(p):
+    return (p["UNROLL"] <= p["BLOCK"]) & ((p["USE_SMEM"] == 1) | (p["VEC"] <= 2))
+
+
 def nbody(bodies: int = 16384, target: int = 3134) -> Dataset:
-    params = [("BLOCK", [32, 64, 128, 256, 512, 1024]), ("OUTER", [1, 2, 4, 8, 16]),
-              ("UNROLL", [1, 2, 4, 8, 16, 32]), ("USE_SMEM", [0, 1]), ("VEC", [1, 2, 4]),
-              ("FAST_RSQRT", [0, 1]), ("SOA", [0, 1])]
-    return _pairwise("nbody", f"nbody-{bodies}", target, 3134, bodies, params,
-                     lambda p: (p["UNROLL"] <= p["BLOCK"]) & ((p["USE_SMEM"] == 1) | (p["VEC"] <= 2)),
-                     20.0, 1.0)
+    return _pairwise("nbody", f"nbody-{bodies}", target, 3134, bodies, NBODY_PARAMS,
+                     _nbody_valid, 20.0, 1.0)
+
+
+COULOMB_PARAMS = [("BLOCK", [32, 64, 128, 256]), ("Z_ITERATIONS", [1, 2, 4, 8, 16, 32]),
+                  ("INNER_UNROLL", [0, 1, 2, 4, 8]), ("USE_SMEM", [0, 1]), ("USE_SOA", [0, 1]),
+                  ("VECTOR_TYPE", [1, 2, 4]), ("USE_CONST", [0])]
+
+
+def _coulomb_valid(p):
+    return (((p["USE_SMEM"] == 0) | (p["USE_CONST"] == 0))
+            & ((p["VECTOR_TYPE"] == 1) | (p["USE_SOA"] == 1))
+            & (p["INNER_UNROLL"] <= p["Z_ITERATIONS"] * 2))
 
 
 def coulomb(grid: int = 256, atoms: int = 256, target: int = 210) -> Dataset:
-    params = [("BLOCK", [32, 64, 128, 256]), ("Z_ITERATIONS", [1, 2, 4, 8, 16, 32]),
-              ("INNER_UNROLL", [0, 1, 2, 4, 8]), ("USE_SMEM", [0, 1]), ("USE_SOA", [0, 1]),
-              ("VECTOR_TYPE", [1, 2, 4]), ("USE_CONST", [0])]
-
-    def valid(p):
-        return (((p["USE_SMEM"] == 0) | (p["USE_CONST"] == 0))
-                & ((p["VECTOR_TYPE"] == 1) | (p["USE_SOA"] == 1))
-                & (p["INNER_UNROLL"] <= p["Z_ITERATIONS"] * 2))
-    tps, g = _enumerate(params, valid, target, seed=210)
+    tps, g = _enumerate(COULOMB_PARAMS, _coulomb_valid, target, seed=210)
     col = {p.name: g[:, j] for j, p in enumerate(tps)}
     n = g.shape[0]
     BS, Z = col["BLOCK"], col["Z_ITERATIONS"]
@@ -328,16 +344,19 @@ def coulomb(grid: int = 256, atoms: int = 256, target: int = 210) -> Dataset:
     return _dataset(f"coulomb-{grid}^3x{atoms}", tps, g, runtime, c, threads)
 
 
-def conv(size: int = 4096, filt: int = 7, target: int = 3928) -> Dataset:
-    params = [("TBX", [8, 16, 32, 64]), ("TBY", [1, 2, 4, 8, 16]), ("WPTX", [1, 2, 4, 8]),
-              ("WPTY", [1, 2, 4, 8]), ("VW", [1, 2, 4]), ("LOCAL", [0, 1, 2]),
-              ("PAD", [0, 1]), ("UNROLL_F", [0, 1]), ("CACHE_F", [0, 1]), ("REVERSE", [0, 1])]
+CONV_PARAMS = [("TBX", [8, 16, 32, 64]), ("TBY", [1, 2, 4, 8, 16]), ("WPTX", [1, 2, 4, 8]),
+               ("WPTY", [1, 2, 4, 8]), ("VW", [1, 2, 4]), ("LOCAL", [0, 1, 2]),
+               ("PAD", [0, 1]), ("UNROLL_F", [0, 1]), ("CACHE_F", [0, 1]), ("REVERSE", [0, 1])]
 
-    def valid(p):
-        t = p["TBX"] * p["TBY"]
-        return ((t >= 32) & (t <= 1024) & (p["WPTX"] % p["VW"] == 0)
-                & ((p["LOCAL"] > 0) | (p["PAD"] == 0)) & (p["WPTX"] * p["WPTY"] <= 32))
-    tps, g = _enumerate(params, valid, target, seed=3928)
+
+def _conv_valid(p):
+    t = p["TBX"] * p["TBY"]
+    return ((t >= 32) & (t <= 1024) & (p["WPTX"] % p["VW"] == 0)
+            & ((p["LOCAL"] > 0) | (p["PAD"] == 0)) & (p["WPTX"] * p["WPTY"] <= 32))
+
+
+def conv(size: int = 4096, filt: int = 7, target: int = 3928) -> Dataset:
+    tps, g = _enumerate(CONV_PARAMS, _conv_valid, target, seed=3928)
     col = {p.name: g[:, j] for j, p in enumerate(tps)}
     n = g.shape[0]
     TBX, TBY, WX, WY, VW = col["TBX"], col["TBY"], col["WPTX"], col["WPTY"], col["VW"]
@@ -374,6 +393,26 @@ def conv(size: int = 4096, filt: int = 7, target: int = 3928) -> Dataset:
                         pipe_eff=np.clip(0.3 + 0.08 * np.log2(WX * WY) + 0.1 * UF + 0.05 * CF
                                          + 0.03 * np.log2(VW), 0.2, 1.0))
     return _dataset(f"conv-{size}-{filt}x{filt}", tps, g, runtime, c, threads)
+
+
+# (parameters, constraint, Table-2 size, subsample seed) of every space: the
+# live benchmarks (live.py) enumerate exactly the same configurations
+SPACE_SPECS = {
+    "coulomb": (COULOMB_PARAMS, _coulomb_valid, 210, 210),
+    "transpose": (TRANSPOSE_PARAMS, _transpose_valid, 1784, 1784),
+    "nbody": (NBODY_PARAMS, _nbody_valid, 3134, 3134),
+    "conv": (CONV_PARAMS, _conv_valid, 3928, 3928),
+    "gemm": (GEMM_PARAMS, _gemm_valid, 5788, 5788),
+    "gemm_full": (GEMM_FULL_PARAMS, lambda p: _gemm_valid(p, True), 205216, 205216),
+}
+
+
+def space_of(name: str) -> TuningSpace:
+    """The tuning space of a benchmark (same configurations, same order as
+    the synthetic dataset of that name)."""
+    params, valid, target, seed = SPACE_SPECS[name]
+    tps, g = _enumerate(params, valid, target, seed)
+    return TuningSpace.from_assignments(tps, g)
 
 
 SPACES = {

@@ -1,0 +1,145 @@
+"""Live measurement path on the GPU: every benchmark kernel against its numpy
+oracle (oracle/benchmarks_oracle.py) on a seeded sample of its tuning space,
+the CUPTI collector's counter set, and the ask/tell searcher against the
+batched device search.
+
+Tolerances (stated FP32 bounds, relative to the magnitude sum of the terms,
+see benchmarks_oracle.within): transpose bit-exact; coulomb / nbody 2e-6
+(rsqrtf is within 2^-22.9 relative, per-term); conv 1e-6; gemm 1e-6 (FFMA
+path and the 3xTF32 tensor-core path).
+"""
+
+import numpy as np
+import pytest
+
+import benchmarks_oracle as bo
+
+pytestmark = pytest.mark.gpu
+
+SAMPLE = 14
+
+
+def _sample(n, seed):
+    rng = np.random.default_rng(seed)
+    return sorted({0, n - 1, *rng.choice(n, size=min(n, SAMPLE), replace=False).tolist()})
+
+
+@pytest.fixture(scope="module")
+def tuner():
+    from paper_2102_05297_b200.tuner import Tuner
+    t = Tuner(0)
+    yield t
+    t.close()
+
+
+def _check(src, idxs, got_want):
+    bad = src.compile_all(idxs)
+    assert bad == 0, src.compile_failures
+    worst = 0.0
+    for i in idxs:
+        worst = max(worst, got_want(i))
+    return worst
+
+
+def test_device_info(tuner):
+    assert tuner.arch.startswith("sm_10")
+    assert tuner.sm_count >= 100
+
+
+def test_transpose_matches_oracle(tuner):
+    from paper_2102_05297_b200.live import CudaMeasurementSource, benchmark
+    b = benchmark("transpose", width=1024, height=512)
+    src = CudaMeasurementSource(b, tuner=tuner)
+    want = bo.transpose(b.host_inputs()["in"])
+    for i in _sample(len(b.space), 1):
+        src.compile_all([i])
+        got = src.output(i)
+        assert np.array_equal(got, want), (i, b.values(i))
+
+
+@pytest.mark.parametrize("name,sizes,rtol", [
+    ("coulomb", dict(grid=64, atoms=256), 2e-6),
+    ("nbody", dict(bodies=2048), 2e-6),
+    ("conv", dict(width=1024, height=256), 1e-6),
+    ("gemm", dict(m=256, n=256, k=128), 1e-6),
+])
+def test_benchmark_matches_oracle(tuner, name, sizes, rtol):
+    from paper_2102_05297_b200.live import CudaMeasurementSource, benchmark
+    b = benchmark(name, **sizes)
+    src = CudaMeasurementSource(b, tuner=tuner)
+    h = b.host_inputs()
+    if name == "coulomb":
+        want, mag = bo.coulomb(h["atoms"], b.spacing, b.grid)
+    elif name == "nbody":
+        want, mag = bo.nbody(h["pm"], b.eps2)
+    elif name == "conv":
+        want, mag = bo.conv(h["in"], h["filt"])
+    else:
+        want, mag = bo.gemm(h["at"], h["b"])
+    idxs = _sample(len(b.space), 2)
+    if name == "gemm":   # make sure the tensor-core path is in the sample
+        tc = [i for i in range(len(b.space)) if b.values(i)["TC"] == 1]
+        idxs = sorted(set(idxs) | set(tc[:: max(1, len(tc) // 4)][:4]))
+    worst = _check(src, idxs, lambda i: bo.within(src.output(i), want, mag, 1.0))
+    assert worst <= rtol, f"{name}: worst relative error {worst:.3g} > {rtol}"
+
+
+def test_profiled_measurement_has_table1_counters(tuner):
+    from paper_2102_05297_b200 import counters as cc
+    from paper_2102_05297_b200.live import CudaMeasurementSource, TABLE1_METRICS, benchmark
+    b = benchmark("transpose", width=2048, height=2048)
+    src = CudaMeasurementSource(b, tuner=tuner)
+    i = 0
+    m = src.measure(i, profiled=True)
+    assert m.runtime_us > 0
+    assert m.global_threads == src.launch_of(i).threads
+    assert set(m.counters) >= set(cc.REQUIRED_COUNTERS)
+    assert src.profile_passes >= 1
+    assert tuner.profile_passes(TABLE1_METRICS) == src.profile_passes
+    # transpose reads and writes every element once: DRAM/L2 sectors are at
+    # least the algorithmic 2 x 4 B x n / 32 B
+    sectors = 2 * 4 * 2048 * 2048 / 32
+    assert m.counters["L2_RT"] + m.counters["L2_WT"] >= 0.9 * sectors
+    for k, v in m.counters.items():
+        assert np.isfinite(v) and v >= 0, (k, v)
+
+
+def test_ask_tell_matches_batched_device_search():
+    """ProfileSearcher driven by a replay source == the batched device search."""
+    from paper_2102_05297_b200 import (DatasetReplaySource, ExactModelSet, ProfileSearcher,
+                                       run_profile_search, spaces)
+    from paper_2102_05297_b200.space import well_performing_set
+    ds = spaces.coulomb()
+    src = DatasetReplaySource(ds)
+    model = ExactModelSet(ds)
+    stop = set(well_performing_set(ds, 1.1))
+    for seed in range(4):
+        want = run_profile_search(src, model, i=8, seed=seed, stop_indices=stop)
+        s = ProfileSearcher(model, ds.space, ds.arch, i=8, seed=seed, stop_indices=stop)
+        while (req := s.next_config()) is not None:
+            s.add_result(src.measure(*req))
+        got = s.trace
+        assert [x.config_index for x in got.steps] == [x.config_index for x in want.steps]
+        assert [x.profiled for x in got.steps] == [x.profiled for x in want.steps]
+        assert got.status == want.status
+
+
+def test_live_profile_search_runs(tuner):
+    """Alg. 1 against real kernels: a live search on the coulomb space with a
+    model from a live sweep of the same space (small grid)."""
+    from paper_2102_05297_b200 import ExactModelSet, run_profile_search
+    from paper_2102_05297_b200.live import CudaMeasurementSource, benchmark, sweep
+    b = benchmark("coulomb", grid=64, atoms=256)
+    src = CudaMeasurementSource(b, tuner=tuner, reps=2)
+    res = sweep(src)
+    ds = res.dataset
+    assert not res.failures, res.failures
+    assert ds.has_record.all()
+    model = ExactModelSet(ds)
+    trace = run_profile_search(src, model, i=4, seed=1)
+    assert len(trace.steps) == 4 * 6
+    assert [s.profiled for s in trace.steps[::6]] == [True] * 4
+    # no configuration drawn twice within an outer iteration
+    for k in range(4):
+        inner = [s.config_index for s in trace.steps[6 * k + 1:6 * k + 6]]
+        assert len(set(inner)) == 5
