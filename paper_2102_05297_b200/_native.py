@@ -16,7 +16,7 @@ from .errors import (CounterTuneError, SpaceExhaustedError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libct_b200.so"
-LIB_PATH = os.path.join(_HERE, LIB_NAME)
+LIB_PATH = os.environ.get("CT_LIB_PATH") or os.path.join(_HERE, LIB_NAME)
 
 CT_OK = 0
 CT_ERR_CUDA = -1

@@ -219,6 +219,12 @@ k_profile_search(const SearchArgs a) {
         w = a.scratch_w + (size_t)blockIdx.x * 32 * (size_t)a.nrows;
     }
 
+#ifdef CT_PHASE_CLOCKS
+    long long clk_p1 = 0, clk_score = 0, clk_weight = 0, clk_p4 = 0, clk_t = 0;
+#define CT_CLK(acc) do { if (tid == 0) { long long n_ = clock64(); acc += n_ - clk_t; clk_t = n_; } } while (0)
+#else
+#define CT_CLK(acc) do { } while (0)
+#endif
     for (int rep = blockIdx.x; rep < a.n_reps; rep += gridDim.x) {
         for (int64_t i = tid; i < a.nwords; i += NT) expl[i] = 0u;
 
@@ -236,6 +242,9 @@ k_profile_search(const SearchArgs a) {
         __syncthreads();
 
         for (int it = 0; it < a.outer; ++it) {
+#ifdef CT_PHASE_CLOCKS
+            if (tid == 0) clk_t = clock64();
+#endif
             // ---------------- profile step, expert system (warp 0) ------------
             // One lane per counter fetches the profile's replayed counters and
             // one lane per delta key its predicted value p; the 18 bottleneck
@@ -293,6 +302,7 @@ k_profile_search(const SearchArgs a) {
                 }
             }
             __syncthreads();
+            CT_CLK(clk_p1);
             if (ctl.done) break;
 
             // ---------------- Eq. 16 raw scores (all threads) ------------------
@@ -305,6 +315,7 @@ k_profile_search(const SearchArgs a) {
             for (int m = 16; m > 0; m >>= 1) lamin = fmin(lamin, __shfl_xor_sync(FULL, lamin, m));
             if (lane == 0) { ctl.red_max[warp] = lmax; ctl.red_min[warp] = lmin; ctl.red_amin[warp] = lamin; }
             __syncthreads();
+            CT_CLK(clk_score);
 
             // ---------------- Eq. 17 weights + exact row totals ----------------
             {
@@ -327,6 +338,7 @@ k_profile_search(const SearchArgs a) {
                 if (lane == 0) { ctl.red_tot[warp] = wtot; ctl.red_pos[warp] = pos; ctl.red_bad[warp] = bad; }
             }
             __syncthreads();
+            CT_CLK(clk_weight);
 
             // ---------------- n certified draws (warp 0) ----------------------
             if (warp == 0) {
@@ -470,6 +482,7 @@ k_profile_search(const SearchArgs a) {
                 if (lane == 0) ctl.done = done;
             }
             __syncthreads();
+            CT_CLK(clk_p4);
             if (ctl.done) break;
         }
 
@@ -485,6 +498,11 @@ k_profile_search(const SearchArgs a) {
         }
         __syncthreads();
     }
+#ifdef CT_PHASE_CLOCKS
+    if (tid == 0 && (blockIdx.x % 37) == 0)
+        printf("[clk] cta %d: profile+expert %lld score %lld weights %lld draws %lld cycles\n",
+               blockIdx.x, clk_p1, clk_score, clk_weight, clk_p4);
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -438,7 +438,7 @@ def sweep(source: CudaMeasurementSource, profiled: bool = True, checkpoint: Opti
             threads[i] = m.global_threads
             cm[i] = [m.counters[a] for a in names]
         done[i] = True
-        if checkpoint:
+        if checkpoint and (i % 64 == 63 or i == n - 1):
             np.savez(checkpoint, runtime=runtime, threads=threads, counters=cm, done=done)
         if progress:
             progress(i, n)

@@ -490,13 +490,22 @@ def _profile_search_host_driven(source, table, total, *, i, n, seed, inst_reacti
         return done.value
 
 
-def _profile_search_steps(space, arch, table, total, *, i, n, seed, inst_reaction,
-                          literal_sign, stop_indices, score_top_k):
-    """run_profile_search (search.py:338-399) as a generator: it yields each
-    empirical test as (config_index, profiled), is sent the Measurement, and
-    returns the SearchTrace.  The RNG is consumed exactly as the reference's
-    loop consumes it, so driving it with source.measure IS the reference's
-    control flow."""
+def _profile_search_batches(space, arch, table, total, *, i, n, seed, inst_reaction,
+                            literal_sign, stop_indices, score_top_k):
+    """run_profile_search (search.py:338-399) as a generator of measurement
+    batches: it yields ``(indices, profiled)`` -- the profiled configuration
+    alone, then the n draws of the outer iteration together -- and is sent the
+    Measurements of a prefix of the batch (all of it, or up to and including
+    a configuration of the stop set); it returns the SearchTrace.
+
+    The n draws of an iteration depend only on that iteration's weights and
+    the Generator, not on the runtimes measured in between (search.py:388-398),
+    so they can be made before any of them is measured: the RNG is consumed
+    exactly as the reference's loop consumes it up to the end of the search
+    (a stop ends the search before the extra draws could matter), and the
+    recorded steps, the stop test and the later-ties-win argmin follow the
+    reference's order.  That is what lets several GPUs time one iteration's
+    candidates concurrently (dist_live.py)."""
     rng = np.random.default_rng(seed)
     explored = np.zeros(total, dtype=bool)
     steps: List[TraceStep] = []
@@ -511,7 +520,7 @@ def _profile_search_steps(space, arch, table, total, *, i, n, seed, inst_reactio
         return stop_indices is not None and idx in stop_indices
 
     for _ in range(i):
-        m = yield (c_profile.index, True)
+        m = (yield ([c_profile.index], True))[0]
         if record(c_profile.index, m.runtime_us, True):
             return SearchTrace(steps=steps, seed=seed, status=STATUS_STOPPED)
         _check_inst_reaction(inst_reaction)
@@ -523,22 +532,52 @@ def _profile_search_steps(space, arch, table, total, *, i, n, seed, inst_reactio
         scores = score_configurations(table, c_profile, delta, space, explored,
                                       literal_sign=literal_sign, score_top_k=score_top_k)
         scores = normalize_scores(scores)
-        t_best = np.inf
+        chosen: List[int] = []
+        exhausted = False
         for _ in range(n):
             try:
                 # zero total mass == norm.max() <= 0 (weights are 0 or >= 1e-4);
                 # the draw is not consumed in that case
-                chosen = weighted_select(scores, rng)
+                c = weighted_select(scores, rng)
             except SpaceExhaustedError:
-                return SearchTrace(steps=steps, seed=seed, status=STATUS_EXHAUSTED)
-            runtime = (yield (chosen, False)).runtime_us
-            scores.norm[chosen] = 0.0
-            if record(chosen, runtime, False):
+                exhausted = True
+                break
+            scores.norm[c] = 0.0
+            chosen.append(c)
+        got = (yield (chosen, False)) if chosen else []
+        t_best = np.inf
+        for c, meas in zip(chosen, got):
+            if record(c, meas.runtime_us, False):
                 return SearchTrace(steps=steps, seed=seed, status=STATUS_STOPPED)
-            if runtime <= t_best:
-                t_best = runtime
-                c_profile = space.configurations[chosen]
+            if meas.runtime_us <= t_best:
+                t_best = meas.runtime_us
+                c_profile = space.configurations[c]
+        if len(got) < len(chosen):
+            raise CounterTuneError("a measurement batch was cut short before a stop configuration")
+        if exhausted:
+            return SearchTrace(steps=steps, seed=seed, status=STATUS_EXHAUSTED)
     return SearchTrace(steps=steps, seed=seed, status=STATUS_BUDGET)
+
+
+def _profile_search_steps(space, arch, table, total, *, i, n, seed, inst_reaction,
+                          literal_sign, stop_indices, score_top_k):
+    """The batch generator one empirical test at a time: yields
+    (config_index, profiled), is sent each Measurement, returns the trace.
+    Draws after a stop configuration are never measured."""
+    core = _profile_search_batches(space, arch, table, total, i=i, n=n, seed=seed,
+                                   inst_reaction=inst_reaction, literal_sign=literal_sign,
+                                   stop_indices=stop_indices, score_top_k=score_top_k)
+    try:
+        batch, profiled = next(core)
+        while True:
+            got = []
+            for idx in batch:
+                got.append((yield (idx, profiled)))
+                if stop_indices is not None and idx in stop_indices:
+                    break
+            batch, profiled = core.send(got)
+    except StopIteration as done:
+        return done.value
 
 
 class ProfileSearcher:

@@ -143,3 +143,30 @@ def test_live_profile_search_runs(tuner):
     for k in range(4):
         inner = [s.config_index for s in trace.steps[6 * k + 1:6 * k + 6]]
         assert len(set(inner)) == 5
+
+
+def test_distributed_live_search_world1_matches_device_search():
+    """dist_live with the device searcher core (world size 1, gloo) gives the
+    batched device search's trajectory on a replayed dataset."""
+    import socket
+    import torch.distributed as dist
+    from paper_2102_05297_b200 import (DatasetReplaySource, ExactModelSet, run_profile_search,
+                                       spaces)
+    from paper_2102_05297_b200.dist_live import run_profile_search_distributed
+    from paper_2102_05297_b200.space import well_performing_set
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        ds = spaces.transpose()
+        src = DatasetReplaySource(ds)
+        model = ExactModelSet(ds)
+        stop = set(well_performing_set(ds, 1.1))
+        for seed in range(3):
+            want = run_profile_search(src, model, i=10, seed=seed, stop_indices=stop)
+            got = run_profile_search_distributed(src, model, i=10, seed=seed, stop_indices=stop)
+            assert [s.config_index for s in got.steps] == [s.config_index for s in want.steps]
+            assert got.status == want.status
+    finally:
+        dist.destroy_process_group()
