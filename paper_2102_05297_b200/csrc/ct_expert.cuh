@@ -80,6 +80,47 @@ CT_HD double analyze_component(const double* c, int k, int generation, int64_t c
     return clamp01(v);
 }
 
+#if defined(__CUDACC__)
+// Warp form (lane k evaluates component k, all 32 lanes call it converged):
+// the same operations as analyze_component, but the b_issue lane takes the
+// seven per-class ratios dvd(c[INST_F32 + j], fitted) from lanes 8..14,
+// which compute exactly those values for their own components, instead of
+// redoing seven dependent divisions.  Bit-identical to analyze_component.
+__device__ __forceinline__ double analyze_component_warp(const double* c, int k, int generation,
+                                                         int64_t cores, int64_t global_threads,
+                                                         bool degenerate) {
+    const bool inst = (k >= B_FP32) && (k <= B_ISSUE) && !degenerate;
+    double ratio = 0.0;
+    if (inst) {
+        const double fitted = mul(mul(mul(32.0, c[INST_EXE]), dvd(100.0, c[WARP_E])),
+                                  dvd(100.0, c[WARP_NP_E]));
+        ratio = dvd(c[INST_F32 + ((k < B_ISSUE) ? (k - B_FP32) : 0)], fitted);
+    }
+    double r[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) r[j] = __shfl_sync(0xffffffffu, ratio, B_FP32 + j);
+    if (k == B_ISSUE) {
+        if (degenerate) return 0.0;
+        double util_max = r[0];
+#pragma unroll
+        for (int j = 1; j < 7; ++j) util_max = pymax(util_max, r[j]);
+        return clamp01(dvd(mul(util_max, sub(100.0, c[INST_ISSUE_U])), 100.0));
+    }
+    if (k >= B_FP32 && k < B_ISSUE) {
+        if (degenerate) return 0.0;
+        double util;
+        if (generation == 0) {
+            util = dvd(c[INST_ISSUE_U], 100.0);
+        } else {
+            const double u = dvd(c[INST_ISSUE_U], 50.0);
+            util = (u < 1.0) ? u : 1.0;
+        }
+        return clamp01(mul(ratio, util));
+    }
+    return analyze_component(c, k, generation, cores, global_threads, degenerate);
+}
+#endif
+
 // analyze(): c = 23 counters, generation 0 = pre_volta, 1 = volta_plus.
 // Returns the degenerate_instructions flag.
 CT_HD bool analyze(const double* c, int generation, int64_t cores, int64_t global_threads,

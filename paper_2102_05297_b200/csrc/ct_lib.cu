@@ -67,6 +67,7 @@ struct ct_ctx {
     int64_t ld = 0;          // padded column stride
     int32_t n_counters = 0;
     uint64_t col_cert = 0;   // columns inside raw_term_cert's domain
+    uint64_t col_nz = 0;     // columns without an exact zero
     // space assignments (row-major n x P)
     DevBuf<double> assign;
     int32_t n_params = 0;
@@ -134,7 +135,7 @@ __global__ void k_score_single(const ScoreSingleArgs a) {
             if (a.vals[k] == 0.0 || a.cols[k] < 0) continue;
             double pv = a.table[(size_t)a.cols[k] * a.ld + a.profile];
             if (pv == 0.0) continue;
-            act[na].col = a.cols[k]; act[na].d = a.vals[k]; act[na].p = pv; ++na;
+            act[na].col = a.cols[k]; act[na].nz = 0; act[na].d = a.vals[k]; act[na].p = pv; ++na;
         }
         n_act = na;
     }
@@ -277,12 +278,18 @@ __global__ void k_select_single(const double* w, int64_t n, int rows, int ntiles
 
 __global__ void k_analyze_react(const double* c, int gen, int64_t cores, int64_t threads,
                                 double inst_reaction, double issue_sign, double* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double b[N_COMP], d[N_COMP];
-    bool deg = analyze(c, gen, cores, threads, b);
-    react(b, inst_reaction, issue_sign, d);
-    for (int k = 0; k < N_COMP; ++k) { out[k] = b[k]; out[N_COMP + k] = d[k]; }
-    out[2 * N_COMP] = deg ? 1.0 : 0.0;
+    // one warp, lane k = component k: the search kernel's own code path
+    // (analyze_component_warp), so the expert-system parity tests pin it
+    if (blockIdx.x != 0) return;
+    const int lane = threadIdx.x & 31;
+    const bool deg = degenerate_of(c);
+    const double b = analyze_component_warp(c, lane < N_COMP ? lane : N_COMP - 1, gen, cores,
+                                            threads, deg);
+    if (lane < N_COMP) {
+        out[lane] = b;
+        out[N_COMP + lane] = react_component(b, lane, inst_reaction, issue_sign);
+    }
+    if (lane == 0) out[2 * N_COMP] = deg ? 1.0 : 0.0;
 }
 
 // Self-check of dvd_fast against __ddiv_rn on generated operand pairs:
@@ -424,6 +431,17 @@ uint64_t certified_columns(const double* m, int64_t n, int32_t c) {
     return cert;
 }
 
+// bit j set when column j of a row-major n x c table holds no exact zero
+uint64_t nonzero_columns(const double* m, int64_t n, int32_t c) {
+    uint64_t nz = 0;
+    for (int32_t j = 0; j < c && j < 64; ++j) {
+        bool any_zero = false;
+        for (int64_t i = 0; i < n && !any_zero; ++i) any_zero = (m[(size_t)i * c + j] == 0.0);
+        if (!any_zero) nz |= 1ull << j;
+    }
+    return nz;
+}
+
 int rows_for(int64_t n) {
     // ~sqrt(N)/32 rows balances the two scans of a draw; at least 2 rows so
     // that each lane sums two weights per tile before the warp reduction
@@ -490,6 +508,32 @@ int launch_profile_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
     kern<<<grid, NT, smem, ctx->stream>>>(a);
     CT_CUDA(cudaGetLastError());
     return CT_OK;
+}
+
+// warp-specialised kernel: two repetitions per CTA, PW parallel warps
+template <int PW, bool SMEM>
+int launch_profile_ws_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
+    auto kern = k_profile_search_ws<PW, SMEM>;
+    constexpr int NTT = 32 * (PW + 1);
+    if (smem > 48 * 1024)
+        CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTT, smem));
+    if (occ < 1) return fail(CT_ERR_CUDA, "search kernel does not fit on an SM");
+    int grid = std::min((n_reps + 1) / 2, occ * ctx->sm_count);
+    if (!SMEM) {
+        CT_CUDA(ctx->scratch_w.ensure((size_t)2 * grid * 32 * (size_t)a.nrows));
+        a.scratch_w = ctx->scratch_w.p;
+    }
+    kern<<<grid, NTT, smem, ctx->stream>>>(a);
+    CT_CUDA(cudaGetLastError());
+    return CT_OK;
+}
+
+template <int PW>
+int launch_profile_ws(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int n_reps) {
+    return in_smem ? launch_profile_ws_t<PW, true>(ctx, a, smem, n_reps)
+                   : launch_profile_ws_t<PW, false>(ctx, a, smem, n_reps);
 }
 
 template <int NT>
@@ -585,6 +629,7 @@ int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
     ctx->ld = ld;
     ctx->n_counters = c;
     ctx->col_cert = cert;
+    ctx->col_nz = nonzero_columns(matrix, n, c);
     return CT_OK;
 }
 
@@ -650,6 +695,7 @@ int ct_model_predict(ct_ctx* ctx, const ct_model_program* pg, const double* assi
     ctx->ld = ld;
     ctx->n_counters = pg->n_cols;
     ctx->col_cert = certified_columns(dst, n, pg->n_cols);
+    ctx->col_nz = nonzero_columns(dst, n, pg->n_cols);
     return CT_OK;
 }
 
@@ -879,6 +925,7 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     a.literal_sign = prm->literal_sign; a.generation = prm->generation; a.cores = prm->cores;
     for (int k = 0; k < CT_N_DELTA; ++k) a.delta_col[k] = prm->delta_columns[k];
     a.col_cert = ctx->col_cert;
+    a.col_nz = ctx->col_nz;
     a.seed = seed_inline; a.n_reps = n_reps;
     a.nrows = (int32_t)((n + 31) / 32);
     a.nwords = (n + 31) / 32;
@@ -906,6 +953,25 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     bool in_smem = head_b + pref_b <= per_cta_cap;
     if (const char* env = std::getenv("CT_SEARCH_SMEM")) in_smem = std::atoi(env) != 0 && head_b + pref_b <= budget;
     const size_t smem = head_b + (in_smem ? pref_b : 0);
+    // warp-specialised two-repetition kernel (CT_SEARCH_WS = parallel warps)
+    int ws = 0;
+    if (const char* env = std::getenv("CT_SEARCH_WS")) ws = std::atoi(env);
+    if (ws > 0) {
+        // two slots per CTA: weights in shared memory when both fit
+        const int64_t ctas_per_sm = std::max<int64_t>(1, (want_per_sm + 1) / 2);
+        const size_t cap2 = std::min<size_t>(
+            2 * budget, (size_t)(228 * 1024 / ctas_per_sm) - 3 * 1024);
+        bool ws_smem = 2 * (head_b + pref_b) <= cap2;
+        if (const char* env = std::getenv("CT_SEARCH_SMEM")) ws_smem = std::atoi(env) != 0 && 2 * (head_b + pref_b) <= 2 * budget;
+        const size_t smem2 = 2 * (head_b + (ws_smem ? pref_b : 0));
+        switch (ws) {
+        case 2: return launch_profile_ws<2>(ctx, a, ws_smem, smem2, n_reps);
+        case 3: return launch_profile_ws<3>(ctx, a, ws_smem, smem2, n_reps);
+        case 4: return launch_profile_ws<4>(ctx, a, ws_smem, smem2, n_reps);
+        case 6: return launch_profile_ws<6>(ctx, a, ws_smem, smem2, n_reps);
+        default: return launch_profile_ws<8>(ctx, a, ws_smem, smem2, n_reps);
+        }
+    }
     switch (nt) {
     case 32: return launch_profile<32>(ctx, a, in_smem, smem, n_reps);
     case 64: return launch_profile<64>(ctx, a, in_smem, smem, n_reps);

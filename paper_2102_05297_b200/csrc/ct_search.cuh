@@ -75,6 +75,7 @@ struct SearchArgs {
     int64_t cores;
     int32_t delta_col[18];
     uint64_t col_cert;           // bit j: table column j admits raw_term_cert
+    uint64_t col_nz;             // bit j: table column j holds no exact zero
     SeedInline seed;
     int32_t n_reps;
     // rows of 32 configurations
@@ -118,59 +119,82 @@ struct __align__(16) Ctl {
     int n_act;
     int done;
     int cert_terms;
+    int cmd;          // k_profile_search_ws: what the parallel warps do next
 };
 
 // Eq. 16 over the whole space for one repetition's active terms: raw score of
 // configuration e into w[e], pool max / min / smallest nonzero magnitude
-// returned per thread.  Columns are padded to a multiple of 4*NT, so the four
-// loads of an iteration use one base pointer and immediate offsets.
-template <int NT, bool CERT, int NW>
+// returned per thread (max / min ignore NaN here; `nan` records one, and the
+// caller turns the extrema into NaN as numpy's max()/min() would).  PT
+// threads share the space (ptid = 0..PT-1).  Full groups of 4 configurations
+// per thread run unguarded (columns are padded to a multiple of 2048, so the
+// four loads use one base pointer and immediate offsets); the last partial
+// group goes one configuration at a time, so no work is spent on the padding.
+__device__ __forceinline__ void score_epilogue(double acc, int64_t e, const uint32_t* expl,
+                                               double* w, double& lmax, double& lmin,
+                                               double& lamin, bool& nan) {
+    // branch-free: an explored configuration contributes the neutral element
+    const bool in = !bit_get(expl, e);
+    w[e] = in ? acc : 0.0;
+    const double vmax = in ? acc : -INFINITY, vmin = in ? acc : INFINITY;
+    lmax = (vmax > lmax) ? vmax : lmax;
+    lmin = (vmin < lmin) ? vmin : lmin;
+    const double m = fabs(acc);
+    lamin = (in && m != 0.0 && m < lamin) ? m : lamin;
+    nan |= in && (acc != acc);
+}
+
+template <int PT, bool CERT, int NW>
 __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& ctl,
-                                           const uint32_t* expl, double* w, double& lmax,
-                                           double& lmin, double& lamin) {
+                                           const uint32_t* expl, double* w, int ptid, double& lmax,
+                                           double& lmin, double& lamin, bool& nan) {
     const int64_t N = a.n;
     const int n_act = ctl.n_act;
-    for (int64_t base = threadIdx.x; base < N; base += 4LL * NT) {
+    int64_t base = ptid;
+    for (; base + 3LL * PT < N; base += 4LL * PT) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         for (int k = 0; k < n_act; ++k) {
             const double d = ctl.act[k].d, pv = ctl.act[k].p;
             const double* col = a.table + (size_t)ctl.act[k].col * a.ld + base;
             double c[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) c[u] = __ldg(col + u * NT);
+            for (int u = 0; u < 4; ++u) c[u] = __ldg(col + u * PT);
+            if (CERT && ctl.act[k].nz) {      // block-uniform: no zero in the column
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                acc[u] = add(acc[u], CERT ? raw_term_cert(c[u], d, pv) : raw_term_nb(c[u], d, pv));
-        }
+                for (int u = 0; u < 4; ++u) acc[u] = add(acc[u], raw_term_cert_nz(c[u], d, pv));
+            } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int64_t e = base + (int64_t)u * NT;
-            if (e < N) {
-                const bool in = !bit_get(expl, e);
-                w[e] = in ? acc[u] : 0.0;
-                if (in) {
-                    lmax = nmax(lmax, acc[u]);
-                    lmin = nmin(lmin, acc[u]);
-                    const double m = fabs(acc[u]);
-                    lamin = (m != 0.0 && m < lamin) ? m : lamin;
-                }
+                for (int u = 0; u < 4; ++u)
+                    acc[u] = add(acc[u], CERT ? raw_term_cert(c[u], d, pv) : raw_term_nb(c[u], d, pv));
             }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            score_epilogue(acc[u], base + (int64_t)u * PT, expl, w, lmax, lmin, lamin, nan);
+    }
+    for (; base < N; base += PT) {
+        double acc = 0.0;
+        for (int k = 0; k < n_act; ++k) {
+            const double c = __ldg(a.table + (size_t)ctl.act[k].col * a.ld + base);
+            acc = add(acc, CERT ? raw_term_cert(c, ctl.act[k].d, ctl.act[k].p)
+                                : raw_term_nb(c, ctl.act[k].d, ctl.act[k].p));
+        }
+        score_epilogue(acc, base, expl, w, lmax, lmin, lamin, nan);
     }
 }
 
-// Eq. 17 weights over the raw scores and each row's exact total: warp wp
-// takes rows wp, wp+NW, ...; lane l owns configuration 32 t + l (padding
-// lanes write weight 0).
+// Eq. 17 weights over the raw scores and each row's exact total: warp pw of
+// the nw-warp group takes rows pw, pw+nw, ...; lane l owns configuration
+// 32 t + l (padding lanes write weight 0).
 template <bool CERT>
-__device__ __forceinline__ void weight_pass(const SearchArgs& a, int NW, double smax, double smin,
-                                            const uint32_t* expl, double* w, u128* row_tot,
-                                            u128& wtot, int& pos, int& bad) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw, double smax,
+                                            double smin, const uint32_t* expl, double* w,
+                                            u128* row_tot, u128& wtot, int& pos, int& bad) {
+    const int lane = threadIdx.x & 31;
     const int64_t N = a.n;
     const double gamma = a.gamma;
     const double y_max = rcp_nv(smax), y_min = rcp_nv(smin);
-    for (int t = warp; t < a.nrows; t += NW) {
+    for (int t = pw; t < a.nrows; t += nw) {
         const int64_t e = 32LL * t + lane;
         double wt = 0.0;
         if (e < N && !bit_get(expl, e)) wt = weight_rcp<CERT>(w[e], smax, smin, y_max, y_min, gamma);
@@ -192,6 +216,291 @@ __device__ __forceinline__ double fx_total_to_double(u128 v) {
     return __fma_rn(hi, 18446744073709551616.0, lo) * 1.3552527156068805e-20;   // 2^64, 2^-66
 }
 
+// ---------------------------------------------------------------------------
+// The phases of one outer iteration of one repetition.  A repetition's state
+// is (RepState, Ctl, explored bits, weights, row totals); the phases below are
+// shared by both kernels.
+
+// Start a repetition: Generator seeded from the repetition's SeedSequence
+// child, first profile drawn with integers(0, N) (search.py:359-364).  One
+// full warp; the explored bits are cleared cooperatively.
+template <int NW>
+__device__ __forceinline__ void rep_begin(const SearchArgs& a, const uint32_t* seed_sh, int rep,
+                                          RepState& rs, Ctl<NW>& ctl, uint32_t* expl, int lane) {
+    for (int64_t i = lane; i < a.nwords; i += 32) expl[i] = 0u;
+    if (lane == 0) {
+        rs.c_prof = 0; rs.ns = 0; rs.n_expl = 0; rs.st = CT_STATUS_BUDGET; rs.err = 0;
+        rs.scored = 0; rs.draws = 0; rs.uncert = 0; rs.outers = 0; rs.abytes = 0;
+        rs.rng.seed(seed_pool(seed_words_of(a.seed, seed_sh, rep)));
+        rs.c_prof = (int64_t)rs.rng.integers((uint64_t)a.n);
+        ctl.done = 0;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void rep_end(const SearchArgs& a, int rep, const RepState& rs) {
+    a.n_steps[rep] = (int32_t)rs.ns;
+    a.status[rep] = rs.st;
+    a.rep_error[rep] = rs.err;
+    atomicAdd(&a.stats[0], rs.scored);
+    atomicAdd(&a.stats[1], rs.draws);
+    atomicAdd(&a.stats[2], rs.uncert);
+    atomicAdd(&a.stats[3], rs.outers);
+    atomicAdd(&a.stats[4], rs.abytes);
+}
+
+// Profile step + expert system (one full warp).  One lane per counter
+// fetches the profile's replayed counters and one lane per delta key its
+// predicted value p; the 18 bottleneck components and their reactions are
+// evaluated on 18 lanes (analyze_component_warp: the scalar analyze()'s
+// operations) and the active terms compacted in react() order with a ballot.
+template <int NW>
+__device__ __forceinline__ void profile_step(const SearchArgs& a, RepState& rs, Ctl<NW>& ctl,
+                                             uint32_t* expl, int32_t* out_idx, uint8_t* out_prof,
+                                             int lane) {
+    const int64_t N = a.n;
+    const int64_t cp = rs.c_prof;
+    if (lane < N_REQ) ctl.cnt[lane] = a.counters[(size_t)cp * N_REQ + lane];
+    const int col = (lane < N_COMP) ? a.delta_col[lane] : -1;
+    const double pv = (col >= 0) ? a.table[(size_t)col * a.ld + cp] : 0.0;
+    const bool rec_ok = a.has_record[cp] != 0;
+    const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cp);
+    const int64_t thr = a.threads[cp];
+    __syncwarp();
+    double dk = 0.0;
+    const double bk = analyze_component_warp(ctl.cnt, lane < N_COMP ? lane : N_COMP - 1,
+                                             a.generation, a.cores, thr, degenerate_of(ctl.cnt));
+    if (lane < N_COMP) dk = react_component(bk, lane, a.inst_reaction, a.issue_sign);
+    const bool act = (lane < N_COMP) && dk != 0.0 && col >= 0 && pv != 0.0;
+    const unsigned amask = __ballot_sync(FULL, act);
+    if (act) {
+        const int slot = __popc(amask & ((1u << lane) - 1u));
+        ctl.act[slot].col = col;
+        ctl.act[slot].nz = (col < 64 && ((a.col_nz >> col) & 1ull)) ? 1 : 0;
+        ctl.act[slot].p = pv;
+        // literal sign: (-d)(c - p) == d(p - c) exactly
+        ctl.act[slot].d = a.literal_sign ? -dk : dk;
+    }
+    // certified division domain for every active term
+    const double two_m200 = 6.223015277861142e-61;
+    const bool cert_ok = !act || (col < 64 && ((a.col_cert >> col) & 1ull) && fabs(dk) >= two_m200);
+    const bool cert_all = __all_sync(FULL, cert_ok);
+    if (lane == 0) {
+        const int na = __popc(amask);
+        ctl.n_act = na;
+        ctl.cert_terms = cert_all ? 1 : 0;
+        if (!rec_ok) {
+            rs.st = CT_STATUS_ERROR; rs.err = -4; ctl.done = 1;
+            if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)cp;   // failing index
+        } else {
+            out_idx[rs.ns] = (int32_t)cp; out_prof[rs.ns] = 1; ++rs.ns;
+            uint32_t m = 1u << (cp & 31);
+            if (!(expl[cp >> 5] & m)) { expl[cp >> 5] |= m; ++rs.n_expl; }
+            if (is_stop) { rs.st = CT_STATUS_STOPPED; ctl.done = 1; }
+            else if (rs.n_expl >= N) { rs.st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
+            else {
+                unsigned long long pool = (unsigned long long)(N - rs.n_expl);
+                rs.scored += pool; ++rs.outers;
+                rs.abytes += pool * (8ull * (unsigned long long)na + 16ull);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// Eq. 16 for the group's share (PT threads, ptid = 0..PT-1), reduced per warp
+// into ctl.red_*[ptid / 32].
+template <int PT, int NW>
+__device__ __forceinline__ void score_phase(const SearchArgs& a, Ctl<NW>& ctl, const uint32_t* expl,
+                                            double* w, int ptid) {
+    const int lane = ptid & 31, pw = ptid >> 5;
+    double lmax = -INFINITY, lmin = INFINITY, lamin = INFINITY;
+    bool nan = false;
+    if (ctl.cert_terms) score_pass<PT, true>(a, ctl, expl, w, ptid, lmax, lmin, lamin, nan);
+    else score_pass<PT, false>(a, ctl, expl, w, ptid, lmax, lmin, lamin, nan);
+    lmax = warp_max(lmax);
+    lmin = warp_min(lmin);
+    if (__any_sync(FULL, nan)) { lmax = NAN; lmin = NAN; }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) lamin = fmin(lamin, __shfl_xor_sync(FULL, lamin, m));
+    if (lane == 0) { ctl.red_max[pw] = lmax; ctl.red_min[pw] = lmin; ctl.red_amin[pw] = lamin; }
+}
+
+// Eq. 17 weights + exact row totals for warp pw of the NW-warp group (after
+// every warp's score_phase is visible), reduced into ctl.red_tot/pos/bad[pw].
+template <int NW>
+__device__ __forceinline__ void weight_phase(const SearchArgs& a, Ctl<NW>& ctl, const uint32_t* expl,
+                                             double* w, u128* row_tot, int pw) {
+    const int lane = threadIdx.x & 31;
+    double smax = ctl.red_max[0], smin = ctl.red_min[0], amin = ctl.red_amin[0];
+#pragma unroll
+    for (int i = 1; i < NW; ++i) {
+        smax = nmax(smax, ctl.red_max[i]); smin = nmin(smin, ctl.red_min[i]);
+        amin = fmin(amin, ctl.red_amin[i]);
+    }
+    // certified Eq. 17 domain: every nonzero |s| in [2^-400, 2^400]
+    // (NaN extrema fail the comparisons)
+    const double lo = 3.872591914849318e-121, hi = 2.5822498780869086e+120;
+    const bool cert = (amin >= lo || amin == INFINITY) && smax <= hi && smin >= -hi;
+    u128 wtot = 0;
+    int pos = 0, bad = 0;
+    if (cert) weight_pass<true>(a, pw, NW, smax, smin, expl, w, row_tot, wtot, pos, bad);
+    else weight_pass<false>(a, pw, NW, smax, smin, expl, w, row_tot, wtot, pos, bad);
+    pos = warp_sum_i(pos);
+    bad = __any_sync(FULL, bad);
+    if (lane == 0) { ctl.red_tot[pw] = wtot; ctl.red_pos[pw] = pos; ctl.red_bad[pw] = bad; }
+}
+
+// n certified draws, replay lookups, stop test and the later-ties-win argmin
+// (one full warp).  Sets ctl.done when the repetition ends here.
+template <int NW>
+__device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl<NW>& ctl,
+                                          uint32_t* expl, double* w, u128* row_tot,
+                                          const u128* jA, const u128* jC, int32_t* out_idx,
+                                          uint8_t* out_prof, int lane) {
+    const int64_t N = a.n;
+    u128 total = 0;
+    int positive = 0, bad = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        total += ctl.red_tot[i]; positive += ctl.red_pos[i]; bad |= ctl.red_bad[i];
+    }
+    // each lane owns a contiguous chunk of rows; its inclusive prefix is kept
+    // across the draws and patched after a zeroing
+    const int cpl = (a.nrows + 31) >> 5;
+    const int t0 = lane * cpl, t1 = min(t0 + cpl, a.nrows);
+    u128 mine = 0;
+    for (int t = t0; t < t1; ++t) mine += row_tot[t];
+    u128 lane_pref = warp_incl_scan(mine, lane);
+    // certificate half-width (SURVEY hard part 3): sequential float prefix vs
+    // exact prefix, weights within 1 ulp, T within 1 ulp; taken at the
+    // iteration's largest total
+    const double bound = (double)(2 * N + 32) * 1.1102230246251565e-16 * fx_total_to_double(total);
+    const u128 b_fx = floor_fx(bound) + 1;
+    int done = 0;
+    if (bad) { if (lane == 0) { rs.st = CT_STATUS_ERROR; rs.err = -7; } done = 1; }
+    double t_best = INFINITY;
+    // The iteration's uniforms come 32 at a time from the repetition's PCG64
+    // by jump-ahead (lane j: the (j+1)-th next Generator.random()), the draws
+    // of a chunk touch shared memory only, and their replay lookups are issued
+    // together afterwards: one L2 round trip per chunk instead of one per
+    // draw.  Draws past a stop / error are discarded (the repetition ends
+    // there, as the reference's loop does).
+    Pcg64 g;
+    g.state = rs.rng.state;
+    g.inc = rs.rng.inc;
+    int k = 0;
+    bool exhausted = false;
+    while (k < a.inner && !done) {
+        const int k0 = k;
+        const int cnt = min(32, a.inner - k0);
+        const double u_lane = (lane < cnt) ? g.double_after(jA[lane + 1], jC[lane + 1]) : 0.0;
+        int64_t my_choice = -1;
+        for (; k < k0 + cnt; ++k) {
+            if (positive <= 0) { exhausted = true; break; }
+            const double u = __shfl_sync(FULL, u_lane, k - k0);
+            const double r = mul(u, fx_total_to_double(total));
+            const u128 r_fx = floor_fx(r);
+            // the lane whose row chunk holds r, then the row, then the
+            // configuration: one ballot each
+            int64_t chosen = -1;
+            bool ok = false;
+            u128 wfx = 0;
+            int row = -1, l2 = 0;
+            const unsigned bal = __ballot_sync(FULL, lane_pref > r_fx);
+            if (bal) {
+                const int L = __ffs(bal) - 1;
+                u128 carry = lane_pref - mine;
+                if (lane == L) {
+                    for (int t = t0; t < t1; ++t) {
+                        const u128 nxt = carry + row_tot[t];
+                        if (nxt > r_fx) { row = t; break; }
+                        carry = nxt;
+                    }
+                }
+                row = __shfl_sync(FULL, row, L);
+                carry = shfl_u128(carry, L);
+                // exact in-row prefix of the row holding r
+                Limbs f;
+                weight_limbs(w[32LL * row + lane], &f);
+                const u128 incl = warp_incl_scan_limbs(f, lane);
+                l2 = __ffs(__ballot_sync(FULL, carry + incl > r_fx)) - 1;
+                const int src = l2 < 0 ? 0 : l2;
+                wfx = shfl_u128(limbs_value(f.l0, f.l1, f.l2), src);
+                const u128 before = carry + shfl_u128(incl, src) - wfx;
+                chosen = 32LL * row + l2;
+                // r far enough from both boundaries of the chosen
+                // configuration: the reference's sequential cumsum picks it too
+                ok = l2 >= 0 && (r_fx - before > b_fx) && (before + wfx - r_fx - 1 > b_fx);
+                ok = ok && !a.force_sequential;
+            }
+            if (!ok) {
+                if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
+                chosen = __shfl_sync(FULL, (long long)chosen, 0);
+                if (chosen >= 0 && chosen < N) {
+                    row = (int)(chosen >> 5); l2 = (int)(chosen & 31);
+                    to_fx(w[chosen], &wfx);
+                }
+            }
+            if (lane == 0) ++rs.draws;
+            if (lane == k - k0) my_choice = chosen;
+            if (!(chosen >= 0 && chosen < N)) { ++k; break; }   // recorded as an error below
+            // zero the drawn weight: its row total and the lane prefixes drop
+            // by wfx (exact)
+            __syncwarp();
+            if (lane == 0) { w[chosen] = 0.0; row_tot[row] -= wfx; }
+            if (row >= t0 && row < t1) mine -= wfx;
+            if (row < t1) lane_pref -= wfx;
+            total -= wfx;
+            --positive;
+            __syncwarp();
+        }
+        const int made = k - k0;
+        g.advance(jA[made], jC[made]);
+        // replay lookups of the chunk's draws, one per lane
+        const bool mine_in = lane < made && my_choice >= 0 && my_choice < N;
+        const int64_t cs = mine_in ? my_choice : 0;
+        const bool rec_ok = mine_in && a.has_record[cs];
+        const double rt = a.runtime[cs];
+        const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cs);
+        // the reference's bookkeeping, draw by draw
+        for (int j = 0; j < made; ++j) {
+            const int64_t cj = __shfl_sync(FULL, (long long)my_choice, j);
+            const bool okj = __shfl_sync(FULL, rec_ok, j);
+            const double rtj = __shfl_sync(FULL, rt, j);
+            const bool stj = __shfl_sync(FULL, is_stop, j);
+            if (!okj) {
+                if (lane == 0) {
+                    rs.st = CT_STATUS_ERROR; rs.err = -4;
+                    if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)cj;
+                }
+                done = 1; break;
+            }
+            if (lane == 0) {
+                out_idx[rs.ns] = (int32_t)cj; out_prof[rs.ns] = 0; ++rs.ns;
+                uint32_t m = 1u << (cj & 31);
+                if (!(expl[cj >> 5] & m)) { expl[cj >> 5] |= m; ++rs.n_expl; }
+            }
+            if (stj) {
+                if (lane == 0) rs.st = CT_STATUS_STOPPED;
+                done = 1; break;
+            }
+            if (rtj <= t_best) { t_best = rtj; if (lane == 0) rs.c_prof = cj; }
+        }
+        if (!done && exhausted) {
+            if (lane == 0) rs.st = CT_STATUS_EXHAUSTED;
+            done = 1;
+        }
+    }
+    if (lane == 0) rs.rng.state = g.state;
+    if (lane == 0) ctl.done = done;
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// k_profile_search: one CTA runs one repetition end to end (then the next one
+// of its persistent slice); the serial phases run on warp 0 while the other
+// warps wait at the CTA barrier.
 template <int NT, bool SMEM>
 __global__ void __launch_bounds__(NT, (NT <= 64) ? 8 : ((NT == 128) ? 7 : (896 / NT)))
 k_profile_search(const SearchArgs a) {
@@ -200,7 +509,6 @@ k_profile_search(const SearchArgs a) {
     __shared__ Ctl<NW> ctl;
     __shared__ RepState rs;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t N = a.n;
 
     __shared__ uint32_t seed_sh[SEED_INLINE_WORDS];
     // PCG64 jump-ahead tables: k steps = (A_k, C_k), k = 0..32
@@ -226,276 +534,31 @@ k_profile_search(const SearchArgs a) {
 #define CT_CLK(acc) do { } while (0)
 #endif
     for (int rep = blockIdx.x; rep < a.n_reps; rep += gridDim.x) {
-        for (int64_t i = tid; i < a.nwords; i += NT) expl[i] = 0u;
-
-        // per-repetition serial state lives in shared memory (only lane 0 of
-        // warp 0 updates it), so it costs no registers in the parallel phases
         int32_t* out_idx = a.step_index + (size_t)rep * a.max_steps;
         uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
-        if (tid == 0) {
-            rs.c_prof = 0; rs.ns = 0; rs.n_expl = 0; rs.st = CT_STATUS_BUDGET; rs.err = 0;
-            rs.scored = 0; rs.draws = 0; rs.uncert = 0; rs.outers = 0; rs.abytes = 0;
-            rs.rng.seed(seed_pool(seed_words_of(a.seed, seed_sh, rep)));
-            rs.c_prof = (int64_t)rs.rng.integers((uint64_t)N);
-            ctl.done = 0;
-        }
+        if (warp == 0) rep_begin(a, seed_sh, rep, rs, ctl, expl, lane);
         __syncthreads();
 
         for (int it = 0; it < a.outer; ++it) {
 #ifdef CT_PHASE_CLOCKS
             if (tid == 0) clk_t = clock64();
 #endif
-            // ---------------- profile step, expert system (warp 0) ------------
-            // One lane per counter fetches the profile's replayed counters and
-            // one lane per delta key its predicted value p; the 18 bottleneck
-            // components and their reactions are then evaluated on 18 lanes
-            // (the same per-component code as the scalar analyze()/react())
-            // and the active terms compacted in react() order with a ballot.
-            if (warp == 0) {
-                const int64_t cp = rs.c_prof;
-                if (lane < N_REQ) ctl.cnt[lane] = a.counters[(size_t)cp * N_REQ + lane];
-                const int col = (lane < N_COMP) ? a.delta_col[lane] : -1;
-                const double pv = (col >= 0) ? a.table[(size_t)col * a.ld + cp] : 0.0;
-                const bool rec_ok = a.has_record[cp] != 0;
-                const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cp);
-                const int64_t thr = a.threads[cp];
-                __syncwarp();
-                double dk = 0.0;
-                if (lane < N_COMP) {
-                    const double bk = analyze_component(ctl.cnt, lane, a.generation, a.cores, thr,
-                                                        degenerate_of(ctl.cnt));
-                    dk = react_component(bk, lane, a.inst_reaction, a.issue_sign);
-                }
-                const bool act = (lane < N_COMP) && dk != 0.0 && col >= 0 && pv != 0.0;
-                const unsigned amask = __ballot_sync(FULL, act);
-                if (act) {
-                    const int slot = __popc(amask & ((1u << lane) - 1u));
-                    ctl.act[slot].col = col;
-                    ctl.act[slot].p = pv;
-                    // literal sign: (-d)(c - p) == d(p - c) exactly
-                    ctl.act[slot].d = a.literal_sign ? -dk : dk;
-                }
-                // certified division domain for every active term
-                const double two_m200 = 6.223015277861142e-61;
-                const bool cert_ok = !act || (col < 64 && ((a.col_cert >> col) & 1ull) &&
-                                              fabs(dk) >= two_m200);
-                const bool cert_all = __all_sync(FULL, cert_ok);
-                if (lane == 0) {
-                    const int na = __popc(amask);
-                    ctl.n_act = na;
-                    ctl.cert_terms = cert_all ? 1 : 0;
-                    if (!rec_ok) {
-                        rs.st = CT_STATUS_ERROR; rs.err = -4; ctl.done = 1;
-                        if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)cp;   // failing index
-                    } else {
-                        out_idx[rs.ns] = (int32_t)cp; out_prof[rs.ns] = 1; ++rs.ns;
-                        uint32_t m = 1u << (cp & 31);
-                        if (!(expl[cp >> 5] & m)) { expl[cp >> 5] |= m; ++rs.n_expl; }
-                        if (is_stop) { rs.st = CT_STATUS_STOPPED; ctl.done = 1; }
-                        else if (rs.n_expl >= N) { rs.st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
-                        else {
-                            unsigned long long pool = (unsigned long long)(N - rs.n_expl);
-                            rs.scored += pool; ++rs.outers;
-                            rs.abytes += pool * (8ull * (unsigned long long)na + 16ull);
-                        }
-                    }
-                }
-            }
+            if (warp == 0) profile_step(a, rs, ctl, expl, out_idx, out_prof, lane);
             __syncthreads();
             CT_CLK(clk_p1);
             if (ctl.done) break;
-
-            // ---------------- Eq. 16 raw scores (all threads) ------------------
-            double lmax = -INFINITY, lmin = INFINITY, lamin = INFINITY;
-            if (ctl.cert_terms) score_pass<NT, true>(a, ctl, expl, w, lmax, lmin, lamin);
-            else score_pass<NT, false>(a, ctl, expl, w, lmax, lmin, lamin);
-            lmax = warp_max(lmax);
-            lmin = warp_min(lmin);
-#pragma unroll
-            for (int m = 16; m > 0; m >>= 1) lamin = fmin(lamin, __shfl_xor_sync(FULL, lamin, m));
-            if (lane == 0) { ctl.red_max[warp] = lmax; ctl.red_min[warp] = lmin; ctl.red_amin[warp] = lamin; }
+            score_phase<NT>(a, ctl, expl, w, tid);
             __syncthreads();
             CT_CLK(clk_score);
-
-            // ---------------- Eq. 17 weights + exact row totals ----------------
-            {
-                double smax = ctl.red_max[0], smin = ctl.red_min[0], amin = ctl.red_amin[0];
-#pragma unroll
-                for (int i = 1; i < NW; ++i) {
-                    smax = nmax(smax, ctl.red_max[i]); smin = nmin(smin, ctl.red_min[i]);
-                    amin = fmin(amin, ctl.red_amin[i]);
-                }
-                // certified Eq. 17 domain: every nonzero |s| in [2^-400, 2^400]
-                // (NaN extrema fail the comparisons)
-                const double lo = 3.872591914849318e-121, hi = 2.5822498780869086e+120;
-                const bool cert = (amin >= lo || amin == INFINITY) && smax <= hi && smin >= -hi;
-                u128 wtot = 0;
-                int pos = 0, bad = 0;
-                if (cert) weight_pass<true>(a, NW, smax, smin, expl, w, row_tot, wtot, pos, bad);
-                else weight_pass<false>(a, NW, smax, smin, expl, w, row_tot, wtot, pos, bad);
-                pos = warp_sum_i(pos);
-                bad = __any_sync(FULL, bad);
-                if (lane == 0) { ctl.red_tot[warp] = wtot; ctl.red_pos[warp] = pos; ctl.red_bad[warp] = bad; }
-            }
+            weight_phase(a, ctl, expl, w, row_tot, warp);
             __syncthreads();
             CT_CLK(clk_weight);
-
-            // ---------------- n certified draws (warp 0) ----------------------
-            if (warp == 0) {
-                u128 total = 0;
-                int positive = 0, bad = 0;
-#pragma unroll
-                for (int i = 0; i < NW; ++i) {
-                    total += ctl.red_tot[i]; positive += ctl.red_pos[i]; bad |= ctl.red_bad[i];
-                }
-                // each lane owns a contiguous chunk of rows; its inclusive
-                // prefix is kept across the draws and patched after a zeroing
-                const int cpl = (a.nrows + 31) >> 5;
-                const int t0 = lane * cpl, t1 = min(t0 + cpl, a.nrows);
-                u128 mine = 0;
-                for (int t = t0; t < t1; ++t) mine += row_tot[t];
-                u128 lane_pref = warp_incl_scan(mine, lane);
-                // certificate half-width (SURVEY hard part 3): sequential
-                // float prefix vs exact prefix, weights within 1 ulp, T within
-                // 1 ulp; taken at the iteration's largest total
-                const double bound = (double)(2 * N + 32) * 1.1102230246251565e-16 *
-                                     fx_total_to_double(total);
-                const u128 b_fx = floor_fx(bound) + 1;
-                int done = 0;
-                if (bad) { if (lane == 0) { rs.st = CT_STATUS_ERROR; rs.err = -7; } done = 1; }
-                double t_best = INFINITY;
-                // The iteration's uniforms come 32 at a time from the
-                // repetition's PCG64 by jump-ahead (lane j: the (j+1)-th next
-                // Generator.random()), the draws of a chunk touch shared
-                // memory only, and their replay lookups are issued together
-                // afterwards: one L2 round trip per chunk instead of one per
-                // draw.  Draws past a stop / error are discarded (the
-                // repetition ends there, as the reference's loop does).
-                Pcg64 g;
-                g.state = rs.rng.state;
-                g.inc = rs.rng.inc;
-                int k = 0;
-                bool exhausted = false;
-                while (k < a.inner && !done) {
-                    const int k0 = k;
-                    const int cnt = min(32, a.inner - k0);
-                    const double u_lane = (lane < cnt) ? g.double_after(jA[lane + 1], jC[lane + 1]) : 0.0;
-                    int64_t my_choice = -1;
-                    for (; k < k0 + cnt; ++k) {
-                        if (positive <= 0) { exhausted = true; break; }
-                        const double u = __shfl_sync(FULL, u_lane, k - k0);
-                        const double r = mul(u, fx_total_to_double(total));
-                        const u128 r_fx = floor_fx(r);
-                        // the lane whose row chunk holds r, then the row, then
-                        // the configuration: one ballot each
-                        int64_t chosen = -1;
-                        bool ok = false;
-                        u128 wfx = 0;
-                        int row = -1, l2 = 0;
-                        const unsigned bal = __ballot_sync(FULL, lane_pref > r_fx);
-                        if (bal) {
-                            const int L = __ffs(bal) - 1;
-                            u128 carry = lane_pref - mine;
-                            if (lane == L) {
-                                for (int t = t0; t < t1; ++t) {
-                                    const u128 nxt = carry + row_tot[t];
-                                    if (nxt > r_fx) { row = t; break; }
-                                    carry = nxt;
-                                }
-                            }
-                            row = __shfl_sync(FULL, row, L);
-                            carry = shfl_u128(carry, L);
-                            // exact in-row prefix of the row holding r
-                            Limbs f;
-                            weight_limbs(w[32LL * row + lane], &f);
-                            const u128 incl = warp_incl_scan_limbs(f, lane);
-                            l2 = __ffs(__ballot_sync(FULL, carry + incl > r_fx)) - 1;
-                            const int src = l2 < 0 ? 0 : l2;
-                            wfx = shfl_u128(limbs_value(f.l0, f.l1, f.l2), src);
-                            const u128 before = carry + shfl_u128(incl, src) - wfx;
-                            chosen = 32LL * row + l2;
-                            // r far enough from both boundaries of the chosen
-                            // configuration: the reference's sequential cumsum
-                            // picks it too
-                            ok = l2 >= 0 && (r_fx - before > b_fx) && (before + wfx - r_fx - 1 > b_fx);
-                            ok = ok && !a.force_sequential;
-                        }
-                        if (!ok) {
-                            if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
-                            chosen = __shfl_sync(FULL, (long long)chosen, 0);
-                            if (chosen >= 0 && chosen < N) {
-                                row = (int)(chosen >> 5); l2 = (int)(chosen & 31);
-                                to_fx(w[chosen], &wfx);
-                            }
-                        }
-                        if (lane == 0) ++rs.draws;
-                        if (lane == k - k0) my_choice = chosen;
-                        if (!(chosen >= 0 && chosen < N)) { ++k; break; }   // recorded as an error below
-                        // zero the drawn weight: its row total and the lane
-                        // prefixes drop by wfx (exact)
-                        __syncwarp();
-                        if (lane == 0) { w[chosen] = 0.0; row_tot[row] -= wfx; }
-                        if (row >= t0 && row < t1) mine -= wfx;
-                        if (row < t1) lane_pref -= wfx;
-                        total -= wfx;
-                        --positive;
-                        __syncwarp();
-                    }
-                    const int made = k - k0;
-                    g.advance(jA[made], jC[made]);
-                    // replay lookups of the chunk's draws, one per lane
-                    const bool mine_in = lane < made && my_choice >= 0 && my_choice < N;
-                    const int64_t cs = mine_in ? my_choice : 0;
-                    const bool rec_ok = mine_in && a.has_record[cs];
-                    const double rt = a.runtime[cs];
-                    const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cs);
-                    // the reference's bookkeeping, draw by draw
-                    for (int j = 0; j < made; ++j) {
-                        const int64_t cj = __shfl_sync(FULL, (long long)my_choice, j);
-                        const bool okj = __shfl_sync(FULL, rec_ok, j);
-                        const double rtj = __shfl_sync(FULL, rt, j);
-                        const bool stj = __shfl_sync(FULL, is_stop, j);
-                        if (!okj) {
-                            if (lane == 0) {
-                                rs.st = CT_STATUS_ERROR; rs.err = -4;
-                                if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)cj;
-                            }
-                            done = 1; break;
-                        }
-                        if (lane == 0) {
-                            out_idx[rs.ns] = (int32_t)cj; out_prof[rs.ns] = 0; ++rs.ns;
-                            uint32_t m = 1u << (cj & 31);
-                            if (!(expl[cj >> 5] & m)) { expl[cj >> 5] |= m; ++rs.n_expl; }
-                        }
-                        if (stj) {
-                            if (lane == 0) rs.st = CT_STATUS_STOPPED;
-                            done = 1; break;
-                        }
-                        if (rtj <= t_best) { t_best = rtj; if (lane == 0) rs.c_prof = cj; }
-                    }
-                    if (!done && exhausted) {
-                        if (lane == 0) rs.st = CT_STATUS_EXHAUSTED;
-                        done = 1;
-                    }
-                }
-                if (lane == 0) rs.rng.state = g.state;
-                if (lane == 0) ctl.done = done;
-            }
+            if (warp == 0) draw_step(a, rs, ctl, expl, w, row_tot, jA, jC, out_idx, out_prof, lane);
             __syncthreads();
             CT_CLK(clk_p4);
             if (ctl.done) break;
         }
-
-        if (tid == 0) {
-            a.n_steps[rep] = (int32_t)rs.ns;
-            a.status[rep] = rs.st;
-            a.rep_error[rep] = rs.err;
-            atomicAdd(&a.stats[0], rs.scored);
-            atomicAdd(&a.stats[1], rs.draws);
-            atomicAdd(&a.stats[2], rs.uncert);
-            atomicAdd(&a.stats[3], rs.outers);
-            atomicAdd(&a.stats[4], rs.abytes);
-        }
+        if (tid == 0) rep_end(a, rep, rs);
         __syncthreads();
     }
 #ifdef CT_PHASE_CLOCKS
@@ -503,6 +566,156 @@ k_profile_search(const SearchArgs a) {
         printf("[clk] cta %d: profile+expert %lld score %lld weights %lld draws %lld cycles\n",
                blockIdx.x, clk_p1, clk_score, clk_weight, clk_p4);
 #endif
+}
+
+// ---------------------------------------------------------------------------
+// k_profile_search_ws: warp-specialised, two repetitions per CTA.
+//
+// In k_profile_search the serial phases (profile step + expert system, the n
+// draws) keep NW-1 warps idle at the CTA barrier.  Here warp 0 is the serial
+// warp and warps 1..PW the parallel warps, and the CTA interleaves two
+// repetitions (slots 0 and 1): while the serial warp runs slot s's draws and
+// its next profile step, the parallel warps score and weight slot s^1.
+// Hand-off through named barriers (bar.arrive by the producer, bar.sync by
+// the consumer; both order shared-memory accesses):
+//   READY_s (1 + s): the serial warp has set up slot s (ctl[s].cmd says
+//                    RUN / SKIP / EXIT)
+//   DONE_s  (3 + s): the parallel warps have finished slot s
+//   barrier 5      : among the parallel warps, between Eq. 16 and Eq. 17
+// Every repetition executes exactly the phases k_profile_search executes,
+// in the same order, so its trajectory is identical.
+enum : int { WS_RUN = 0, WS_SKIP = 1, WS_EXIT = 2 };
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int PW, bool SMEM>
+__global__ void __launch_bounds__(32 * (PW + 1), (PW <= 4) ? 4 : (PW <= 6 ? 4 : 3))
+k_profile_search_ws(const SearchArgs a) {
+    constexpr int PT = 32 * PW, NTT = PT + 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ Ctl<PW> ctl[2];
+    __shared__ RepState rs[2];
+    __shared__ uint32_t seed_sh[SEED_INLINE_WORDS];
+    __shared__ u128 jA[33], jC[33];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) Pcg64::jump_tables(jA, jC, 32);
+    load_seed_words(a.seed, seed_sh);      // ends with __syncthreads()
+
+    // dynamic shared memory, per slot: row totals | explored bits | [weights]
+    const size_t head = (sizeof(u128) * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+    const size_t per_slot = head + (SMEM ? 8 * 32 * (size_t)a.nrows : 0);
+    u128* row_tot[2];
+    uint32_t* expl[2];
+    double* w[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        unsigned char* base = smem + per_slot * s;
+        row_tot[s] = reinterpret_cast<u128*>(base);
+        expl[s] = reinterpret_cast<uint32_t*>(base + sizeof(u128) * (size_t)a.nrows);
+        w[s] = SMEM ? reinterpret_cast<double*>(base + head)
+                    : a.scratch_w + (size_t)(2 * blockIdx.x + s) * 32 * (size_t)a.nrows;
+    }
+    const int stride = 2 * gridDim.x;
+
+    if (warp == 0) {
+        // ------------------------------ serial warp ------------------------
+        int rep[2], it[2];
+#ifdef CT_PHASE_CLOCKS
+        long long clk_wait = 0, clk_work = 0, clk_t = clock64();
+#endif
+        // set up slot s with its next repetition that still has a parallel
+        // phase to run (a repetition can end at its first profile step)
+        auto next_run = [&](int s) {
+            while (rep[s] < a.n_reps) {
+                int32_t* out_idx = a.step_index + (size_t)rep[s] * a.max_steps;
+                uint8_t* out_prof = a.step_profiled + (size_t)rep[s] * a.max_steps;
+                if (it[s] < 0) { rep_begin(a, seed_sh, rep[s], rs[s], ctl[s], expl[s], lane); it[s] = 0; }
+                profile_step(a, rs[s], ctl[s], expl[s], out_idx, out_prof, lane);
+                if (!ctl[s].done) { if (lane == 0) ctl[s].cmd = WS_RUN; __syncwarp(); return; }
+                if (lane == 0) rep_end(a, rep[s], rs[s]);
+                rep[s] += stride; it[s] = -1;
+            }
+            if (lane == 0) ctl[s].cmd = WS_SKIP;
+            __syncwarp();
+        };
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            rep[s] = 2 * blockIdx.x + s; it[s] = -1;
+            next_run(s);
+            bar_arrive_n(1 + s, NTT);
+        }
+        int cur = 0;
+        for (;;) {
+#ifdef CT_PHASE_CLOCKS
+            long long t_ = clock64(); clk_work += t_ - clk_t; clk_t = t_;
+#endif
+            bar_sync_n(3 + cur, NTT);
+#ifdef CT_PHASE_CLOCKS
+            t_ = clock64(); clk_wait += t_ - clk_t; clk_t = t_;
+#endif
+            if (ctl[cur].cmd == WS_RUN) {
+                int32_t* out_idx = a.step_index + (size_t)rep[cur] * a.max_steps;
+                uint8_t* out_prof = a.step_profiled + (size_t)rep[cur] * a.max_steps;
+                draw_step(a, rs[cur], ctl[cur], expl[cur], w[cur], row_tot[cur], jA, jC, out_idx,
+                          out_prof, lane);
+                ++it[cur];
+                if (ctl[cur].done || it[cur] >= a.outer) {
+                    if (lane == 0) rep_end(a, rep[cur], rs[cur]);
+                    rep[cur] += stride; it[cur] = -1;
+                }
+                next_run(cur);
+            }
+            if (ctl[0].cmd == WS_SKIP && ctl[1].cmd == WS_SKIP) {
+                if (lane == 0) ctl[cur].cmd = WS_EXIT;
+                __syncwarp();
+                bar_arrive_n(1 + cur, NTT);
+                bar_sync_n(3 + (cur ^ 1), NTT);
+                break;
+            }
+            bar_arrive_n(1 + cur, NTT);
+            cur ^= 1;
+        }
+#ifdef CT_PHASE_CLOCKS
+        if (lane == 0 && (blockIdx.x % 37) == 0)
+            printf("[clk-ws] cta %d: serial warp busy %lld waiting %lld cycles\n", blockIdx.x,
+                   clk_work, clk_wait);
+#endif
+    } else {
+        // ------------------------------ parallel warps ---------------------
+        const int ptid = tid - 32, pw = warp - 1;
+        int cur = 0;
+#ifdef CT_PHASE_CLOCKS
+        long long clk_wait = 0, clk_work = 0, clk_t = clock64();
+#endif
+        for (;;) {
+            bar_sync_n(1 + cur, NTT);
+#ifdef CT_PHASE_CLOCKS
+            long long t_ = clock64(); clk_wait += t_ - clk_t; clk_t = t_;
+#endif
+            const int cmd = ctl[cur].cmd;
+            if (cmd == WS_EXIT) break;
+            if (cmd == WS_RUN) {
+                score_phase<PT>(a, ctl[cur], expl[cur], w[cur], ptid);
+                bar_sync_n(5, PT);
+                weight_phase(a, ctl[cur], expl[cur], w[cur], row_tot[cur], pw);
+            }
+#ifdef CT_PHASE_CLOCKS
+            t_ = clock64(); clk_work += t_ - clk_t; clk_t = t_;
+#endif
+            bar_arrive_n(3 + cur, NTT);
+            cur ^= 1;
+        }
+#ifdef CT_PHASE_CLOCKS
+        if (tid == 32 && (blockIdx.x % 37) == 0)
+            printf("[clk-ws] cta %d: parallel warps busy %lld waiting %lld cycles\n", blockIdx.x,
+                   clk_work, clk_wait);
+#endif
+    }
 }
 
 // ---------------------------------------------------------------------------

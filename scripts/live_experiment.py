@@ -1,0 +1,132 @@
+"""The paper's experiments on real B200 datasets (BASELINE metric: empirical
+steps & wall-s to reach <= 1.1x the exhaustive best).
+
+For every dataset directory given (written by scripts/live_sweep.py):
+
+  1. replay: harness.simulate of the profile searcher (exact model, and a
+     decision-tree model trained on the same dataset) and of random search,
+     R = 1000 repetitions on the GPU -> mean steps, censored, improvement
+     (the paper's Table 4 layout), simulated wall-s with the MEASURED
+     profiling overhead (profiled step cost / unprofiled step cost);
+  2. live (optional, --live K): K real searches per searcher against the
+     benchmark kernels themselves (NVRTC compile + CUDA-event timing + CUPTI
+     profiling inside the loop), wall-clock seconds until a configuration
+     within 1.1x of the dataset's best was measured.
+
+    python scripts/live_experiment.py gpurun_out/datasets/*-b200 [--live 5] \
+        [--out gpurun_out/experiments.json]
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def replay(ds, reps, seed, overhead):
+    from paper_2102_05297_b200 import ExactModelSet, ExperimentSpec, simulate
+    from paper_2102_05297_b200.models import train_model_set
+    out = {}
+    random = simulate(ExperimentSpec(dataset=ds, searcher="random", repetitions=reps, seed=seed,
+                                     profiling_overhead=overhead))
+    out["random_mean_steps"] = float(np.mean(random.steps))
+    out["random_mean_wall_s"] = random.mean_time_seconds
+    for label, model in (("exact", ExactModelSet(ds)), ("tree", train_model_set(ds, "tree", 0))):
+        rep = simulate(ExperimentSpec(dataset=ds, searcher="profile", model=model,
+                                      repetitions=reps, seed=seed, profiling_overhead=overhead))
+        out[f"profile_{label}_mean_steps"] = float(np.mean(rep.steps))
+        out[f"profile_{label}_censored"] = int(rep.censored)
+        out[f"profile_{label}_mean_wall_s"] = rep.mean_time_seconds
+        out[f"improvement_{label}"] = out["random_mean_steps"] / float(np.mean(rep.steps))
+    return out
+
+
+def live(name, ds, k, seed):
+    """k real searches per searcher; wall seconds to the first <=1.1x config."""
+    from paper_2102_05297_b200 import ExactModelSet, ProfileSearcher
+    from paper_2102_05297_b200.live import CudaMeasurementSource, benchmark
+    from paper_2102_05297_b200.space import well_performing_set
+    bench = benchmark(name)
+    src = CudaMeasurementSource(bench)
+    stop = set(well_performing_set(ds, 1.1))
+    model = ExactModelSet(ds)
+    res = {"profile_wall_s": [], "profile_steps": [], "random_wall_s": [], "random_steps": []}
+    seeds = np.random.SeedSequence(seed).spawn(2 * k)
+    for r in range(k):
+        # profile searcher, measurements live (compile on first use)
+        src._variants.clear()
+        t0 = time.perf_counter()
+        s = ProfileSearcher(model, ds.space, ds.arch, i=max(1, -(-(len(ds.space) - 1) // 5)),
+                            seed=seeds[r], stop_indices=stop)
+        steps = 0
+        while (req := s.next_config()) is not None:
+            s.add_result(src.measure(*req))
+            steps += 1
+        res["profile_wall_s"].append(time.perf_counter() - t0)
+        res["profile_steps"].append(steps)
+        # random search, same measurement path
+        src._variants.clear()
+        t0 = time.perf_counter()
+        order = np.random.default_rng(seeds[k + r]).permutation(len(ds.space))
+        steps = 0
+        for idx in order:
+            src.measure(int(idx), profiled=False)
+            steps += 1
+            if int(idx) in stop:
+                break
+        res["random_wall_s"].append(time.perf_counter() - t0)
+        res["random_steps"].append(steps)
+    # measured profiling overhead on the dataset's best configuration
+    best = int(np.argmin(np.where(ds.has_record, ds.runtime_us, np.inf)))
+    t0 = time.perf_counter()
+    for _ in range(3):
+        src.measure(best, profiled=False)
+    t1 = time.perf_counter()
+    for _ in range(3):
+        src.measure(best, profiled=True)
+    t2 = time.perf_counter()
+    res["profiled_step_s"] = (t2 - t1) / 3
+    res["timed_step_s"] = (t1 - t0) / 3
+    res["profile_passes"] = src.profile_passes
+    src.close()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("dirs", nargs="+")
+    ap.add_argument("--reps", type=int, default=1000)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--live", type=int, default=0)
+    ap.add_argument("--overhead", type=float, default=3.0)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    from paper_2102_05297_b200 import formats
+    results = {}
+    for d in a.dirs:
+        ds = formats.load_dataset_dir(d)
+        name = os.path.basename(os.path.normpath(d)).replace("-b200", "")
+        r = {"configs": len(ds.space), "measured": int(ds.has_record.sum()),
+             "best_us": float(ds.best_runtime),
+             "well_performing": int(len(__import__("paper_2102_05297_b200").well_performing_set(ds, 1.1)))}
+        overhead = a.overhead
+        if a.live:
+            r["live"] = live(name, ds, a.live, a.seed)
+            overhead = r["live"]["profiled_step_s"] / max(r["live"]["timed_step_s"], 1e-9)
+            r["measured_profiling_overhead"] = overhead
+        r["replay"] = replay(ds, a.reps, a.seed, overhead)
+        results[name] = r
+        print(json.dumps({name: r}), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(results, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -156,7 +156,7 @@ int hc_profile_search(const double* table, int64_t n, const double* runtime,
             if (d[k] == 0.0 || prm->delta_columns[k] < 0) continue;
             double pv = table[prm->delta_columns[k] * n + c_prof];
             if (pv == 0.0) continue;
-            act[na].col = prm->delta_columns[k]; act[na].d = d[k]; act[na].p = pv; ++na;
+            act[na].col = prm->delta_columns[k]; act[na].nz = 0; act[na].d = d[k]; act[na].p = pv; ++na;
         }
         if (n_expl >= n) { status = CT_STATUS_EXHAUSTED; break; }
         *scored += n - n_expl;

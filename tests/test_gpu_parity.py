@@ -297,3 +297,18 @@ def test_gpu_model_inference_matches_reference_table(name, family):
     ds = dataset_from_golden("gradient") if name == "gradient" else spaces.SPACES[name]()
     table = PredictionTable.from_model_set(ms, ds.space)
     np.testing.assert_array_equal(table.matrix.view(np.uint64), want.view(np.uint64))
+
+
+def test_device_expert_system_bit_exact():
+    """The search kernel's warp expert system (analyze_component_warp, run by
+    ct_analyze_react) against the 3,020 reference-recorded cases, bit for bit."""
+    from paper_2102_05297_b200 import _native
+    e = golden("expert.npz")
+    ctx = _native.context(0)
+    for k in range(e["counters"].shape[0]):
+        b, d, deg = ctx.analyze_react(e["counters"][k], int(e["generation"][k]),
+                                      int(e["cores"][k]), int(e["threads"][k]),
+                                      float(e["inst_reaction"][k]))
+        np.testing.assert_array_equal(b, e["b"][k], err_msg=f"case {k}")
+        np.testing.assert_array_equal(d, e["delta"][k], err_msg=f"case {k}")
+        assert deg == bool(e["degenerate"][k])
