@@ -310,13 +310,14 @@ class CudaMeasurementSource:
 
     def __init__(self, bench: Benchmark, device: int = 0, tuner: Optional[Tuner] = None,
                  warmup: int = 1, reps: int = 3, flush_l2: bool = True,
-                 metrics: Sequence[str] = TABLE1_METRICS):
+                 metrics: Sequence[str] = TABLE1_METRICS, slow_us: float = 5000.0):
         self.bench = bench
         self.tuner = tuner if tuner is not None else Tuner(device)
         self._own_tuner = tuner is None
         self.space = bench.space
         self.arch = b200_arch(self.tuner.sm_count)
         self.warmup, self.reps, self.flush_l2 = warmup, reps, flush_l2
+        self.slow_us = slow_us
         self.metrics = tuple(metrics)
         self._bufs = bench.setup(self.tuner)
         self._variants: Dict[int, int] = {}
@@ -362,8 +363,14 @@ class CudaMeasurementSource:
         v = self.variant(config_index)
         launch = self.launch_of(config_index)
         try:
-            times = self.tuner.time(v, launch, warmup=self.warmup, reps=self.reps,
-                                    flush_l2=self.flush_l2)
+            times = self.tuner.time(v, launch, warmup=self.warmup, reps=1, flush_l2=self.flush_l2)
+            # a slow variant (>= slow_us) is timed once: its run-to-run spread
+            # is far below the gaps the search distinguishes, and a sweep of a
+            # space full of pathological variants stays affordable
+            if self.reps > 1 and times[0] < self.slow_us:
+                more = self.tuner.time(v, launch, warmup=0, reps=self.reps - 1,
+                                       flush_l2=self.flush_l2)
+                times = np.concatenate([times, more])
         except LaunchError as e:
             raise CounterTuneError(f"configuration {config_index} failed to launch: {e}")
         runtime = float(np.median(times))
@@ -405,12 +412,15 @@ class SweepResult:
 
 
 def sweep(source: CudaMeasurementSource, profiled: bool = True, checkpoint: Optional[str] = None,
-          compile_threads: int = 0, progress=None) -> SweepResult:
+          compile_threads: int = 0, progress=None,
+          budget_s: Optional[float] = None) -> SweepResult:
     """Exhaustive sweep of the source's space -> a replay Dataset in the
     reference's layout (runtime, threads, the Table-1 counters canonicalised).
 
-    With ``checkpoint`` the partial results are kept in an .npz after every
-    configuration and a rerun resumes from it (config_index order)."""
+    With ``checkpoint`` the partial results are kept in an .npz every 64
+    configurations and a rerun resumes from it (config_index order).  With
+    ``budget_s`` measuring stops after that many seconds; configurations not
+    reached carry no record (a later run with the same checkpoint resumes)."""
     import time
     n = len(source.space)
     names = TABLE1_ABBRS
@@ -428,6 +438,8 @@ def sweep(source: CudaMeasurementSource, profiled: bool = True, checkpoint: Opti
     for i in range(n):
         if done[i] or i in failures:
             continue
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
         try:
             m = source.measure(i, profiled=profiled)
         except CounterTuneError as e:
@@ -440,6 +452,8 @@ def sweep(source: CudaMeasurementSource, profiled: bool = True, checkpoint: Opti
         done[i] = True
         if checkpoint and (i % 64 == 63 or i == n - 1):
             np.savez(checkpoint, runtime=runtime, threads=threads, counters=cm, done=done)
+    if checkpoint:
+        np.savez(checkpoint, runtime=runtime, threads=threads, counters=cm, done=done)
         if progress:
             progress(i, n)
     t2 = time.perf_counter()

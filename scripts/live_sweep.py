@@ -43,6 +43,12 @@ def roofline(bench, runtime_us, pk):
     if bench.name == "nbody":
         fl = 20.0 * work
         return fl / t / 1e12, pk["fp32"] / 1e12, "TFLOP/s (20 flop/interaction)", fl / t / pk["fp32"]
+    if bench.name == "conv":
+        # both bounds are close at 7x7: the roofline time is the larger one
+        bytes_ = 2.0 * 4.0 * bench.width * bench.height
+        t_roof = max(work / pk["fp32"], bytes_ / pk["hbm"])
+        return work / t / 1e12, pk["fp32"] / 1e12, \
+            "TFLOP/s (frac = max(flop, HBM-byte) roofline time / time)", t_roof / t
     return work / t / 1e12, pk["fp32"] / 1e12, "TFLOP/s", work / t / pk["fp32"]
 
 
@@ -55,6 +61,8 @@ def main():
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--limit", type=int, default=0, help="sweep only the first K configs")
+    ap.add_argument("--budget-s", type=float, default=None,
+                    help="stop measuring after this many seconds (partial dataset)")
     args = ap.parse_args()
 
     from paper_2102_05297_b200 import formats, live
@@ -81,7 +89,7 @@ def main():
                           "best_us": float(min(rts)), "passes": src.profile_passes}))
         return
     res = live.sweep(src, profiled=not args.no_profile, checkpoint=args.checkpoint,
-                     progress=progress)
+                     progress=progress, budget_s=args.budget_s)
     ds = res.dataset
     formats.save_dataset(ds, args.out)
     rt = np.where(ds.has_record, ds.runtime_us, np.inf)
