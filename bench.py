@@ -3,9 +3,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Workload (configs[1] of BASELINE.json): the matrix-transpose tuning space
-(1,784 configurations, 8 parameters; synthetic B200 replay dataset, see
-paper_2102_05297_b200/spaces.py), profile-guided searcher with the exact
-model, R = 1000 repetitions per GPU (SeedSequence(42) children), n = 5,
+(1,784 configurations, 8 parameters) replayed from its exhaustive B200 sweep
+(datasets/transpose-b200: every configuration of the NVRTC transpose kernel
+timed and profiled on a B200 by scripts/live_sweep.py, 24 CUPTI counters,
+reference on-disk format), profile-guided searcher with the exact model, R = 1000 repetitions per GPU (SeedSequence(42) children), n = 5,
 i = 40 outer iterations, throughput mode (stop_indices = {}).  One step = one
 batched device search over all R repetitions.  value = configurations scored
 per second over the whole job (sum over ranks / max rank time).
@@ -110,9 +111,17 @@ def dist_env():
     return world, rank, local
 
 
+DATASET = os.path.join(ROOT, "datasets", "transpose-b200")
+
+
+def load_dataset():
+    from paper_2102_05297_b200 import formats
+    return formats.load_dataset_dir(DATASET)
+
+
 def workload(reps=REPS, stop=False):
-    from paper_2102_05297_b200 import ExactModelSet, ExperimentSpec, spaces
-    ds = spaces.transpose()
+    from paper_2102_05297_b200 import ExactModelSet, ExperimentSpec
+    ds = load_dataset()
     spec = ExperimentSpec(dataset=ds, searcher="profile", model=ExactModelSet(ds),
                           name="profile-search", repetitions=reps, inner_steps=INNER,
                           outer_iterations=OUTER, seed=SEED, stop_at_well_performing=stop)
@@ -124,9 +133,9 @@ def _oracle_chunk(args):
     rep_lo, rep_hi, reps_total = args
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import countertune_oracle as oracle
-    from paper_2102_05297_b200 import ExactModelSet, spaces
+    from paper_2102_05297_b200 import ExactModelSet
     from paper_2102_05297_b200.space import replay_arrays
-    ds = spaces.transpose()
+    ds = load_dataset()
     ms = ExactModelSet(ds)
     matrix = ms.prediction_matrix(ds.space)
     column = {n: j for j, n in enumerate(ms.counters)}
@@ -176,7 +185,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "B200-measured replay dataset (datasets/transpose-b200)",
         "config": {"workload": "transpose space (1,784 configs) replay, profile searcher, "
                                f"exact model, i={OUTER}, n={INNER}, throughput mode",
                    "repetitions_per_step": sample},
@@ -334,9 +344,11 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_launch * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "transpose tuning space (1,784 configs, 8 params) replay; "
-                               "profile searcher, exact model, throughput mode",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "B200-measured replay dataset (datasets/transpose-b200)",
+        "config": {"workload": "transpose tuning space (1,784 configs, 8 params) replay of its "
+                               "exhaustive B200 sweep; profile searcher, exact model, "
+                               "throughput mode",
                    "repetitions_per_gpu": REPS, "outer_iterations": OUTER, "inner_steps": INNER,
                    "seed": SEED, "configs_scored_per_step_per_gpu": configs_per_step,
                    "l2": "256 MiB buffer written between timed steps (table 271 KB)",

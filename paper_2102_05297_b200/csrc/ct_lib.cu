@@ -502,7 +502,7 @@ int launch_profile_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
     if (occ < 1) return fail(CT_ERR_CUDA, "search kernel does not fit on an SM");
     int grid = std::min(n_reps, occ * ctx->sm_count);
     if (!SMEM) {
-        CT_CUDA(ctx->scratch_w.ensure((size_t)grid * 32 * (size_t)a.nrows));
+        CT_CUDA(ctx->scratch_w.ensure((size_t)grid * 64 * (size_t)a.nrows));
         a.scratch_w = ctx->scratch_w.p;
     }
     kern<<<grid, NT, smem, ctx->stream>>>(a);
@@ -522,7 +522,7 @@ int launch_profile_ws_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
     if (occ < 1) return fail(CT_ERR_CUDA, "search kernel does not fit on an SM");
     int grid = std::min((n_reps + 1) / 2, occ * ctx->sm_count);
     if (!SMEM) {
-        CT_CUDA(ctx->scratch_w.ensure((size_t)2 * grid * 32 * (size_t)a.nrows));
+        CT_CUDA(ctx->scratch_w.ensure((size_t)2 * grid * 64 * (size_t)a.nrows));
         a.scratch_w = ctx->scratch_w.p;
     }
     kern<<<grid, NTT, smem, ctx->stream>>>(a);
@@ -944,7 +944,7 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     // otherwise a per-CTA slice of global scratch (L2-resident)
     const size_t budget = 200 * 1024;
     const size_t head_b = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
-    const size_t pref_b = 8 * 32 * (size_t)a.nrows;
+    const size_t pref_b = 16 * 32 * (size_t)a.nrows;   // weights + in-row prefixes
     if (head_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the row index");
     const int64_t want_per_sm = std::min<int64_t>(std::min<int64_t>(
         (n_reps + ctx->sm_count - 1) / ctx->sm_count, 32), 2048 / nt);
@@ -956,7 +956,7 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     // warp-specialised two-repetition kernel (CT_SEARCH_WS = parallel warps)
     int ws = 0;
     if (const char* env = std::getenv("CT_SEARCH_WS")) ws = std::atoi(env);
-    if (ws > 0) {
+    if (ws > 0 && 2 * head_b <= budget) {
         // two slots per CTA: weights in shared memory when both fit
         const int64_t ctas_per_sm = std::max<int64_t>(1, (want_per_sm + 1) / 2);
         const size_t cap2 = std::min<size_t>(

@@ -108,7 +108,6 @@ struct __align__(16) RepState {
 
 template <int NW>
 struct __align__(16) Ctl {
-    u128 red_tot[NW];
     double red_max[NW];
     double red_min[NW];
     double red_amin[NW];
@@ -144,6 +143,20 @@ __device__ __forceinline__ void score_epilogue(double acc, int64_t e, const uint
     nan |= in && (acc != acc);
 }
 
+// one Eq. 16 term added to four configurations' raw scores
+template <bool CERT>
+__device__ __forceinline__ void term4(const ActiveTerm& t, const double* c, double* acc) {
+    const double d = t.d, pv = t.p;
+    if (CERT && t.nz) {      // block-uniform: no zero in the column
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = add(acc[u], raw_term_cert_nz(c[u], d, pv));
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            acc[u] = add(acc[u], CERT ? raw_term_cert(c[u], d, pv) : raw_term_nb(c[u], d, pv));
+    }
+}
+
 template <int PT, bool CERT, int NW>
 __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& ctl,
                                            const uint32_t* expl, double* w, int ptid, double& lmax,
@@ -153,20 +166,24 @@ __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& c
     int64_t base = ptid;
     for (; base + 3LL * PT < N; base += 4LL * PT) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k = 0; k < n_act; ++k) {
-            const double d = ctl.act[k].d, pv = ctl.act[k].p;
+        // two terms per step: eight loads in flight, then the terms in
+        // react() order for each configuration
+        int k = 0;
+        for (; k + 1 < n_act; k += 2) {
+            const double* col0 = a.table + (size_t)ctl.act[k].col * a.ld + base;
+            const double* col1 = a.table + (size_t)ctl.act[k + 1].col * a.ld + base;
+            double c0[4], c1[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { c0[u] = __ldg(col0 + u * PT); c1[u] = __ldg(col1 + u * PT); }
+            term4<CERT>(ctl.act[k], c0, acc);
+            term4<CERT>(ctl.act[k + 1], c1, acc);
+        }
+        if (k < n_act) {
             const double* col = a.table + (size_t)ctl.act[k].col * a.ld + base;
             double c[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) c[u] = __ldg(col + u * PT);
-            if (CERT && ctl.act[k].nz) {      // block-uniform: no zero in the column
-#pragma unroll
-                for (int u = 0; u < 4; ++u) acc[u] = add(acc[u], raw_term_cert_nz(c[u], d, pv));
-            } else {
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    acc[u] = add(acc[u], CERT ? raw_term_cert(c[u], d, pv) : raw_term_nb(c[u], d, pv));
-            }
+            term4<CERT>(ctl.act[k], c, acc);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -183,13 +200,15 @@ __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& c
     }
 }
 
-// Eq. 17 weights over the raw scores and each row's exact total: warp pw of
-// the nw-warp group takes rows pw, pw+nw, ...; lane l owns configuration
-// 32 t + l (padding lanes write weight 0).
+// Eq. 17 weights over the raw scores, each configuration's inclusive in-row
+// prefix and each row's total (float64): warp pw of the nw-warp group takes
+// rows pw, pw+nw, ...; lane l owns configuration 32 t + l (padding lanes
+// write weight 0).  The draws locate r with these sums and certify the choice
+// against their rounding error (draw_step).
 template <bool CERT>
 __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw, double smax,
                                             double smin, const uint32_t* expl, double* w,
-                                            u128* row_tot, u128& wtot, int& pos, int& bad) {
+                                            double* pre, double* row_tot, int& pos, int& bad) {
     const int lane = threadIdx.x & 31;
     const int64_t N = a.n;
     const double gamma = a.gamma;
@@ -199,12 +218,17 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
         double wt = 0.0;
         if (e < N && !bit_get(expl, e)) wt = weight_rcp<CERT>(w[e], smax, smin, y_max, y_min, gamma);
         w[e] = wt;
-        Limbs f;
-        if (!weight_limbs(wt, &f)) bad = 1;
+        // every Eq. 17 weight of finite scores is 0 or in [1e-4, 256]
+        if (!(wt == 0.0 || (wt >= SCORE_FLOOR && wt <= SCORE_CEILING))) bad = 1;
         pos += (wt > 0.0);
-        const u128 tot = warp_sum_limbs(f);
-        if (lane == 0) row_tot[t] = tot;
-        wtot += tot;
+        double incl = wt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double v = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl = add(incl, v);
+        }
+        pre[e] = incl;
+        if (lane == 31) row_tot[t] = incl;
     }
 }
 
@@ -326,11 +350,11 @@ __device__ __forceinline__ void score_phase(const SearchArgs& a, Ctl<NW>& ctl, c
     if (lane == 0) { ctl.red_max[pw] = lmax; ctl.red_min[pw] = lmin; ctl.red_amin[pw] = lamin; }
 }
 
-// Eq. 17 weights + exact row totals for warp pw of the NW-warp group (after
-// every warp's score_phase is visible), reduced into ctl.red_tot/pos/bad[pw].
+// Eq. 17 weights + in-row prefixes for warp pw of the NW-warp group (after
+// every warp's score_phase is visible), reduced into ctl.red_pos/bad[pw].
 template <int NW>
 __device__ __forceinline__ void weight_phase(const SearchArgs& a, Ctl<NW>& ctl, const uint32_t* expl,
-                                             double* w, u128* row_tot, int pw) {
+                                             double* w, double* pre, double* row_tot, int pw) {
     const int lane = threadIdx.x & 31;
     double smax = ctl.red_max[0], smin = ctl.red_min[0], amin = ctl.red_amin[0];
 #pragma unroll
@@ -342,41 +366,49 @@ __device__ __forceinline__ void weight_phase(const SearchArgs& a, Ctl<NW>& ctl, 
     // (NaN extrema fail the comparisons)
     const double lo = 3.872591914849318e-121, hi = 2.5822498780869086e+120;
     const bool cert = (amin >= lo || amin == INFINITY) && smax <= hi && smin >= -hi;
-    u128 wtot = 0;
     int pos = 0, bad = 0;
-    if (cert) weight_pass<true>(a, pw, NW, smax, smin, expl, w, row_tot, wtot, pos, bad);
-    else weight_pass<false>(a, pw, NW, smax, smin, expl, w, row_tot, wtot, pos, bad);
+    if (cert) weight_pass<true>(a, pw, NW, smax, smin, expl, w, pre, row_tot, pos, bad);
+    else weight_pass<false>(a, pw, NW, smax, smin, expl, w, pre, row_tot, pos, bad);
     pos = warp_sum_i(pos);
     bad = __any_sync(FULL, bad);
-    if (lane == 0) { ctl.red_tot[pw] = wtot; ctl.red_pos[pw] = pos; ctl.red_bad[pw] = bad; }
+    if (lane == 0) { ctl.red_pos[pw] = pos; ctl.red_bad[pw] = bad; }
 }
 
 // n certified draws, replay lookups, stop test and the later-ties-win argmin
 // (one full warp).  Sets ctl.done when the repetition ends here.
+//
+// Locating r: lane L owns a contiguous chunk of rows and keeps the inclusive
+// prefix over the chunks (lane_pref); a ballot finds the chunk, lane L walks
+// its rows, and the row's precomputed in-row prefixes give the configuration
+// with one more ballot.  All sums are float64; the choice is CERTIFIED: with
+// P(i-1) <= r < P(i) the computed prefixes around the chosen configuration,
+// the reference's sequential cumsum c over numpy's weights (each within 1 ulp
+// of ours) satisfies |c(j) - P(j)| + |r_ref - r| < B = (8N + 128) 2^-53 T
+// (any summation order of N positive terms errs by < N 2^-53 T; the weight
+// difference adds 2 2^-53 T; r and the zeroing updates a few 2^-53 T more),
+// so P(i-1) + B < r and r + B < P(i) imply that the reference picks i too.
+// Otherwise the draw is re-decided with the sequential float64 cumsum.
 template <int NW>
 __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl<NW>& ctl,
-                                          uint32_t* expl, double* w, u128* row_tot,
+                                          uint32_t* expl, double* w, double* pre, double* row_tot,
                                           const u128* jA, const u128* jC, int32_t* out_idx,
                                           uint8_t* out_prof, int lane) {
     const int64_t N = a.n;
-    u128 total = 0;
     int positive = 0, bad = 0;
 #pragma unroll
-    for (int i = 0; i < NW; ++i) {
-        total += ctl.red_tot[i]; positive += ctl.red_pos[i]; bad |= ctl.red_bad[i];
-    }
-    // each lane owns a contiguous chunk of rows; its inclusive prefix is kept
-    // across the draws and patched after a zeroing
+    for (int i = 0; i < NW; ++i) { positive += ctl.red_pos[i]; bad |= ctl.red_bad[i]; }
     const int cpl = (a.nrows + 31) >> 5;
     const int t0 = lane * cpl, t1 = min(t0 + cpl, a.nrows);
-    u128 mine = 0;
-    for (int t = t0; t < t1; ++t) mine += row_tot[t];
-    u128 lane_pref = warp_incl_scan(mine, lane);
-    // certificate half-width (SURVEY hard part 3): sequential float prefix vs
-    // exact prefix, weights within 1 ulp, T within 1 ulp; taken at the
-    // iteration's largest total
-    const double bound = (double)(2 * N + 32) * 1.1102230246251565e-16 * fx_total_to_double(total);
-    const u128 b_fx = floor_fx(bound) + 1;
+    double mine = 0.0;
+    for (int t = t0; t < t1; ++t) mine = add(mine, row_tot[t]);
+    double lane_pref = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double v = __shfl_up_sync(FULL, lane_pref, d);
+        if (lane >= d) lane_pref = add(lane_pref, v);
+    }
+    double total = __shfl_sync(FULL, lane_pref, 31);
+    const double B = (double)(8 * N + 128) * 1.1102230246251565e-16 * total;   // 2^-53
     int done = 0;
     if (bad) { if (lane == 0) { rs.st = CT_STATUS_ERROR; rs.err = -7; } done = 1; }
     double t_best = INFINITY;
@@ -399,59 +431,54 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
         for (; k < k0 + cnt; ++k) {
             if (positive <= 0) { exhausted = true; break; }
             const double u = __shfl_sync(FULL, u_lane, k - k0);
-            const double r = mul(u, fx_total_to_double(total));
-            const u128 r_fx = floor_fx(r);
-            // the lane whose row chunk holds r, then the row, then the
-            // configuration: one ballot each
+            const double r = mul(u, total);
             int64_t chosen = -1;
             bool ok = false;
-            u128 wfx = 0;
-            int row = -1, l2 = 0;
-            const unsigned bal = __ballot_sync(FULL, lane_pref > r_fx);
+            int row = -1, l2 = -1;
+            const unsigned bal = __ballot_sync(FULL, lane_pref > r);
             if (bal) {
                 const int L = __ffs(bal) - 1;
-                u128 carry = lane_pref - mine;
+                double carry = __shfl_up_sync(FULL, lane_pref, 1);
+                if (lane == 0) carry = 0.0;
                 if (lane == L) {
                     for (int t = t0; t < t1; ++t) {
-                        const u128 nxt = carry + row_tot[t];
-                        if (nxt > r_fx) { row = t; break; }
+                        const double nxt = add(carry, row_tot[t]);
+                        if (nxt > r) { row = t; break; }
                         carry = nxt;
                     }
                 }
                 row = __shfl_sync(FULL, row, L);
-                carry = shfl_u128(carry, L);
-                // exact in-row prefix of the row holding r
-                Limbs f;
-                weight_limbs(w[32LL * row + lane], &f);
-                const u128 incl = warp_incl_scan_limbs(f, lane);
-                l2 = __ffs(__ballot_sync(FULL, carry + incl > r_fx)) - 1;
-                const int src = l2 < 0 ? 0 : l2;
-                wfx = shfl_u128(limbs_value(f.l0, f.l1, f.l2), src);
-                const u128 before = carry + shfl_u128(incl, src) - wfx;
-                chosen = 32LL * row + l2;
-                // r far enough from both boundaries of the chosen
-                // configuration: the reference's sequential cumsum picks it too
-                ok = l2 >= 0 && (r_fx - before > b_fx) && (before + wfx - r_fx - 1 > b_fx);
-                ok = ok && !a.force_sequential;
+                carry = __shfl_sync(FULL, carry, L);
+                if (row >= 0) {
+                    const double v = add(carry, pre[32LL * row + lane]);
+                    l2 = __ffs(__ballot_sync(FULL, v > r)) - 1;
+                    if (l2 >= 0) {
+                        const double p_hi = __shfl_sync(FULL, v, l2);
+                        double p_lo = __shfl_sync(FULL, v, l2 > 0 ? l2 - 1 : 0);
+                        if (l2 == 0) p_lo = carry;
+                        chosen = 32LL * row + l2;
+                        ok = (add(p_lo, B) < r) && (add(r, B) < p_hi) && !a.force_sequential;
+                    }
+                }
             }
             if (!ok) {
                 if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
                 chosen = __shfl_sync(FULL, (long long)chosen, 0);
-                if (chosen >= 0 && chosen < N) {
-                    row = (int)(chosen >> 5); l2 = (int)(chosen & 31);
-                    to_fx(w[chosen], &wfx);
-                }
+                if (chosen >= 0 && chosen < N) { row = (int)(chosen >> 5); l2 = (int)(chosen & 31); }
             }
             if (lane == 0) ++rs.draws;
             if (lane == k - k0) my_choice = chosen;
             if (!(chosen >= 0 && chosen < N)) { ++k; break; }   // recorded as an error below
-            // zero the drawn weight: its row total and the lane prefixes drop
-            // by wfx (exact)
+            // zero the drawn weight: its row's later in-row prefixes, the row
+            // total, the chunk sums and the total drop by it
+            const double wc = w[chosen];
             __syncwarp();
-            if (lane == 0) { w[chosen] = 0.0; row_tot[row] -= wfx; }
-            if (row >= t0 && row < t1) mine -= wfx;
-            if (row < t1) lane_pref -= wfx;
-            total -= wfx;
+            // inclusive prefixes: the drawn configuration's own and the later ones
+            if (lane >= l2) pre[32LL * row + lane] = sub(pre[32LL * row + lane], wc);
+            if (lane == 0) { w[chosen] = 0.0; row_tot[row] = sub(row_tot[row], wc); }
+            if (row >= t0 && row < t1) mine = sub(mine, wc);
+            if (row < t1) lane_pref = sub(lane_pref, wc);
+            total = __shfl_sync(FULL, lane_pref, 31);
             --positive;
             __syncwarp();
         }
@@ -516,16 +543,17 @@ k_profile_search(const SearchArgs a) {
     if (tid == 0) Pcg64::jump_tables(jA, jC, 32);
     load_seed_words(a.seed, seed_sh);
 
-    // dynamic shared memory: row totals | explored bits | [weights]
-    u128* row_tot = reinterpret_cast<u128*>(smem);
-    uint32_t* expl = reinterpret_cast<uint32_t*>(smem + sizeof(u128) * (size_t)a.nrows);
+    // dynamic shared memory: row totals | explored bits | [weights | in-row prefixes]
+    double* row_tot = reinterpret_cast<double*>(smem);
+    uint32_t* expl = reinterpret_cast<uint32_t*>(smem + 16 * (size_t)a.nrows);
     double* w;
     if (SMEM) {
-        const size_t off = (sizeof(u128) * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+        const size_t off = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
         w = reinterpret_cast<double*>(smem + off);
     } else {
-        w = a.scratch_w + (size_t)blockIdx.x * 32 * (size_t)a.nrows;
+        w = a.scratch_w + (size_t)blockIdx.x * 64 * (size_t)a.nrows;
     }
+    double* pre = w + 32 * (size_t)a.nrows;
 
 #ifdef CT_PHASE_CLOCKS
     long long clk_p1 = 0, clk_score = 0, clk_weight = 0, clk_p4 = 0, clk_t = 0;
@@ -550,10 +578,10 @@ k_profile_search(const SearchArgs a) {
             score_phase<NT>(a, ctl, expl, w, tid);
             __syncthreads();
             CT_CLK(clk_score);
-            weight_phase(a, ctl, expl, w, row_tot, warp);
+            weight_phase(a, ctl, expl, w, pre, row_tot, warp);
             __syncthreads();
             CT_CLK(clk_weight);
-            if (warp == 0) draw_step(a, rs, ctl, expl, w, row_tot, jA, jC, out_idx, out_prof, lane);
+            if (warp == 0) draw_step(a, rs, ctl, expl, w, pre, row_tot, jA, jC, out_idx, out_prof, lane);
             __syncthreads();
             CT_CLK(clk_p4);
             if (ctl.done) break;
@@ -606,25 +634,28 @@ k_profile_search_ws(const SearchArgs a) {
     if (tid == 0) Pcg64::jump_tables(jA, jC, 32);
     load_seed_words(a.seed, seed_sh);      // ends with __syncthreads()
 
-    // dynamic shared memory, per slot: row totals | explored bits | [weights]
-    const size_t head = (sizeof(u128) * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
-    const size_t per_slot = head + (SMEM ? 8 * 32 * (size_t)a.nrows : 0);
-    u128* row_tot[2];
+    // dynamic shared memory, per slot: row totals | explored bits |
+    // [weights | in-row prefixes]
+    const size_t head = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+    const size_t per_slot = head + (SMEM ? 16 * 32 * (size_t)a.nrows : 0);
+    double* row_tot[2];
     uint32_t* expl[2];
     double* w[2];
+    double* pre[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
         unsigned char* base = smem + per_slot * s;
-        row_tot[s] = reinterpret_cast<u128*>(base);
-        expl[s] = reinterpret_cast<uint32_t*>(base + sizeof(u128) * (size_t)a.nrows);
+        row_tot[s] = reinterpret_cast<double*>(base);
+        expl[s] = reinterpret_cast<uint32_t*>(base + 16 * (size_t)a.nrows);
         w[s] = SMEM ? reinterpret_cast<double*>(base + head)
-                    : a.scratch_w + (size_t)(2 * blockIdx.x + s) * 32 * (size_t)a.nrows;
+                    : a.scratch_w + (size_t)(2 * blockIdx.x + s) * 64 * (size_t)a.nrows;
+        pre[s] = w[s] + 32 * (size_t)a.nrows;
     }
     const int stride = 2 * gridDim.x;
 
     if (warp == 0) {
         // ------------------------------ serial warp ------------------------
-        int rep[2], it[2];
+        int rep[2] = {0, 0}, it[2] = {-1, -1};
 #ifdef CT_PHASE_CLOCKS
         long long clk_wait = 0, clk_work = 0, clk_t = clock64();
 #endif
@@ -661,8 +692,8 @@ k_profile_search_ws(const SearchArgs a) {
             if (ctl[cur].cmd == WS_RUN) {
                 int32_t* out_idx = a.step_index + (size_t)rep[cur] * a.max_steps;
                 uint8_t* out_prof = a.step_profiled + (size_t)rep[cur] * a.max_steps;
-                draw_step(a, rs[cur], ctl[cur], expl[cur], w[cur], row_tot[cur], jA, jC, out_idx,
-                          out_prof, lane);
+                draw_step(a, rs[cur], ctl[cur], expl[cur], w[cur], pre[cur], row_tot[cur], jA, jC,
+                          out_idx, out_prof, lane);
                 ++it[cur];
                 if (ctl[cur].done || it[cur] >= a.outer) {
                     if (lane == 0) rep_end(a, rep[cur], rs[cur]);
@@ -702,7 +733,7 @@ k_profile_search_ws(const SearchArgs a) {
             if (cmd == WS_RUN) {
                 score_phase<PT>(a, ctl[cur], expl[cur], w[cur], ptid);
                 bar_sync_n(5, PT);
-                weight_phase(a, ctl[cur], expl[cur], w[cur], row_tot[cur], pw);
+                weight_phase(a, ctl[cur], expl[cur], w[cur], pre[cur], row_tot[cur], pw);
             }
 #ifdef CT_PHASE_CLOCKS
             t_ = clock64(); clk_work += t_ - clk_t; clk_t = t_;

@@ -13,7 +13,8 @@ from conftest import dataset_from_golden, golden, ragged
 
 pytestmark = pytest.mark.gpu
 
-TRAJ_SETS = ["gradient", "calibration", "transpose", "coulomb"]
+TRAJ_SETS = ["gradient", "calibration", "transpose", "coulomb",
+             "b200_transpose", "b200_coulomb", "b200_conv"]   # b200_*: B200-measured sweeps
 
 
 def _table(name, model):

@@ -53,7 +53,8 @@ def test_scores_and_weights_match_reference():
         assert np.abs(w.view(np.int64) - s[f"norm_{k}"].view(np.int64)).max() <= 1
 
 
-@pytest.mark.parametrize("name", ["gradient", "calibration", "transpose", "coulomb"])
+@pytest.mark.parametrize("name", ["gradient", "calibration", "transpose", "coulomb",
+                                  "b200_transpose", "b200_coulomb", "b200_conv"])
 def test_trajectories_match_reference(name):
     d = golden(f"ds_{name}.npz")
     traj = golden(f"traj_{name}.npz")
