@@ -15,8 +15,11 @@ scoring kernels) and, per outer iteration:
     cross-GPU argmax" -- later ties win, truncated at the first stop
     configuration -- is then evaluated identically on every rank.
 
-Nothing else crosses the interconnect, so every rank ends with the same
-SearchTrace, and for a replayed source it is the reference's trajectory for
+The model itself is shared once: ``broadcast_table`` sends rank 0's
+prediction table (N x C float64, e.g. 31 MB at N = 205,216) to every rank, so
+only one rank needs the model (north_star: NCCL "for that and for the model
+broadcast").  Nothing else crosses the interconnect, so every rank ends with
+the same SearchTrace, and for a replayed source it is the reference's trajectory for
 any world size.  Collectives use the default group's backend (NCCL over
 NVLink with one rank per GPU; gloo on CPU for the tests).
 """
@@ -54,6 +57,34 @@ def _decode(v: np.ndarray) -> Measurement:
     counters = {a: float(v[2 + j]) for j, a in enumerate(_NAMES) if not np.isnan(v[2 + j])}
     threads = None if v[1] < 0 else int(v[1])
     return Measurement(runtime_us=float(v[0]), global_threads=threads, counters=counters)
+
+
+def broadcast_table(table, space=None, src: int = 0):
+    """Rank src's PredictionTable (or model: it is materialised there first)
+    on every rank, by one broadcast of its N x C float64 matrix.  Other ranks
+    pass None (or anything) plus the space."""
+    import torch
+    import torch.distributed as dist
+    from .search import PredictionTable
+    rank = dist.get_rank()
+    dev = _device(dist)
+    if rank == src:
+        t = _as_table(table, space if space is not None else table.space)
+        names = list(t.counter_names)
+        shape = torch.tensor(list(t.matrix.shape), dtype=torch.int64, device=dev)
+    else:
+        names = None
+        shape = torch.zeros(2, dtype=torch.int64, device=dev)
+    dist.broadcast(shape, src=src)
+    holder = [names]
+    dist.broadcast_object_list(holder, src=src)
+    n, c = (int(x) for x in shape.cpu().tolist())
+    buf = (torch.from_numpy(np.ascontiguousarray(t.matrix, dtype=np.float64)).to(dev)
+           if rank == src else torch.empty((n, c), dtype=torch.float64, device=dev))
+    dist.broadcast(buf, src=src)
+    if rank == src:
+        return t
+    return PredictionTable(space, holder[0], buf.cpu().numpy())
 
 
 def run_profile_search_distributed(source, models, *, i: int, n: int = DEFAULT_INNER_STEPS,

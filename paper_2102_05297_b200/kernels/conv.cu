@@ -3,12 +3,17 @@
 // NVRTC source; tuning parameters arrive as -D<NAME>=<v>.
 //
 //   TBX, TBY    threads per block in x / y
-//   WPTX, WPTY  outputs per thread in x (contiguous) / y (strided by TBY)
+//   WPTX, WPTY  outputs per thread in x (contiguous) / y (strided by TBY;
+//               contiguous with LOCAL = 2)
 //   VW          floats per output store (WPTX % VW == 0)
 //   LOCAL       0: input straight from global memory
 //               1: block's input tile (+ halo) staged in shared memory
-//               2: as 1, plus a per-thread register window of each input
-//                  row (WPTX + FILTER - 1 values reused by FILTER taps)
+//               2: as 1, and each thread owns WPTY contiguous output rows:
+//                  every input row it needs is read from shared memory once
+//                  into a register window (WPTX + FILTER - 1 values) and
+//                  feeds all the thread's output rows it touches (2D
+//                  register blocking: (WPTX+F-1)(WPTY+F-1) loads per
+//                  WPTX*WPTY*F*F FMAs)
 //   PAD         +1 float per shared-memory tile row (LOCAL > 0)
 //   UNROLL_F    fully unroll the filter loops
 //   CACHE_F     filter staged in shared memory (else read through L1)
@@ -103,31 +108,43 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, float* __rest
 #pragma unroll
         for (int i = 0; i < WPTX; ++i) acc[wy][i] = 0.0f;
 
+#if LOCAL == 2
+    {
+        const int ly0 = ty * WPTY;         // first output row inside the tile
+        const int lx = tx * WPTX;          // first output column inside the tile
+        // input row iy feeds output row wy through filter row fy = iy - wy;
+        // per output the taps still go fy ascending, fx ascending
+#pragma unroll
+        for (int iy = 0; iy < WPTY + F - 1; ++iy) {
+            float win[WPTX + F - 1];
+#pragma unroll
+            for (int k = 0; k < WPTX + F - 1; ++k) win[k] = INPUT(ly0 + iy, lx + k);
+#pragma unroll
+            for (int wy = 0; wy < WPTY; ++wy) {
+                const int fy = iy - wy;
+                if (fy >= 0 && fy < F) {
+#if REVERSE
+#pragma unroll
+                    for (int i = 0; i < WPTX; ++i)
+#pragma unroll kUnrollF
+                        for (int fx = 0; fx < F; ++fx) acc[wy][i] += win[i + fx] * FILT(fy, fx);
+#else
+#pragma unroll kUnrollF
+                    for (int fx = 0; fx < F; ++fx) {
+                        const float f = FILT(fy, fx);
+#pragma unroll
+                        for (int i = 0; i < WPTX; ++i) acc[wy][i] += win[i + fx] * f;
+                    }
+#endif
+                }
+            }
+        }
+    }
+#else
 #pragma unroll
     for (int wy = 0; wy < WPTY; ++wy) {
         const int ly = wy * TBY + ty;      // output row inside the tile
         const int lx = tx * WPTX;          // first output column inside the tile
-#if LOCAL == 2
-#pragma unroll kUnrollF
-        for (int fy = 0; fy < F; ++fy) {
-            float win[WPTX + F - 1];
-#pragma unroll
-            for (int k = 0; k < WPTX + F - 1; ++k) win[k] = INPUT(ly + fy, lx + k);
-#if REVERSE
-#pragma unroll
-            for (int i = 0; i < WPTX; ++i)
-#pragma unroll kUnrollF
-                for (int fx = 0; fx < F; ++fx) acc[wy][i] += win[i + fx] * FILT(fy, fx);
-#else
-#pragma unroll kUnrollF
-            for (int fx = 0; fx < F; ++fx) {
-                const float f = FILT(fy, fx);
-#pragma unroll
-                for (int i = 0; i < WPTX; ++i) acc[wy][i] += win[i + fx] * f;
-            }
-#endif
-        }
-#else
 #if REVERSE
 #pragma unroll kUnrollF
         for (int fx = 0; fx < F; ++fx)
@@ -143,11 +160,11 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, float* __rest
 #pragma unroll
                 for (int i = 0; i < WPTX; ++i) acc[wy][i] += INPUT(ly + fy, lx + i + fx) * f;
             }
-#endif
     }
+#endif
 #pragma unroll
     for (int wy = 0; wy < WPTY; ++wy) {
-        const int y = y0 + wy * TBY + ty;
+        const int y = y0 + (LOCAL == 2 ? ty * WPTY + wy : wy * TBY + ty);
         float* row = out + (size_t)y * width + x0 + tx * WPTX;
 #pragma unroll
         for (int i = 0; i < WPTX; i += VW) {

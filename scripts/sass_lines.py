@@ -20,6 +20,8 @@ import subprocess
 import tempfile
 from collections import defaultdict
 
+INNERMOST = False
+
 
 def sass_lines(so, kernel, file_sub):
     tmp = tempfile.mkdtemp()
@@ -41,7 +43,10 @@ def sass_lines(so, kernel, file_sub):
             frames += [(f, int(l)) for f, l in re.findall(r'inlined at "([^"]+)", line (\d+)',
                                                           m.group(3))]
             inside = [l for f, l in frames if file_sub in f]
-            loc = inside[-1] if inside else frames[-1][1]
+            if INNERMOST:
+                loc = inside[0] if inside else frames[-1][1]
+            else:
+                loc = inside[-1] if inside else frames[-1][1]
             continue
         a = re.match(r"\s+/\*([0-9a-f]{4,})\*/", line)
         if a:
@@ -56,7 +61,11 @@ def main():
     ap.add_argument("--rep", required=True)
     ap.add_argument("--file", default="ct_search.cuh")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--innermost", action="store_true",
+                    help="charge each instruction to its innermost line inside --file")
     a = ap.parse_args()
+    global INNERMOST
+    INNERMOST = a.innermost
     lines = sass_lines(a.so, a.kernel, a.file)
     page = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source",
                            "sass"], capture_output=True, text=True, check=True).stdout

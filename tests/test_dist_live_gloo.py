@@ -166,3 +166,33 @@ def test_distributed_live_search_is_the_reference_trajectory(world, tmp_path):
             # ones past a stop configuration inside the last batch
             assert set(drawn) <= set(timed)
             assert len(timed) == len(set(timed)) or not use_stop
+
+
+def _bcast_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2102_05297_b200 import ExactModelSet, spaces
+        from paper_2102_05297_b200.dist_live import broadcast_table
+        ds = spaces.coulomb()
+        model = ExactModelSet(ds) if rank == 0 else None
+        t = broadcast_table(model, ds.space, src=0)
+        np.savez(os.path.join(out_dir, f"t{rank}.npz"), m=t.matrix,
+                 names=np.array(t.counter_names))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_model_broadcast(tmp_path):
+    from paper_2102_05297_b200 import ExactModelSet, spaces
+    mp.spawn(_bcast_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    ds = spaces.coulomb()
+    ms = ExactModelSet(ds)
+    want = ms.prediction_matrix(ds.space)
+    for r in range(3):
+        got = np.load(tmp_path / f"t{r}.npz")
+        np.testing.assert_array_equal(got["m"], want)
+        assert got["names"].tolist() == list(ms.counters)
