@@ -8,10 +8,17 @@
 //   VWM, VWN     vector width of A / B loads (and of C stores along n)
 //   SA, SB       stage the A / B slice in shared memory (else each thread
 //                reads its operands through L1)
-//   TC           tensor-core path (needs SA = SB = 1): mma.sync m16n8k8
-//                TF32 with the 3xTF32 split (big*big + big*small +
-//                small*big), accurate to fp32 level; warps take 16x8 tiles
-//                of the block tile round-robin
+//   TC           tensor-core path (needs SA = SB = 1), TF32 with the 3xTF32
+//                split (big*big + big*small + small*big), accurate to fp32
+//                level:
+//                  MWG = 128 and >= 4 warps: 5th-generation tensor cores --
+//                    one thread issues tcgen05.mma (M = 128, N = NWG, K = 8)
+//                    from K-major canonical shared-memory tiles into a TMEM
+//                    accumulator, completion through tcgen05.commit on an
+//                    mbarrier, epilogue by tcgen05.ld (warp q reads TMEM
+//                    lanes 32q..32q+31 = rows of C);
+//                  otherwise: mma.sync m16n8k8, warps take 16x8 tiles of the
+//                    block tile round-robin
 //
 // Thread (tm, tn) owns MWI = MWG/MDIMC rows and NWI = NWG/NDIMC columns of
 // the block tile, in groups of VWM (VWN) contiguous elements interleaved
@@ -81,6 +88,12 @@ __device__ __forceinline__ void stage(const float* __restrict__ src, int ld, flo
     }
 }
 
+#if TC && MWG == 128 && MDIMC * NDIMC >= 128
+#define TC5 1
+#else
+#define TC5 0
+#endif
+
 #if TC
 __device__ __forceinline__ unsigned tf32(float x) {
     unsigned r;
@@ -98,6 +111,139 @@ constexpr int TILES = (MWG / 16) * (NWG / 8);
 constexpr int MAXT = (TILES + NWARP - 1) / NWARP;
 #endif
 
+#if TC5
+// K-major canonical (no swizzle) layout of a ROWS x KWG fp32 tile: 8x16-byte
+// core matrices; element (r, k) at (r/8)*SBO + (k/4)*128 + (r%8)*16 + (k%4)*4
+// bytes with LBO = 128 (next 4 k) and SBO = KWG*32 (next 8 rows).
+constexpr int SBO = KWG * 32;
+__device__ __forceinline__ int kmaj(int r, int k) {
+    return (r >> 3) * (SBO / 4) + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+}
+// shared-memory matrix descriptor (sm_100 UMMA): start >> 4 | LBO >> 4 << 16 |
+// SBO >> 4 << 32 | version 1 << 46, layout type 0 (SWIZZLE_NONE)
+__device__ __forceinline__ unsigned long long sdesc(const void* p) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    return (unsigned long long)((a >> 4) & 0x3FFF) | ((unsigned long long)(128 >> 4) << 16) |
+           ((unsigned long long)(SBO >> 4) << 32) | (1ull << 46);
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, N = NWG, M = 128
+constexpr unsigned IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(NWG >> 3) << 17) |
+                           ((unsigned)(128 >> 4) << 24);
+constexpr unsigned TMEM_COLS = NWG < 32 ? 32 : NWG;
+
+__device__ __forceinline__ void umma(unsigned tmem_d, unsigned long long da,
+                                     unsigned long long db, unsigned acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(tmem_d), "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+}
+#endif
+
+#if TC5
+// 5th-generation tensor-core path (see the header): per KWG slice the threads
+// stage A and B as tf32 big/small pairs in the K-major canonical layout, one
+// thread issues 3 x KWG/8 tcgen05.mma into the TMEM accumulator and commits
+// them to an mbarrier that every thread waits on before the next slice.
+extern "C" __global__ void __launch_bounds__(NT)
+gemm(const float* __restrict__ at, const float* __restrict__ b, float* __restrict__ c, int M, int N,
+     int K) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int m0 = blockIdx.x * MWG, n0 = blockIdx.y * NWG;
+    extern __shared__ __align__(1024) float dsm[];
+    float* a_big = dsm;
+    float* a_small = a_big + 128 * KWG;
+    float* b_big = a_small + 128 * KWG;
+    float* b_small = b_big + NWG * KWG;
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ unsigned tmem_base;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"((unsigned)__cvta_generic_to_shared(&tmem_base)), "n"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;"
+                     :: "r"((unsigned)__cvta_generic_to_shared(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const unsigned tmem_d = tmem_base;
+    unsigned phase = 0;
+    for (int k0 = 0; k0 < K; k0 += KWG) {
+        // stage: A(m, k) = at[k][m], B(n, k) = b[k][n]; coalesced reads along m / n
+        for (int i = tid; i < KWG * 128; i += NT) {
+            const int k = i / 128, m = i % 128;
+            const float v = at[(size_t)(k0 + k) * M + m0 + m];
+            const float hi = __uint_as_float(tf32(v));
+            a_big[kmaj(m, k)] = hi;
+            a_small[kmaj(m, k)] = __uint_as_float(tf32(v - hi));
+        }
+        for (int i = tid; i < KWG * NWG; i += NT) {
+            const int k = i / NWG, n = i % NWG;
+            const float v = b[(size_t)(k0 + k) * N + n0 + n];
+            const float hi = __uint_as_float(tf32(v));
+            b_big[kmaj(n, k)] = hi;
+            b_small[kmaj(n, k)] = __uint_as_float(tf32(v - hi));
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int kk = 0; kk < KWG / 8; ++kk) {
+                const int off = kk * 64;   // 8 k = two 4-k core-matrix columns = 256 B
+                const unsigned acc0 = (k0 > 0 || kk > 0) ? 1u : 0u;
+                umma(tmem_d, sdesc(a_small + off), sdesc(b_big + off), acc0);
+                umma(tmem_d, sdesc(a_big + off), sdesc(b_small + off), 1u);
+                umma(tmem_d, sdesc(a_big + off), sdesc(b_big + off), 1u);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                         :: "r"((unsigned)__cvta_generic_to_shared(&mbar)));
+        }
+        // the slice's MMAs are complete (smem reusable, accumulator current)
+        {
+            unsigned done = 0;
+            while (!done) {
+                asm volatile("{\n\t.reg .pred p;\n\t"
+                             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                             "selp.u32 %0, 1, 0, p;\n\t}\n"
+                             : "=r"(done) : "r"((unsigned)__cvta_generic_to_shared(&mbar)), "r"(phase));
+            }
+            phase ^= 1;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    // epilogue: warps 0..3 read rows 32q + lane of the accumulator
+    if (warp < 4) {
+        const int row = warp * 32 + lane;
+        float* crow = c + (size_t)(m0 + row) * N + n0;
+#pragma unroll
+        for (int c0 = 0; c0 < NWG; c0 += 8) {
+            unsigned v[8];
+            const unsigned taddr = tmem_d + ((unsigned)(warp * 32) << 16) + (unsigned)c0;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                           "=r"(v[6]), "=r"(v[7])
+                         : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            *reinterpret_cast<float4*>(crow + c0) =
+                make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]),
+                            __uint_as_float(v[3]));
+            *reinterpret_cast<float4*>(crow + c0 + 4) =
+                make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]),
+                            __uint_as_float(v[7]));
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                     :: "r"(tmem_d), "n"(TMEM_COLS));
+}
+#else
 extern "C" __global__ void __launch_bounds__(NT)
 gemm(const float* __restrict__ at, const float* __restrict__ b, float* __restrict__ c, int M, int N,
      int K) {
@@ -220,3 +366,4 @@ gemm(const float* __restrict__ at, const float* __restrict__ b, float* __restric
     }
 #endif
 }
+#endif  // TC5

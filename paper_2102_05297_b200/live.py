@@ -277,10 +277,20 @@ class GemmBenchmark(Benchmark):
         return {"at": tuner.upload(h["at"]), "b": tuner.upload(h["b"]),
                 "c": tuner.alloc(4 * self.m * self.n)}
 
+    @staticmethod
+    def tc5(v) -> bool:
+        """TC=1 variants that run on the 5th-generation tensor cores
+        (tcgen05.mma, M = 128, >= 4 warps); other TC=1 variants use mma.sync."""
+        return v["TC"] == 1 and v["MWG"] == 128 and v["MDIMC"] * v["NDIMC"] >= 128
+
+    def smem_bytes(self, v) -> int:
+        # tf32 big/small tiles of A (128 x KWG) and B (NWG x KWG) for tcgen05
+        return 4 * v["KWG"] * (2 * 128 + 2 * v["NWG"]) if self.tc5(v) else 0
+
     def launch(self, v, bufs):
         return Launch((self.m // v["MWG"], self.n // v["NWG"]), (v["MDIMC"] * v["NDIMC"],),
                       [_u64(bufs["at"]), _u64(bufs["b"]), _u64(bufs["c"]), _i32(self.m),
-                       _i32(self.n), _i32(self.k)])
+                       _i32(self.n), _i32(self.k)], dynamic_smem=self.smem_bytes(v))
 
     def output(self, tuner, bufs):
         return tuner.d2h(bufs["c"], np.empty((self.m, self.n), np.float32))

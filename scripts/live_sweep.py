@@ -63,6 +63,11 @@ def main():
     ap.add_argument("--limit", type=int, default=0, help="sweep only the first K configs")
     ap.add_argument("--budget-s", type=float, default=None,
                     help="stop measuring after this many seconds (partial dataset)")
+    ap.add_argument("--update", default=None,
+                    help="existing dataset dir: re-measure only --select configs, keep the rest")
+    ap.add_argument("--select", default=None,
+                    help="'tc5' (gemm tcgen05 variants), 'PARAM=value', or a comma list of "
+                         "config indices")
     args = ap.parse_args()
 
     from paper_2102_05297_b200 import formats, live
@@ -80,6 +85,38 @@ def main():
             last[0] = time.time()
             print(f"[sweep] {bench.name}: {i + 1}/{n} after {time.time() - t0:.0f} s", flush=True)
 
+    if args.update:
+        # re-measure a subset (variants whose kernel code changed) and merge
+        ds = formats.load_dataset_dir(args.update)
+        if args.select == "tc5":
+            idx = [i for i in range(len(bench.space)) if bench.tc5(bench.values(i))]
+        elif "=" in args.select:
+            key, val = args.select.split("=")
+            idx = [i for i in range(len(bench.space)) if bench.values(i)[key] == int(val)]
+        else:
+            idx = [int(x) for x in args.select.split(",")]
+        src.compile_all(idx)
+        names = list(ds.counter_names)
+        for i in idx:
+            m = src.measure(i, profiled=True)
+            ds.runtime_us[i] = m.runtime_us
+            ds.global_threads[i] = m.global_threads
+            ds.counter_matrix[i] = [m.counters[a] for a in names]
+            ds.has_record[i] = True
+        ds._records = None
+        formats.save_dataset(ds, args.out)
+        rt = np.where(ds.has_record, ds.runtime_us, np.inf)
+        best = int(np.argmin(rt))
+        pk = peaks(src.tuner.sm_count)
+        ach, peak, unit, frac = roofline(bench, float(rt[best]), pk)
+        sub = np.array(idx)
+        bsub = int(sub[np.argmin(rt[sub])])
+        print(json.dumps({"bench": bench.name, "updated": len(idx), "best_index": best,
+                          "best_values": bench.values(best), "best_us": float(rt[best]),
+                          "best_updated_index": bsub, "best_updated_us": float(rt[bsub]),
+                          "best_updated_values": bench.values(bsub),
+                          "roofline": {"achieved": ach, "peak": peak, "unit": unit, "frac": frac}}))
+        return
     if args.limit:
         # restricted sweep (smoke): measure the first K only
         idx = list(range(min(args.limit, len(bench.space))))

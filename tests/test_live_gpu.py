@@ -77,9 +77,12 @@ def test_benchmark_matches_oracle(tuner, name, sizes, rtol):
     else:
         want, mag = bo.gemm(h["at"], h["b"])
     idxs = _sample(len(b.space), 2)
-    if name == "gemm":   # make sure the tensor-core path is in the sample
-        tc = [i for i in range(len(b.space)) if b.values(i)["TC"] == 1]
-        idxs = sorted(set(idxs) | set(tc[:: max(1, len(tc) // 4)][:4]))
+    if name == "gemm":   # both tensor-core paths (mma.sync, tcgen05) in the sample
+        tc = [i for i in range(len(b.space)) if b.values(i)["TC"] == 1 and not b.tc5(b.values(i))]
+        tc5 = [i for i in range(len(b.space)) if b.tc5(b.values(i))]
+        assert tc5, "no tcgen05 variant in the space"
+        idxs = sorted(set(idxs) | set(tc[:: max(1, len(tc) // 4)][:4])
+                      | set(tc5[:: max(1, len(tc5) // 8)][:8]))
     worst = _check(src, idxs, lambda i: bo.within(src.output(i), want, mag, 1.0))
     assert worst <= rtol, f"{name}: worst relative error {worst:.3g} > {rtol}"
 
