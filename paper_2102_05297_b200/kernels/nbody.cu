@@ -2,13 +2,18 @@
 //   a_i = sum_j m_j (p_j - p_i) / (|p_j - p_i|^2 + eps^2)^(3/2)
 // NVRTC source; tuning parameters arrive as -D<NAME>=<v>.
 //
-//   BLOCK       threads per block
-//   OUTER       bodies per thread (strided by the launch's thread count)
+//   BLOCK       bodies per block (threads along x)
+//   OUTER       bodies per thread (strided by the launch's x extent)
 //   UNROLL      unroll factor of the j loop
 //   USE_SMEM    stage BLOCK bodies at a time in shared memory
 //   VEC         j bodies per load step (SoA: float2/float4 vector loads)
 //   FAST_RSQRT  rsqrtf (MUFU) instead of 1/sqrtf (IEEE sqrt + division)
 //   SOA         positions/masses as four float arrays instead of float4
+//
+// JS (set by the host, not a tuning parameter): the j range is split over
+// blockDim.y = JS thread rows, so that n = 16,384 bodies still fill the 148
+// SMs (one thread per body would be 512 warps); the JS partial sums of a body
+// are reduced in shared memory in a fixed order (deterministic).
 //
 // 20 flops per interaction (the customary count); FP32/MUFU-bound.
 #ifndef BLOCK
@@ -32,6 +37,9 @@
 #ifndef SOA
 #define SOA 0
 #endif
+#ifndef JS
+#define JS 1
+#endif
 
 constexpr int kUnroll = UNROLL;
 
@@ -46,23 +54,27 @@ struct Body {
     float px, py, pz, ax, ay, az;
     __device__ __forceinline__ void interact(float qx, float qy, float qz, float m, float eps2) {
         const float dx = qx - px, dy = qy - py, dz = qz - pz;
-        const float r2 = dx * dx + dy * dy + dz * dz + eps2;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
 #if FAST_RSQRT
         const float inv = rsqrtf(r2);
 #else
         const float inv = 1.0f / sqrtf(r2);
 #endif
-        const float s = m * (inv * inv * inv);
-        ax += dx * s; ay += dy * s; az += dz * s;
+        const float s = (m * inv) * (inv * inv);
+        ax = fmaf(dx, s, ax); ay = fmaf(dy, s, ay); az = fmaf(dz, s, az);
     }
 };
 
-extern "C" __global__ void __launch_bounds__(BLOCK)
+extern "C" __global__ void __launch_bounds__(BLOCK * JS)
 nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* __restrict__ y,
       const float* __restrict__ z, const float* __restrict__ m, int n, float eps2,
       float4* __restrict__ acc) {
     const int nthreads = gridDim.x * BLOCK;
-    const int t = blockIdx.x * BLOCK + threadIdx.x;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int t = blockIdx.x * BLOCK + tx;
+    // this thread row's share of the j range (a multiple of BLOCK when JS > 1)
+    const int span = ((n + JS - 1) / JS + BLOCK - 1) / BLOCK * BLOCK;
+    const int j0 = min(n, ty * span), j1 = min(n, j0 + span);
     Body b[OUTER];
 #pragma unroll
     for (int o = 0; o < OUTER; ++o) {
@@ -77,27 +89,28 @@ nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* _
     }
 #if USE_SMEM
 #if SOA
-    __shared__ __align__(16) float sx[BLOCK], sy[BLOCK], sz[BLOCK], sm[BLOCK];
+    __shared__ __align__(16) float sx[JS][BLOCK], sy[JS][BLOCK], sz[JS][BLOCK], sm[JS][BLOCK];
 #else
-    __shared__ float4 sp[BLOCK];
+    __shared__ float4 sp[JS][BLOCK];
 #endif
-    for (int base = 0; base < n; base += BLOCK) {
+    // every thread row walks the same number of tiles (barriers stay uniform)
+    for (int base = 0; base < span; base += BLOCK) {
         __syncthreads();
-        const int j = base + threadIdx.x;
+        const int j = j0 + base + tx;
 #if SOA
-        if (j < n) { sx[threadIdx.x] = x[j]; sy[threadIdx.x] = y[j]; sz[threadIdx.x] = z[j]; sm[threadIdx.x] = m[j]; }
+        if (j < j1) { sx[ty][tx] = x[j]; sy[ty][tx] = y[j]; sz[ty][tx] = z[j]; sm[ty][tx] = m[j]; }
 #else
-        if (j < n) sp[threadIdx.x] = pm[j];
+        if (j < j1) sp[ty][tx] = pm[j];
 #endif
         __syncthreads();
-        const int cnt = min(BLOCK, n - base);
+        const int cnt = max(0, min(BLOCK, j1 - j0 - base));
 #pragma unroll kUnroll
         for (int jj = 0; jj < cnt; jj += VEC) {
 #if SOA
-            const vec vx = *reinterpret_cast<const vec*>(sx + jj);
-            const vec vy = *reinterpret_cast<const vec*>(sy + jj);
-            const vec vz = *reinterpret_cast<const vec*>(sz + jj);
-            const vec vm = *reinterpret_cast<const vec*>(sm + jj);
+            const vec vx = *reinterpret_cast<const vec*>(&sx[ty][jj]);
+            const vec vy = *reinterpret_cast<const vec*>(&sy[ty][jj]);
+            const vec vz = *reinterpret_cast<const vec*>(&sz[ty][jj]);
+            const vec vm = *reinterpret_cast<const vec*>(&sm[ty][jj]);
 #pragma unroll
             for (int k = 0; k < VEC; ++k)
 #pragma unroll
@@ -105,7 +118,7 @@ nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* _
 #else
 #pragma unroll
             for (int k = 0; k < VEC; ++k) {
-                const float4 q = sp[jj + k];
+                const float4 q = sp[ty][jj + k];
 #pragma unroll
                 for (int o = 0; o < OUTER; ++o) b[o].interact(q.x, q.y, q.z, q.w, eps2);
             }
@@ -114,7 +127,7 @@ nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* _
     }
 #else
 #pragma unroll kUnroll
-    for (int j = 0; j < n; j += VEC) {
+    for (int j = j0; j < j1; j += VEC) {
 #if SOA
         const vec vx = __ldg(reinterpret_cast<const vec*>(x + j));
         const vec vy = __ldg(reinterpret_cast<const vec*>(y + j));
@@ -133,6 +146,23 @@ nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* _
         }
 #endif
     }
+#endif
+#if JS > 1
+    // partial sums of the JS thread rows, reduced in row order
+    __shared__ float3 part[JS][BLOCK];
+#pragma unroll
+    for (int o = 0; o < OUTER; ++o) {
+        __syncthreads();
+        part[ty][tx] = make_float3(b[o].ax, b[o].ay, b[o].az);
+        __syncthreads();
+        if (ty == 0) {
+            float3 s = part[0][tx];
+#pragma unroll
+            for (int r = 1; r < JS; ++r) { s.x += part[r][tx].x; s.y += part[r][tx].y; s.z += part[r][tx].z; }
+            b[o].ax = s.x; b[o].ay = s.y; b[o].az = s.z;
+        }
+    }
+    if (ty != 0) return;
 #endif
 #pragma unroll
     for (int o = 0; o < OUTER; ++o) {

@@ -204,9 +204,20 @@ class NBodyBenchmark(Benchmark):
         out["acc"] = tuner.alloc(16 * self.bodies)
         return out
 
+    SM_THREADS = 148 * 1024      # aim: at least half of the B200's thread slots busy
+
+    def js(self, v) -> int:
+        """Thread rows the j range is split over (compile-time JS of the
+        kernel): enough threads to fill the GPU, at most 1024 per block."""
+        want = -(-self.SM_THREADS * v["OUTER"] // self.bodies)
+        return max(1, min(1024 // v["BLOCK"], want))
+
+    def options(self, values):
+        return super().options(values) + [f"-DJS={self.js(values)}"]
+
     def launch(self, v, bufs):
         per_block = v["BLOCK"] * v["OUTER"]
-        return Launch((-(-self.bodies // per_block),), (v["BLOCK"],),
+        return Launch((-(-self.bodies // per_block),), (v["BLOCK"], self.js(v)),
                       [_u64(bufs["pm"]), _u64(bufs["x"]), _u64(bufs["y"]), _u64(bufs["z"]),
                        _u64(bufs["m"]), _i32(self.bodies), _f32(self.eps2), _u64(bufs["acc"])])
 

@@ -10,6 +10,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pr
 timeout 1200 python scripts/live_experiment.py datasets/coulomb-b200 datasets/transpose-b200 --live 3 --out gpurun_out/${TAG}_experiments_live.json > gpurun_out/${TAG}_experiments_live.log 2>&1; echo "exp rc=$?" >> gpurun_out/${TAG}_experiments_live.log
 for f in gpurun_out/${TAG}_*.log; do echo "== $f"; tail -n 3 "$f" | cut -c1-600; done
 # partial re-sweeps of variants whose kernel code changed (gemm tcgen05 path, conv LOCAL=2)
-timeout 1500 python scripts/live_sweep.py --bench gemm --update datasets/gemm-b200 --select tc5 --out gpurun_out/datasets/gemm-b200 > gpurun_out/${TAG}_gemm_tc5.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_gemm_tc5.log
 timeout 1500 python scripts/live_sweep.py --bench conv --update datasets/conv-b200 --select LOCAL=2 --out gpurun_out/datasets/conv-b200 > gpurun_out/${TAG}_conv_l2.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_conv_l2.log
-tail -n 2 gpurun_out/${TAG}_gemm_tc5.log gpurun_out/${TAG}_conv_l2.log | cut -c1-800
+tail -n 2 gpurun_out/${TAG}_conv_l2.log | cut -c1-800
