@@ -492,9 +492,9 @@ int ensure_results(ct_ctx* ctx, int64_t reps, int64_t max_steps) {
     return CT_OK;
 }
 
-template <int NT, bool SMEM>
+template <int NT, bool SMEM, bool PRE>
 int launch_profile_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
-    auto kern = k_profile_search<NT, SMEM>;
+    auto kern = k_profile_search<NT, SMEM, PRE>;
     if (smem > 48 * 1024)
         CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -536,10 +536,17 @@ int launch_profile_ws(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int
                    : launch_profile_ws_t<PW, false>(ctx, a, smem, n_reps);
 }
 
+// PRE: in-row prefixes computed by all warps in the weight pass (default), or
+// the drawn row scanned by the drawing warp (CT_SEARCH_PRE=0)
 template <int NT>
 int launch_profile(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int n_reps) {
-    return in_smem ? launch_profile_t<NT, true>(ctx, a, smem, n_reps)
-                   : launch_profile_t<NT, false>(ctx, a, smem, n_reps);
+    bool pre = true;
+    if (const char* env = std::getenv("CT_SEARCH_PRE")) pre = std::atoi(env) != 0;
+    if (pre)
+        return in_smem ? launch_profile_t<NT, true, true>(ctx, a, smem, n_reps)
+                       : launch_profile_t<NT, false, true>(ctx, a, smem, n_reps);
+    return in_smem ? launch_profile_t<NT, true, false>(ctx, a, smem, n_reps)
+                   : launch_profile_t<NT, false, false>(ctx, a, smem, n_reps);
 }
 
 }  // namespace

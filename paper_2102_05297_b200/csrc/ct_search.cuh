@@ -111,7 +111,6 @@ struct __align__(16) Ctl {
     double red_max[NW];
     double red_min[NW];
     double red_amin[NW];
-    int red_pos[NW];
     int red_bad[NW];
     ActiveTerm act[MAX_ACTIVE];
     double cnt[N_REQ];
@@ -200,34 +199,53 @@ __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& c
     }
 }
 
-// Eq. 17 weights over the raw scores, each configuration's inclusive in-row
-// prefix and each row's total (float64): warp pw of the nw-warp group takes
-// rows pw, pw+nw, ...; lane l owns configuration 32 t + l (padding lanes
-// write weight 0).  The draws locate r with these sums and certify the choice
-// against their rounding error (draw_step).
+// Eq. 17 weights over the raw scores (the form of weight_rcp in ct_hd.cuh,
+// search.py:156-170), each row's total and -- with PRE -- each
+// configuration's inclusive in-row prefix (float64): warp pw of the nw-warp
+// group takes rows pw, pw+nw, ...; lane l owns configuration 32 t + l
+// (padding and explored lanes write weight 0).  s_min == 0 makes every
+// non-positive pool score 0 and its ratio 0, which dividing 0 by 1 gives
+// too, so the per-element den == 0 test is folded into (smin_e, y_min).
+// Every pool weight of finite scores is in [1e-4, 256]; bad flags NaN / Inf
+// (the reference then draws from non-finite weights).
 template <bool CERT>
+__device__ __forceinline__ double weight_of(double s, double smax, double smin_e, double y_max,
+                                            double y_min, double gamma) {
+    const bool pos = s > 0.0;
+    const double den = pos ? smax : smin_e;
+    double r;
+    double ratio = markstein(s, den, pos ? y_max : y_min, &r);
+    if (!CERT) {
+        if (__builtin_expect(!dvd_accept(s, den, r, ratio), 0)) ratio = dvd_term(s, den);
+    }
+    const double w = pow8(pos ? add(1.0, ratio) : sub(1.0, ratio));
+    if (pos) return (w > SCORE_CEILING) ? SCORE_CEILING : w;            // np.minimum
+    if (s > gamma) return (w < SCORE_FLOOR) ? SCORE_FLOOR : w;          // np.maximum
+    return (s <= gamma) ? SCORE_FLOOR : 0.0;                            // NaN: no branch
+}
+
+template <bool CERT, bool PRE>
 __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw, double smax,
                                             double smin, const uint32_t* expl, double* w,
-                                            double* pre, double* row_tot, int& pos, int& bad) {
+                                            double* pre, double* row_tot, int& bad) {
     const int lane = threadIdx.x & 31;
     const int64_t N = a.n;
     const double gamma = a.gamma;
-    const double y_max = rcp_nv(smax), y_min = rcp_nv(smin);
+    const double smin_e = (smin != 0.0) ? smin : 1.0;
+    const double y_max = rcp_nv(smax), y_min = rcp_nv(smin_e);
     for (int t = pw; t < a.nrows; t += nw) {
         const int64_t e = 32LL * t + lane;
         double wt = 0.0;
-        if (e < N && !bit_get(expl, e)) wt = weight_rcp<CERT>(w[e], smax, smin, y_max, y_min, gamma);
+        if (e < N && !bit_get(expl, e)) wt = weight_of<CERT>(w[e], smax, smin_e, y_max, y_min, gamma);
         w[e] = wt;
-        // every Eq. 17 weight of finite scores is 0 or in [1e-4, 256]
-        if (!(wt == 0.0 || (wt >= SCORE_FLOOR && wt <= SCORE_CEILING))) bad = 1;
-        pos += (wt > 0.0);
+        bad |= !(wt <= SCORE_CEILING);
         double incl = wt;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const double v = __shfl_up_sync(FULL, incl, d);
             if (lane >= d) incl = add(incl, v);
         }
-        pre[e] = incl;
+        if (PRE) pre[e] = incl;
         if (lane == 31) row_tot[t] = incl;
     }
 }
@@ -350,9 +368,9 @@ __device__ __forceinline__ void score_phase(const SearchArgs& a, Ctl<NW>& ctl, c
     if (lane == 0) { ctl.red_max[pw] = lmax; ctl.red_min[pw] = lmin; ctl.red_amin[pw] = lamin; }
 }
 
-// Eq. 17 weights + in-row prefixes for warp pw of the NW-warp group (after
-// every warp's score_phase is visible), reduced into ctl.red_pos/bad[pw].
-template <int NW>
+// Eq. 17 weights (+ in-row prefixes) for warp pw of the NW-warp group (after
+// every warp's score_phase is visible), reduced into ctl.red_bad[pw].
+template <bool PRE, int NW>
 __device__ __forceinline__ void weight_phase(const SearchArgs& a, Ctl<NW>& ctl, const uint32_t* expl,
                                              double* w, double* pre, double* row_tot, int pw) {
     const int lane = threadIdx.x & 31;
@@ -366,12 +384,11 @@ __device__ __forceinline__ void weight_phase(const SearchArgs& a, Ctl<NW>& ctl, 
     // (NaN extrema fail the comparisons)
     const double lo = 3.872591914849318e-121, hi = 2.5822498780869086e+120;
     const bool cert = (amin >= lo || amin == INFINITY) && smax <= hi && smin >= -hi;
-    int pos = 0, bad = 0;
-    if (cert) weight_pass<true>(a, pw, NW, smax, smin, expl, w, pre, row_tot, pos, bad);
-    else weight_pass<false>(a, pw, NW, smax, smin, expl, w, pre, row_tot, pos, bad);
-    pos = warp_sum_i(pos);
+    int bad = 0;
+    if (cert) weight_pass<true, PRE>(a, pw, NW, smax, smin, expl, w, pre, row_tot, bad);
+    else weight_pass<false, PRE>(a, pw, NW, smax, smin, expl, w, pre, row_tot, bad);
     bad = __any_sync(FULL, bad);
-    if (lane == 0) { ctl.red_pos[pw] = pos; ctl.red_bad[pw] = bad; }
+    if (lane == 0) ctl.red_bad[pw] = bad;
 }
 
 // n certified draws, replay lookups, stop test and the later-ties-win argmin
@@ -388,15 +405,16 @@ __device__ __forceinline__ void weight_phase(const SearchArgs& a, Ctl<NW>& ctl, 
 // difference adds 2 2^-53 T; r and the zeroing updates a few 2^-53 T more),
 // so P(i-1) + B < r and r + B < P(i) imply that the reference picks i too.
 // Otherwise the draw is re-decided with the sequential float64 cumsum.
-template <int NW>
+template <bool PRE, int NW>
 __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl<NW>& ctl,
                                           uint32_t* expl, double* w, double* pre, double* row_tot,
                                           const u128* jA, const u128* jC, int32_t* out_idx,
                                           uint8_t* out_prof, int lane) {
     const int64_t N = a.n;
-    int positive = 0, bad = 0;
+    // every pool configuration has a weight in [1e-4, 256] unless bad
+    int positive = (int)(N - rs.n_expl), bad = 0;
 #pragma unroll
-    for (int i = 0; i < NW; ++i) { positive += ctl.red_pos[i]; bad |= ctl.red_bad[i]; }
+    for (int i = 0; i < NW; ++i) bad |= ctl.red_bad[i];
     const int cpl = (a.nrows + 31) >> 5;
     const int t0 = lane * cpl, t1 = min(t0 + cpl, a.nrows);
     double mine = 0.0;
@@ -450,7 +468,18 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
                 row = __shfl_sync(FULL, row, L);
                 carry = __shfl_sync(FULL, carry, L);
                 if (row >= 0) {
-                    const double v = add(carry, pre[32LL * row + lane]);
+                    double incl;
+                    if (PRE) {
+                        incl = pre[32LL * row + lane];
+                    } else {   // in-row prefix of the row holding r, scanned now
+                        incl = w[32LL * row + lane];
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const double t = __shfl_up_sync(FULL, incl, d);
+                            if (lane >= d) incl = add(incl, t);
+                        }
+                    }
+                    const double v = add(carry, incl);
                     l2 = __ffs(__ballot_sync(FULL, v > r)) - 1;
                     if (l2 >= 0) {
                         const double p_hi = __shfl_sync(FULL, v, l2);
@@ -474,7 +503,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
             const double wc = w[chosen];
             __syncwarp();
             // inclusive prefixes: the drawn configuration's own and the later ones
-            if (lane >= l2) pre[32LL * row + lane] = sub(pre[32LL * row + lane], wc);
+            if (PRE && lane >= l2) pre[32LL * row + lane] = sub(pre[32LL * row + lane], wc);
             if (lane == 0) { w[chosen] = 0.0; row_tot[row] = sub(row_tot[row], wc); }
             if (row >= t0 && row < t1) mine = sub(mine, wc);
             if (row < t1) lane_pref = sub(lane_pref, wc);
@@ -528,7 +557,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
 // k_profile_search: one CTA runs one repetition end to end (then the next one
 // of its persistent slice); the serial phases run on warp 0 while the other
 // warps wait at the CTA barrier.
-template <int NT, bool SMEM>
+template <int NT, bool SMEM, bool PRE>
 __global__ void __launch_bounds__(NT, (NT <= 64) ? 8 : ((NT == 128) ? 7 : (896 / NT)))
 k_profile_search(const SearchArgs a) {
     constexpr int NW = NT / 32;
@@ -578,10 +607,10 @@ k_profile_search(const SearchArgs a) {
             score_phase<NT>(a, ctl, expl, w, tid);
             __syncthreads();
             CT_CLK(clk_score);
-            weight_phase(a, ctl, expl, w, pre, row_tot, warp);
+            weight_phase<PRE>(a, ctl, expl, w, pre, row_tot, warp);
             __syncthreads();
             CT_CLK(clk_weight);
-            if (warp == 0) draw_step(a, rs, ctl, expl, w, pre, row_tot, jA, jC, out_idx, out_prof, lane);
+            if (warp == 0) draw_step<PRE>(a, rs, ctl, expl, w, pre, row_tot, jA, jC, out_idx, out_prof, lane);
             __syncthreads();
             CT_CLK(clk_p4);
             if (ctl.done) break;
@@ -692,7 +721,7 @@ k_profile_search_ws(const SearchArgs a) {
             if (ctl[cur].cmd == WS_RUN) {
                 int32_t* out_idx = a.step_index + (size_t)rep[cur] * a.max_steps;
                 uint8_t* out_prof = a.step_profiled + (size_t)rep[cur] * a.max_steps;
-                draw_step(a, rs[cur], ctl[cur], expl[cur], w[cur], pre[cur], row_tot[cur], jA, jC,
+                draw_step<true>(a, rs[cur], ctl[cur], expl[cur], w[cur], pre[cur], row_tot[cur], jA, jC,
                           out_idx, out_prof, lane);
                 ++it[cur];
                 if (ctl[cur].done || it[cur] >= a.outer) {
@@ -733,7 +762,7 @@ k_profile_search_ws(const SearchArgs a) {
             if (cmd == WS_RUN) {
                 score_phase<PT>(a, ctl[cur], expl[cur], w[cur], ptid);
                 bar_sync_n(5, PT);
-                weight_phase(a, ctl[cur], expl[cur], w[cur], pre[cur], row_tot[cur], pw);
+                weight_phase<true>(a, ctl[cur], expl[cur], w[cur], pre[cur], row_tot[cur], pw);
             }
 #ifdef CT_PHASE_CLOCKS
             t_ = clock64(); clk_work += t_ - clk_t; clk_t = t_;

@@ -217,7 +217,9 @@ int launch_once(ct_tuner* t, Variant* var, const ct_launch* l) {
     std::vector<void*> params((size_t)std::max(l->n_args, 0));
     for (int i = 0; i < l->n_args; ++i)
         params[i] = const_cast<char*>(static_cast<const char*>(l->args) + l->arg_offsets[i]);
-    if (l->dynamic_smem > var->smem_attr && l->dynamic_smem > 48 * 1024) {
+    // the opt-in limit counts dynamic + static shared memory: raise it for any
+    // dynamic request (48 KB of dynamic memory on top of static fails otherwise)
+    if (l->dynamic_smem > var->smem_attr) {
         TU_CU(D.cuFuncSetAttribute(var->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                                  (int)l->dynamic_smem));
         var->smem_attr = l->dynamic_smem;
