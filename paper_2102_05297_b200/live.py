@@ -49,6 +49,17 @@ _i32 = ctypes.c_int32
 _f32 = ctypes.c_float
 
 
+def clamp_counter(abbr: str, value: float) -> float:
+    """A canonical reading inside the catalog's value range (the reference's
+    dataset format rejects anything else, space.py:286-350): CUPTI's
+    pct_of_peak ratios can read a few percent above 100 (e.g. SM_E 101.03
+    on a kernel shorter than the sampling window), counts are >= 0."""
+    from .formats import VALUE_RANGES
+    lo, hi = VALUE_RANGES.get(abbr, (0.0, None))
+    v = max(lo, value)
+    return min(hi, v) if hi is not None else v
+
+
 def b200_arch(sm_count: int = spaces.B200_SMS) -> ArchProfile:
     """ArchProfile of the device: Volta+ counter dialect, 128 FP32 cores/SM
     (the b_paral saturation rule of bottlenecks.py:172-173 counts cores)."""
@@ -402,7 +413,7 @@ class CudaMeasurementSource:
         counter_map: Dict[str, float] = {}
         for name, value in zip(self.metrics, vals):
             abbr, canonical = cc.canonicalize(name, float(value), self.arch)
-            counter_map[abbr] = canonical
+            counter_map[abbr] = clamp_counter(abbr, canonical)
         return Measurement(runtime_us=runtime, global_threads=launch.threads,
                            counters=counter_map)
 
