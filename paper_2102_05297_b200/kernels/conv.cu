@@ -20,7 +20,7 @@
 //   REVERSE     filter traversal order (fx outer instead of fy outer)
 //
 // The tile lives in dynamic shared memory: the host passes
-// smem_bytes() = 4 * ((TH + F - 1) * (TW + F - 1 + PAD) + CACHE_F * F * F).
+// smem_bytes() = 4 * ((TH + F - 1) * (TW + 8 + PAD) + CACHE_F * F * F).
 #ifndef TBX
 #define TBX 32
 #endif
@@ -58,7 +58,9 @@
 constexpr int F = FILTER, R = FILTER / 2;
 constexpr int TW = TBX * WPTX, TH = TBY * WPTY;
 constexpr int LW = TW + F - 1, LH = TH + F - 1;   // tile incl. halo
-constexpr int SW = LW + PAD;                      // shared row stride
+constexpr int V4 = (TW + 8) / 4;                  // float4 per staged row: x0-4 .. x0+TW+3
+constexpr int SW = 4 * V4 + PAD;                  // shared row stride
+static_assert(F <= 9, "the staged row holds a halo of at most 4 columns per side");
 constexpr int NT = TBX * TBY;
 constexpr int kUnrollF = UNROLL_F ? F : 1;
 
@@ -88,14 +90,21 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, float* __rest
 #define FILT(fy, fx) __ldg(filt + (fy) * F + (fx))
 #endif
 #if LOCAL
+    // the tile starts at column x0 - 4 (16-byte aligned: x0 is a multiple of
+    // TW >= 8, the image width a multiple of 4), so it is read with float4
+    // loads that are either wholly inside the image or wholly outside; the
+    // R = FILTER/2 halo columns the filter needs begin at tile column 4 - R
     float* tile = dsm;
-    for (int i = tid; i < LH * LW; i += NT) {
-        const int ry = i / LW, rx = i - ry * LW;
-        const int gx = x0 + rx - R, gy = y0 + ry - R;
-        tile[ry * SW + rx] = (gx >= 0 && gx < width && gy >= 0 && gy < height)
-                                 ? __ldg(in + (size_t)gy * width + gx) : 0.0f;
+    for (int i = tid; i < LH * V4; i += NT) {
+        const int ry = i / V4, c4 = i - ry * V4;
+        const int gx = x0 - 4 + 4 * c4, gy = y0 + ry - R;
+        float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (gx >= 0 && gx < width && gy >= 0 && gy < height)
+            v = __ldg(reinterpret_cast<const float4*>(in + (size_t)gy * width + gx));
+        float* d = tile + ry * SW + 4 * c4;
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
     }
-#define INPUT(ly, lx) tile[(ly) * SW + (lx)]
+#define INPUT(ly, lx) tile[(ly) * SW + (lx) + (4 - R)]
 #else
 #define INPUT(ly, lx) load_global(in, width, height, x0 - R + (lx), y0 - R + (ly))
 #endif

@@ -10,10 +10,13 @@
 //   FAST_RSQRT  rsqrtf (MUFU) instead of 1/sqrtf (IEEE sqrt + division)
 //   SOA         positions/masses as four float arrays instead of float4
 //
-// JS (set by the host, not a tuning parameter): the j range is split over
-// blockDim.y = JS thread rows, so that n = 16,384 bodies still fill the 148
-// SMs (one thread per body would be 512 warps); the JS partial sums of a body
-// are reduced in shared memory in a fixed order (deterministic).
+// JS and gridDim.y = JB (set by the host, not tuning parameters): the j range
+// is split over JB blocks and, inside a block, over blockDim.y = JS thread
+// rows, so that n = 16,384 bodies still fill the 148 SMs (one thread per body
+// would be 512 warps).  A body's JS partial sums are reduced in shared
+// memory, its JB block partials by the last block to finish (fixed order,
+// deterministic; the arrival counters reset themselves, so a launch is
+// idempotent under timing and profiler replay).
 //
 // 20 flops per interaction (the customary count); FP32/MUFU-bound.
 #ifndef BLOCK
@@ -68,13 +71,15 @@ struct Body {
 extern "C" __global__ void __launch_bounds__(BLOCK * JS)
 nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* __restrict__ y,
       const float* __restrict__ z, const float* __restrict__ m, int n, float eps2,
-      float4* __restrict__ acc) {
+      float4* __restrict__ acc, float4* __restrict__ partial, unsigned* __restrict__ arrivals) {
     const int nthreads = gridDim.x * BLOCK;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int t = blockIdx.x * BLOCK + tx;
-    // this thread row's share of the j range (a multiple of BLOCK when JS > 1)
-    const int span = ((n + JS - 1) / JS + BLOCK - 1) / BLOCK * BLOCK;
-    const int j0 = min(n, ty * span), j1 = min(n, j0 + span);
+    const int JB = gridDim.y;
+    // this thread row's share of the j range (a multiple of BLOCK)
+    const int splits = JB * JS;
+    const int span = ((n + splits - 1) / splits + BLOCK - 1) / BLOCK * BLOCK;
+    const int j0 = min(n, (blockIdx.y * JS + ty) * span), j1 = min(n, j0 + span);
     Body b[OUTER];
 #pragma unroll
     for (int o = 0; o < OUTER; ++o) {
@@ -162,11 +167,46 @@ nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* _
             b[o].ax = s.x; b[o].ay = s.y; b[o].az = s.z;
         }
     }
-    if (ty != 0) return;
 #endif
+    // thread row 0 holds the block's sums (the other rows stay for the barriers)
+    if (JB == 1) {
+        if (ty == 0) {
 #pragma unroll
-    for (int o = 0; o < OUTER; ++o) {
-        const int i = t + o * nthreads;
-        if (i < n) acc[i] = make_float4(b[o].ax, b[o].ay, b[o].az, 0.0f);
+            for (int o = 0; o < OUTER; ++o) {
+                const int i = t + o * nthreads;
+                if (i < n) acc[i] = make_float4(b[o].ax, b[o].ay, b[o].az, 0.0f);
+            }
+        }
+        return;
     }
+    // block partials; the last of the JB blocks of this body group sums them
+    if (ty == 0) {
+#pragma unroll
+        for (int o = 0; o < OUTER; ++o) {
+            const int i = t + o * nthreads;
+            if (i < n) partial[(size_t)blockIdx.y * n + i] = make_float4(b[o].ax, b[o].ay, b[o].az, 0.0f);
+        }
+    }
+    __threadfence();
+    __shared__ int last;
+    __syncthreads();
+    if (tx == 0 && ty == 0) last = (atomicAdd(&arrivals[blockIdx.x], 1u) == (unsigned)JB - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (ty == 0) {
+#pragma unroll
+        for (int o = 0; o < OUTER; ++o) {
+            const int i = t + o * nthreads;
+            if (i < n) {
+                float4 sum = __ldcg(partial + i);
+                for (int r = 1; r < JB; ++r) {
+                    const float4 q = __ldcg(partial + (size_t)r * n + i);
+                    sum.x += q.x; sum.y += q.y; sum.z += q.z;
+                }
+                acc[i] = make_float4(sum.x, sum.y, sum.z, 0.0f);
+            }
+        }
+    }
+    if (tx == 0 && ty == 0) arrivals[blockIdx.x] = 0u;
 }

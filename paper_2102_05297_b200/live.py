@@ -213,14 +213,26 @@ class NBodyBenchmark(Benchmark):
         for k, name in enumerate(("x", "y", "z", "m")):
             out[name] = tuner.upload(soa[k])
         out["acc"] = tuner.alloc(16 * self.bodies)
+        out["partial"] = tuner.alloc(16 * self.bodies * self.MAX_JB)
+        groups = -(-self.bodies // 32)
+        out["arrivals"] = tuner.alloc(4 * groups)
+        tuner.memset(out["arrivals"], 0, 4 * groups)
         return out
 
     SM_THREADS = 148 * 1024      # aim: at least half of the B200's thread slots busy
+    MIN_BLOCKS = 2 * 148         # and at least two blocks per SM
+    MAX_JB = 16
+
+    def jb(self, v) -> int:
+        """Blocks the j range is split over (gridDim.y): enough blocks for
+        every SM when the bodies alone make fewer."""
+        gx = -(-self.bodies // (v["BLOCK"] * v["OUTER"]))
+        return max(1, min(self.MAX_JB, -(-self.MIN_BLOCKS // gx)))
 
     def js(self, v) -> int:
-        """Thread rows the j range is split over (compile-time JS of the
-        kernel): enough threads to fill the GPU, at most 1024 per block."""
-        want = -(-self.SM_THREADS * v["OUTER"] // self.bodies)
+        """Thread rows the j range is split over inside a block (compile-time
+        JS of the kernel): enough threads to fill the GPU, <= 1024 per block."""
+        want = -(-self.SM_THREADS * v["OUTER"] // (self.bodies * self.jb(v)))
         return max(1, min(1024 // v["BLOCK"], want))
 
     def options(self, values):
@@ -228,9 +240,10 @@ class NBodyBenchmark(Benchmark):
 
     def launch(self, v, bufs):
         per_block = v["BLOCK"] * v["OUTER"]
-        return Launch((-(-self.bodies // per_block),), (v["BLOCK"], self.js(v)),
+        return Launch((-(-self.bodies // per_block), self.jb(v)), (v["BLOCK"], self.js(v)),
                       [_u64(bufs["pm"]), _u64(bufs["x"]), _u64(bufs["y"]), _u64(bufs["z"]),
-                       _u64(bufs["m"]), _i32(self.bodies), _f32(self.eps2), _u64(bufs["acc"])])
+                       _u64(bufs["m"]), _i32(self.bodies), _f32(self.eps2), _u64(bufs["acc"]),
+                       _u64(bufs["partial"]), _u64(bufs["arrivals"])])
 
     def output(self, tuner, bufs):
         return tuner.d2h(bufs["acc"], np.empty((self.bodies, 4), np.float32))[:, :3]
@@ -264,7 +277,7 @@ class ConvBenchmark(Benchmark):
     def smem_bytes(self, v) -> int:
         f = self.filt
         tw, th = v["TBX"] * v["WPTX"], v["TBY"] * v["WPTY"]
-        tile = (th + f - 1) * (tw + f - 1 + v["PAD"]) if v["LOCAL"] else 0
+        tile = (th + f - 1) * (tw + 8 + v["PAD"]) if v["LOCAL"] else 0
         return 4 * (tile + (f * f if v["CACHE_F"] else 0))
 
     def launch(self, v, bufs):

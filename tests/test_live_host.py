@@ -52,7 +52,7 @@ def test_launch_geometry_covers_problem(name):
     from paper_2102_05297_b200 import live
     b = live.benchmark(name)
     bufs = {k: 0 for k in ("in", "out", "atoms", "x", "y", "z", "w", "energy", "pm", "m",
-                           "acc", "filt", "at", "b", "c")}
+                           "acc", "filt", "at", "b", "c", "partial", "arrivals")}
     for i in range(len(b.space)):
         v = b.values(i)
         l = b.launch(v, bufs)
@@ -65,6 +65,7 @@ def test_launch_geometry_covers_problem(name):
             assert l.grid[2] * v["Z_ITERATIONS"] >= b.grid
         elif name == "nbody":
             assert l.grid[0] * v["BLOCK"] * v["OUTER"] >= b.bodies
+            assert 1 <= l.grid[1] <= b.MAX_JB and l.grid[0] * l.grid[1] >= min(b.MIN_BLOCKS, l.grid[0] * b.MAX_JB)
         elif name == "conv":
             assert l.grid[0] * v["TBX"] * v["WPTX"] == b.width
             assert l.grid[1] * v["TBY"] * v["WPTY"] == b.height
