@@ -106,6 +106,17 @@ struct __align__(16) RepState {
     unsigned long long scored, draws, uncert, outers, abytes;
 };
 
+#ifdef CT_PHASE_CLOCKS
+// sub-phase clocks of draw_step (lane 0 of the drawing warp): setup, locate,
+// certify+zero, lookups, bookkeeping
+__device__ unsigned long long g_subclk[8];
+#define CT_SUB(k) do { if (lane == 0) { long long n_ = clock64(); atomicAdd(&g_subclk[k], (unsigned long long)(n_ - sub_t)); sub_t = n_; } } while (0)
+#define CT_SUB_START() long long sub_t = clock64()
+#else
+#define CT_SUB(k) do { } while (0)
+#define CT_SUB_START() do { } while (0)
+#endif
+
 template <int NW>
 struct __align__(16) Ctl {
     double red_max[NW];
@@ -411,6 +422,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
                                           const u128* jA, const u128* jC, int32_t* out_idx,
                                           uint8_t* out_prof, int lane) {
     const int64_t N = a.n;
+    CT_SUB_START();
     // every pool configuration has a weight in [1e-4, 256] unless bad
     int positive = (int)(N - rs.n_expl), bad = 0;
 #pragma unroll
@@ -430,6 +442,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
     int done = 0;
     if (bad) { if (lane == 0) { rs.st = CT_STATUS_ERROR; rs.err = -7; } done = 1; }
     double t_best = INFINITY;
+    CT_SUB(0);
     // The iteration's uniforms come 32 at a time from the repetition's PCG64
     // by jump-ahead (lane j: the (j+1)-th next Generator.random()), the draws
     // of a chunk touch shared memory only, and their replay lookups are issued
@@ -448,6 +461,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
         int64_t my_choice = -1;
         for (; k < k0 + cnt; ++k) {
             if (positive <= 0) { exhausted = true; break; }
+            CT_SUB(1);
             const double u = __shfl_sync(FULL, u_lane, k - k0);
             const double r = mul(u, total);
             int64_t chosen = -1;
@@ -490,6 +504,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
                     }
                 }
             }
+            CT_SUB(2);
             if (!ok) {
                 if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
                 chosen = __shfl_sync(FULL, (long long)chosen, 0);
@@ -510,6 +525,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
             total = __shfl_sync(FULL, lane_pref, 31);
             --positive;
             __syncwarp();
+            CT_SUB(3);
         }
         const int made = k - k0;
         g.advance(jA[made], jC[made]);
@@ -519,6 +535,8 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
         const bool rec_ok = mine_in && a.has_record[cs];
         const double rt = a.runtime[cs];
         const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cs);
+        __syncwarp();
+        CT_SUB(4);
         // the reference's bookkeeping, draw by draw
         for (int j = 0; j < made; ++j) {
             const int64_t cj = __shfl_sync(FULL, (long long)my_choice, j);
@@ -547,6 +565,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
             if (lane == 0) rs.st = CT_STATUS_EXHAUSTED;
             done = 1;
         }
+        CT_SUB(5);
     }
     if (lane == 0) rs.rng.state = g.state;
     if (lane == 0) ctl.done = done;
@@ -622,6 +641,10 @@ k_profile_search(const SearchArgs a) {
     if (tid == 0 && (blockIdx.x % 37) == 0)
         printf("[clk] cta %d: profile+expert %lld score %lld weights %lld draws %lld cycles\n",
                blockIdx.x, clk_p1, clk_score, clk_weight, clk_p4);
+    if (tid == 0 && blockIdx.x == 0)
+        printf("[clk-draw] all CTAs so far: setup %llu jump-ahead %llu locate %llu zero %llu "
+               "lookup %llu bookkeeping %llu\n", g_subclk[0], g_subclk[1], g_subclk[2],
+               g_subclk[3], g_subclk[4], g_subclk[5]);
 #endif
 }
 
