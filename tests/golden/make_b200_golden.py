@@ -23,7 +23,12 @@ from countertune import space as rspace  # noqa: E402
 
 
 def main():
-    for name, tree, reps in (("transpose", True, 32), ("coulomb", True, 32), ("conv", False, 16)):
+    import sys as _sys
+    which = set(_sys.argv[1:])
+    for name, tree, reps in (("transpose", True, 32), ("coulomb", True, 32), ("conv", False, 16),
+                             ("gemm", False, 16), ("nbody", False, 16)):
+        if which and name not in which:
+            continue
         d = os.path.join(ROOT, "datasets", f"{name}-b200")
         if not os.path.isdir(d):
             print("missing", d)
