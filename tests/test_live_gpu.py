@@ -116,15 +116,21 @@ def test_ask_tell_matches_batched_device_search():
     src = DatasetReplaySource(ds)
     model = ExactModelSet(ds)
     stop = set(well_performing_set(ds, 1.1))
-    for seed in range(4):
-        want = run_profile_search(src, model, i=8, seed=seed, stop_indices=stop)
-        s = ProfileSearcher(model, ds.space, ds.arch, i=8, seed=seed, stop_indices=stop)
+    total = 0
+    for seed in range(6):
+        st = stop if seed % 2 else None      # budget runs and stop-set runs
+        want = run_profile_search(src, model, i=8, seed=seed, stop_indices=st)
+        s = ProfileSearcher(model, ds.space, ds.arch, i=8, seed=seed, stop_indices=st)
         while (req := s.next_config()) is not None:
             s.add_result(src.measure(*req))
         got = s.trace
         assert [x.config_index for x in got.steps] == [x.config_index for x in want.steps]
         assert [x.profiled for x in got.steps] == [x.profiled for x in want.steps]
         assert got.status == want.status
+        total += len(got.steps)
+    assert total >= 3 * 8 * 6                # the budget runs went the full 8 iterations
+    with pytest.raises(Exception):
+        s.add_result(src.measure(0, False))  # nothing pending after the end
 
 
 def test_live_profile_search_runs(tuner):
