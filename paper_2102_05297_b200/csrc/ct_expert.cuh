@@ -81,43 +81,75 @@ CT_HD double analyze_component(const double* c, int k, int generation, int64_t c
 }
 
 #if defined(__CUDACC__)
-// Warp form (lane k evaluates component k, all 32 lanes call it converged):
-// the same operations as analyze_component, but the b_issue lane takes the
-// seven per-class ratios dvd(c[INST_F32 + j], fitted) from lanes 8..14,
-// which compute exactly those values for their own components, instead of
-// redoing seven dependent divisions.  Bit-identical to analyze_component.
+// Warp form (lane k evaluates component k, all 32 lanes call it converged).
+// analyze_component branches by component kind, so a warp would run the
+// kinds' divisions one after another.  Here every lane runs the same three
+// division stages on its own operands (lanes without a division in a stage
+// divide 1 by 1); the operands are chosen with selects, so each lane performs
+// exactly analyze_component's operations in its order -- bit-identical:
+//   stage 1  memory: share = part / total (0 if total <= 0); tex: TEX_U / 10;
+//            local: LOC_O / 100; instruction classes + issue: 100 / WARP_E,
+//            100 / WARP_NP_E, ISSUE_U / 100 (pre-Volta) or / 50; SM:
+//            (100 - SM_E) / 100; paral: (sat - threads) / sat
+//   stage 2  memory: (share * util) / 10; local: (. * busiest) / 10;
+//            classes: c / fitted
+//   stage 3  issue: (util_max * (100 - ISSUE_U)) / 100 over the seven class
+//            ratios taken from lanes 8..14 by shuffle
 __device__ __forceinline__ double analyze_component_warp(const double* c, int k, int generation,
                                                          int64_t cores, int64_t global_threads,
                                                          bool degenerate) {
-    const bool inst = (k >= B_FP32) && (k <= B_ISSUE) && !degenerate;
-    double ratio = 0.0;
-    if (inst) {
-        const double fitted = mul(mul(mul(32.0, c[INST_EXE]), dvd(100.0, c[WARP_E])),
-                                  dvd(100.0, c[WARP_NP_E]));
-        ratio = dvd(c[INST_F32 + ((k < B_ISSUE) ? (k - B_FP32) : 0)], fitted);
-    }
+    const bool mem = k < B_TEX, tex = k == B_TEX, loc = k == B_LOCAL;
+    const bool cls = (k >= B_FP32) && (k < B_ISSUE), iss = k == B_ISSUE;
+    const bool inst = cls || iss;
+    const bool smk = k == B_SM, par = k == B_PARAL;
+    const int rd = (k < 2) ? DRAM_RT : (k < 4 ? L2_RT : SHR_LT);
+    const int util_i = (k < 2) ? DRAM_U : (k < 4 ? L2_U : SHR_U);
+    const double tot = mem ? add(c[rd], c[rd + 1]) : 1.0;
+    const double sat = (double)(cores * 5);
+    // ---- stage 1
+    double n1 = 1.0, d1 = 1.0;
+    if (mem) { n1 = c[rd + (k & 1)]; d1 = tot; }
+    if (tex) { n1 = c[TEX_U]; d1 = 10.0; }
+    if (loc) { n1 = c[LOC_O]; d1 = 100.0; }
+    if (inst) { n1 = 100.0; d1 = c[WARP_E]; }
+    if (smk) { n1 = sub(100.0, c[SM_E_]); d1 = 100.0; }
+    if (par) { n1 = sub(sat, (double)global_threads); d1 = sat; }
+    const double n2 = inst ? 100.0 : 1.0, d2 = inst ? c[WARP_NP_E] : 1.0;
+    const double n3 = inst ? c[INST_ISSUE_U] : 1.0;
+    const double d3 = inst ? (generation == 0 ? 100.0 : 50.0) : 1.0;
+    const double q1 = dvd(n1, d1), q2 = dvd(n2, d2), q3 = dvd(n3, d3);
+    // ---- stage 2
+    const double share = (mem && !(tot > 0.0)) ? 0.0 : q1;       // _traffic_share
+    const double busiest = pymax(pymax(c[DRAM_U], c[L2_U]), c[TEX_U]);
+    const double fitted = mul(mul(mul(32.0, c[INST_EXE]), q1), q2);
+    double n4 = 1.0, d4 = 1.0;
+    if (mem) { n4 = mul(share, c[util_i]); d4 = 10.0; }
+    if (loc) { n4 = mul(q1, busiest); d4 = 10.0; }
+    if (inst) { n4 = c[INST_F32 + (cls ? k - B_FP32 : 0)]; d4 = fitted; }
+    const double q4 = dvd(n4, d4);
+    // ---- stage 3 (b_issue): the class ratios of lanes 8..14
+    const double ratio = (cls && !degenerate) ? q4 : 0.0;
     double r[7];
 #pragma unroll
     for (int j = 0; j < 7; ++j) r[j] = __shfl_sync(0xffffffffu, ratio, B_FP32 + j);
-    if (k == B_ISSUE) {
-        if (degenerate) return 0.0;
-        double util_max = r[0];
+    double util_max = r[0];
 #pragma unroll
-        for (int j = 1; j < 7; ++j) util_max = pymax(util_max, r[j]);
-        return clamp01(dvd(mul(util_max, sub(100.0, c[INST_ISSUE_U])), 100.0));
-    }
-    if (k >= B_FP32 && k < B_ISSUE) {
+    for (int j = 1; j < 7; ++j) util_max = pymax(util_max, r[j]);
+    const double q5 = dvd(iss ? mul(util_max, sub(100.0, c[INST_ISSUE_U])) : 1.0, iss ? 100.0 : 1.0);
+    // ---- per-kind result
+    double v;
+    if (mem || loc) v = q4;
+    else if (tex || smk) v = q1;
+    else if (par) v = q1 > 0.0 ? q1 : 0.0;                        // max(0.0, par)
+    else if (cls) {
         if (degenerate) return 0.0;
-        double util;
-        if (generation == 0) {
-            util = dvd(c[INST_ISSUE_U], 100.0);
-        } else {
-            const double u = dvd(c[INST_ISSUE_U], 50.0);
-            util = (u < 1.0) ? u : 1.0;
-        }
-        return clamp01(mul(ratio, util));
+        const double util = (generation == 0) ? q3 : (q3 < 1.0 ? q3 : 1.0);
+        v = mul(q4, util);
+    } else {                                                      // b_issue
+        if (degenerate) return 0.0;
+        v = q5;
     }
-    return analyze_component(c, k, generation, cores, global_threads, degenerate);
+    return clamp01(v);
 }
 #endif
 
