@@ -14,7 +14,7 @@ from conftest import dataset_from_golden, golden, ragged
 pytestmark = pytest.mark.gpu
 
 TRAJ_SETS = ["gradient", "calibration", "transpose", "coulomb",
-             "b200_transpose", "b200_coulomb", "b200_conv", "b200_gemm"]   # b200_*: B200 sweeps
+             "b200_transpose", "b200_coulomb", "b200_conv", "b200_gemm", "b200_nbody"]   # B200 sweeps
 
 
 def _table(name, model):

@@ -54,7 +54,8 @@ def test_scores_and_weights_match_reference():
 
 
 @pytest.mark.parametrize("name", ["gradient", "calibration", "transpose", "coulomb",
-                                  "b200_transpose", "b200_coulomb", "b200_conv", "b200_gemm"])
+                                  "b200_transpose", "b200_coulomb", "b200_conv", "b200_gemm",
+                                  "b200_nbody"])
 def test_trajectories_match_reference(name):
     d = golden(f"ds_{name}.npz")
     traj = golden(f"traj_{name}.npz")
