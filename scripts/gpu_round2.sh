@@ -1,5 +1,5 @@
 # full GPU session after the sweeps: tests, smoke, bench, ncu, experiments
-TAG=${1:-r01d}
+TAG=${1:-r01f}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q --timeout 400 > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.log
@@ -7,8 +7,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TA
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/${TAG}_bench.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --kernel-only > gpurun_out/${TAG}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_profile_search -c 1 -o gpurun_out/${TAG}_search_full python bench.py --steps 1 --warmup 3 --kernel-only > gpurun_out/${TAG}_ncu_full.log 2>&1
-timeout 1200 python scripts/live_experiment.py datasets/coulomb-b200 datasets/transpose-b200 --live 3 --out gpurun_out/${TAG}_experiments_live.json > gpurun_out/${TAG}_experiments_live.log 2>&1; echo "exp rc=$?" >> gpurun_out/${TAG}_experiments_live.log
 for f in gpurun_out/${TAG}_*.log; do echo "== $f"; tail -n 3 "$f" | cut -c1-600; done
-# partial re-sweeps of variants whose kernel code changed (gemm tcgen05 path, conv LOCAL=2)
-timeout 1500 python scripts/live_sweep.py --bench conv --update datasets/conv-b200 --select LOCAL=2 --out gpurun_out/datasets/conv-b200 > gpurun_out/${TAG}_conv_l2.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_conv_l2.log
-tail -n 2 gpurun_out/${TAG}_conv_l2.log | cut -c1-800
