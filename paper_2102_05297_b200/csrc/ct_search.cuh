@@ -210,8 +210,8 @@ __device__ __forceinline__ void score_pass(const SearchArgs& a, const Ctl<NW>& c
     }
 }
 
-// Eq. 17 weights over the raw scores (the form of weight_rcp in ct_hd.cuh,
-// search.py:156-170), each row's total and -- with PRE -- each
+// Eq. 17 weights over the raw scores (weight() in ct_hd.cuh with the pool's
+// reciprocals hoisted, search.py:156-170), each row's total and -- with PRE -- each
 // configuration's inclusive in-row prefix (float64): warp pw of the nw-warp
 // group takes rows pw, pw+nw, ...; lane l owns configuration 32 t + l
 // (padding and explored lanes write weight 0).  s_min == 0 makes every
@@ -259,14 +259,6 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
         if (PRE) pre[e] = incl;
         if (lane == 31) row_tot[t] = incl;
     }
-}
-
-// v * 2^-66 for the draw's r = u * T: within 1 ulp of T (one hardware
-// rounding of hi 2^64 + double(lo)); the certificate charges the error.
-__device__ __forceinline__ double fx_total_to_double(u128 v) {
-    const double hi = (double)(unsigned long long)(v >> 64);
-    const double lo = (double)(unsigned long long)v;
-    return __fma_rn(hi, 18446744073709551616.0, lo) * 1.3552527156068805e-20;   // 2^64, 2^-66
 }
 
 // ---------------------------------------------------------------------------

@@ -389,6 +389,11 @@ class CudaMeasurementSource:
                 bad += 1
         return bad
 
+    def reset_variants(self) -> None:
+        """Forget the compiled variants (the next measure() compiles again,
+        as a fresh tuning session would)."""
+        self._variants.clear()
+
     def variant(self, config_index: int) -> int:
         v = self._variants.get(config_index)
         if v is None:

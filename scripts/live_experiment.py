@@ -60,7 +60,7 @@ def live(name, ds, k, seed):
     seeds = np.random.SeedSequence(seed).spawn(2 * k)
     for r in range(k):
         # profile searcher, measurements live (compile on first use)
-        src._variants.clear()
+        src.reset_variants()
         t0 = time.perf_counter()
         s = ProfileSearcher(model, ds.space, ds.arch, i=max(1, -(-(len(ds.space) - 1) // 5)),
                             seed=seeds[r], stop_indices=stop)
@@ -71,7 +71,7 @@ def live(name, ds, k, seed):
         res["profile_wall_s"].append(time.perf_counter() - t0)
         res["profile_steps"].append(steps)
         # random search, same measurement path
-        src._variants.clear()
+        src.reset_variants()
         t0 = time.perf_counter()
         order = np.random.default_rng(seeds[k + r]).permutation(len(ds.space))
         steps = 0
@@ -107,14 +107,14 @@ def main():
     ap.add_argument("--overhead", type=float, default=3.0)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    from paper_2102_05297_b200 import formats
+    from paper_2102_05297_b200 import formats, well_performing_set
     results = {}
     for d in a.dirs:
         ds = formats.load_dataset_dir(d)
         name = os.path.basename(os.path.normpath(d)).replace("-b200", "")
         r = {"configs": len(ds.space), "measured": int(ds.has_record.sum()),
              "best_us": float(ds.best_runtime),
-             "well_performing": int(len(__import__("paper_2102_05297_b200").well_performing_set(ds, 1.1)))}
+             "well_performing": len(well_performing_set(ds, 1.1))}
         overhead = a.overhead
         if a.live:
             r["live"] = live(name, ds, a.live, a.seed)
