@@ -163,8 +163,8 @@ def simulate_distributed(spec: ExperimentSpec, device: int = 0,
     step_std = np.sqrt(var)
 
     tr = reps if spec.time_repetitions is None else min(reps, spec.time_repetitions)
-    t_start = max(float(t) for t in first_times[:tr])
-    t_end = max(float(t) for t in total_times[:tr])
+    t_start = float(np.max(first_times[:tr]))     # exact in any order
+    t_end = float(np.max(total_times[:tr]))
     if t_end > t_start:
         grid = np.linspace(t_start, t_end, TIME_GRID_POINTS)
     else:
