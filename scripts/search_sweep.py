@@ -14,7 +14,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--nt", default="32,64,128,256")
+    ap.add_argument("--nt", default="32,64,128,256,512")
     ap.add_argument("--spaces", default="coulomb,transpose,nbody,conv,gemm")
     ap.add_argument("--reps", type=int, default=1000)
     ap.add_argument("--outer", type=int, default=40)
@@ -27,8 +27,14 @@ def main():
     torch.cuda.set_stream(stream)
     ctx = _native.context(0)
     ctx.set_stream(stream.cuda_stream)
+    from paper_2102_05297_b200 import formats
+    hbm = 6548.5
     for name in a.spaces.split(","):
-        ds = spaces.SPACES[name]()
+        # "<name>" = synthetic stand-in, "b200:<name>" = datasets/<name>-b200
+        if name.startswith("b200:"):
+            ds = formats.load_dataset_dir(os.path.join(ROOT, "datasets", name[5:] + "-b200"))
+        else:
+            ds = spaces.SPACES[name]()
         spec = harness.ExperimentSpec(dataset=ds, searcher="profile", model=ExactModelSet(ds),
                                       repetitions=a.reps, outer_iterations=a.outer, seed=42,
                                       stop_at_well_performing=False)
@@ -52,8 +58,11 @@ def main():
             else:
                 same = bool((ref[1] == nst).all() and (ref[0] == idx).all())
             ms = sorted(times)[len(times) // 2]
+            gbs = stats.algorithmic_bytes / (ms / 1e3) / 1e9
             print(json.dumps({"space": name, "n": len(ds.space), "nt": int(nt), "ms": ms,
                               "configs_per_s": stats.configs_scored / (ms / 1e3),
+                              "algorithmic_GBps": gbs, "hbm_frac": gbs / hbm,
+                              "uncertified": int(stats.uncertified),
                               "same_as_first": same}), flush=True)
     os.environ.pop("CT_SEARCH_NT", None)
 
