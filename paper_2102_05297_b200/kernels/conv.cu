@@ -16,7 +16,9 @@
 //                  WPTX*WPTY*F*F FMAs)
 //   PAD         +1 float per shared-memory tile row (LOCAL > 0)
 //   UNROLL_F    fully unroll the filter loops
-//   CACHE_F     filter staged in shared memory (else read through L1)
+//   CACHE_F     1: filter staged in shared memory; 0: filter passed by value
+//               in the kernel parameters (the constant bank: FFMA takes it
+//               as an operand, no load instruction at all)
 //   REVERSE     filter traversal order (fx outer instead of fy outer)
 //
 // The tile lives in dynamic shared memory: the host passes
@@ -76,8 +78,11 @@ __device__ __forceinline__ float load_global(const float* __restrict__ in, int w
                                                              : 0.0f;
 }
 
+struct Filter { float f[FILTER * FILTER]; };
+
 extern "C" __global__ void __launch_bounds__(NT)
-conv(const float* __restrict__ in, const float* __restrict__ filt, float* __restrict__ out,
+conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter kf,
+     float* __restrict__ out,
      int width, int height) {
     extern __shared__ __align__(16) float dsm[];
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TBX + tx;
@@ -87,7 +92,7 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, float* __rest
     for (int i = tid; i < F * F; i += NT) sf[i] = filt[i];
 #define FILT(fy, fx) sf[(fy) * F + (fx)]
 #else
-#define FILT(fy, fx) __ldg(filt + (fy) * F + (fx))
+#define FILT(fy, fx) kf.f[(fy) * F + (fx)]
 #endif
 #if LOCAL
     // the tile starts at column x0 - 4 (16-byte aligned: x0 is a multiple of

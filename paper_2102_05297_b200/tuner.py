@@ -133,7 +133,8 @@ class Launch:
         offsets, off = [], 0
         for a in args:
             sz = ctypes.sizeof(a)
-            off = (off + sz - 1) // sz * sz
+            al = ctypes.alignment(a)          # arrays / structs: element alignment
+            off = (off + al - 1) // al * al
             offsets.append(off)
             off += sz
         self._blob = ctypes.create_string_buffer(max(off, 8))
