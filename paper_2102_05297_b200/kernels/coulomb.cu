@@ -62,7 +62,11 @@ struct Point {
         const float dxy2 = dx * dx + dy * dy;
 #pragma unroll
         for (int j = 0; j < Z; ++j) {
-            e[j] += aw * rsqrtf(dxy2 + dz * dz);
+            // MUFU.RSQ alone (atoms sit between grid planes: r^2 is never
+            // denormal, so rsqrtf's denormal scaling is not needed)
+            float rd;
+            asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(dxy2 + dz * dz));
+            e[j] += aw * rd;
             dz += spacing;
         }
     }

@@ -7,7 +7,8 @@
 //   UNROLL      unroll factor of the j loop
 //   USE_SMEM    stage BLOCK bodies at a time in shared memory
 //   VEC         j bodies per load step (SoA: float2/float4 vector loads)
-//   FAST_RSQRT  rsqrtf (MUFU) instead of 1/sqrtf (IEEE sqrt + division)
+//   FAST_RSQRT  MUFU rsqrt (rsqrt.approx.ftz) instead of 1/sqrtf (IEEE sqrt +
+//               division)
 //   SOA         positions/masses as four float arrays instead of float4
 //
 // JS and gridDim.y = JB (set by the host, not tuning parameters): the j range
@@ -59,7 +60,10 @@ struct Body {
         const float dx = qx - px, dy = qy - py, dz = qz - pz;
         const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, eps2)));
 #if FAST_RSQRT
-        const float inv = rsqrtf(r2);
+        // MUFU.RSQ alone: r2 >= eps2 > 0 is never denormal, so rsqrtf's
+        // denormal scaling (a compare and two multiplies) is dropped
+        float inv;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(r2));
 #else
         const float inv = 1.0f / sqrtf(r2);
 #endif
