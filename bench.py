@@ -203,10 +203,17 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     world, rank, local = dist_env()
+    # CT_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 over gloo, to
+    # exercise the multi-rank path on a one-GPU box; timings are meaningless
+    shared = os.environ.get("CT_BENCH_SHARED_GPU") == "1"
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = local if world > 1 else 0
+        if shared:
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = 0 if (world == 1 or shared) else local
     torch.cuda.set_device(device)
 
     from paper_2102_05297_b200 import _native, harness
