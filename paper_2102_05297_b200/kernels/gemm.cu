@@ -173,15 +173,19 @@ gemm(const float* __restrict__ at, const float* __restrict__ b, float* __restric
     unsigned phase = 0;
     for (int k0 = 0; k0 < K; k0 += KWG) {
         // stage: A(m, k) = at[k][m], B(n, k) = b[k][n]; coalesced reads along m / n
-        for (int i = tid; i < KWG * 128; i += NT) {
-            const int k = i / 128, m = i % 128;
+        // a warp stages 8 rows x 4 k per step: lane l takes row 8q + l%8 and
+        // k 4p + l/8, so the loads are four full 32-byte sectors and the 32
+        // shared stores hit 32 different banks (bank = (r%8)*4 + k%4)
+        const int lr = lane & 7, lk = lane >> 3;
+        for (int blk = warp; blk < 16 * (KWG / 4); blk += NT / 32) {
+            const int m = (blk & 15) * 8 + lr, k = (blk >> 4) * 4 + lk;
             const float v = at[(size_t)(k0 + k) * M + m0 + m];
             const float hi = __uint_as_float(tf32(v));
             a_big[kmaj(m, k)] = hi;
             a_small[kmaj(m, k)] = __uint_as_float(tf32(v - hi));
         }
-        for (int i = tid; i < KWG * NWG; i += NT) {
-            const int k = i / NWG, n = i % NWG;
+        for (int blk = warp; blk < (NWG / 8) * (KWG / 4); blk += NT / 32) {
+            const int n = (blk % (NWG / 8)) * 8 + lr, k = (blk / (NWG / 8)) * 4 + lk;
             const float v = b[(size_t)(k0 + k) * N + n0 + n];
             const float hi = __uint_as_float(tf32(v));
             b_big[kmaj(n, k)] = hi;

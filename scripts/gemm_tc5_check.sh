@@ -8,6 +8,6 @@ if grep -q "rc=0" gpurun_out/tc5_pytest.log; then
       --out gpurun_out/datasets/gemm-b200 > gpurun_out/datasets/gemm_tc5.log 2>&1
   tail -n 1 gpurun_out/datasets/gemm_tc5.log | cut -c1-900
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^gemm\$" -s 1 -c 1 \
-      -o gpurun_out/kb_gemm2 python scripts/run_variant.py --bench gemm --best gpurun_out/datasets/gemm-b200 > gpurun_out/kb_gemm2.log 2>&1
-  tail -n 1 gpurun_out/kb_gemm2.log
+      -o gpurun_out/kb_gemm3 python scripts/run_variant.py --bench gemm --best gpurun_out/datasets/gemm-b200 > gpurun_out/kb_gemm3.log 2>&1
+  tail -n 1 gpurun_out/kb_gemm3.log
 fi
