@@ -56,6 +56,39 @@ struct DevBuf {
 
 }  // namespace
 
+// Page-locked host staging for an upload: the caller's (pageable) arrays are
+// copied into it on the host, the H2D copy then runs asynchronously on the
+// context's stream and the next upload through the same stage first waits
+// for the previous copy's event.  No stream synchronisation per upload.
+struct PinnedStage {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t done = nullptr;
+    cudaError_t acquire(size_t want) {
+        if (!done) {
+            cudaError_t e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = cudaEventSynchronize(done);      // previous copy finished
+        if (e != cudaSuccess) return e;
+        if (want > bytes) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            bytes = 0;
+            e = cudaHostAlloc(&p, want, cudaHostAllocDefault);
+            if (e != cudaSuccess) return e;
+            bytes = want;
+        }
+        return cudaSuccess;
+    }
+    void release() {
+        if (done) { cudaEventSynchronize(done); cudaEventDestroy(done); done = nullptr; }
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
 struct ct_ctx {
     int device = 0;
     int sm_count = 0;
@@ -97,6 +130,7 @@ struct ct_ctx {
     DevBuf<int32_t> val_a, val_b;
     DevBuf<unsigned char> cub_tmp;
     DevBuf<double> part_d;
+    PinnedStage stage_table, stage_replay;
     DevBuf<int32_t> part_i;
     DevBuf<u128> tiles;
     DevBuf<long long> pick;
@@ -597,6 +631,7 @@ int ct_destroy(ct_ctx* ctx) {
     ctx->part_d.release(); ctx->part_i.release(); ctx->tiles.release(); ctx->pick.release();
     ctx->agg_bsf.release(); ctx->agg_times.release(); ctx->agg_vec.release();
     ctx->agg_sampled.release(); ctx->model_blob.release(); ctx->model_out.release();
+    ctx->stage_table.release(); ctx->stage_replay.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     return CT_OK;
@@ -624,14 +659,18 @@ int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
     // search kernel's unrolled loads (4 x up to 512 threads) never need a
     // bounds test
     const int64_t ld = (n + 2047) / 2048 * 2048;
-    std::vector<double> colmajor((size_t)ld * c, 0.0);
-    for (int64_t i = 0; i < n; ++i)
-        for (int32_t j = 0; j < c; ++j) colmajor[(size_t)j * ld + i] = matrix[(size_t)i * c + j];
+    CT_CUDA(ctx->stage_table.acquire(sizeof(double) * (size_t)ld * c));
+    double* colmajor = static_cast<double*>(ctx->stage_table.p);
+    for (int32_t j = 0; j < c; ++j) {
+        double* col = colmajor + (size_t)j * ld;
+        for (int64_t i = 0; i < n; ++i) col[i] = matrix[(size_t)i * c + j];
+        for (int64_t i = n; i < ld; ++i) col[i] = 0.0;
+    }
     const uint64_t cert = certified_columns(matrix, n, c);
     CT_CUDA(ctx->table.ensure((size_t)ld * c));
-    CT_CUDA(cudaMemcpyAsync(ctx->table.p, colmajor.data(), sizeof(double) * ld * c,
+    CT_CUDA(cudaMemcpyAsync(ctx->table.p, colmajor, sizeof(double) * ld * c,
                             cudaMemcpyHostToDevice, ctx->stream));
-    CT_CUDA(cudaStreamSynchronize(ctx->stream));
+    CT_CUDA(cudaEventRecord(ctx->stage_table.done, ctx->stream));
     ctx->n = n;
     ctx->ld = ld;
     ctx->n_counters = c;
@@ -729,22 +768,32 @@ int ct_replay_upload(ct_ctx* ctx, int64_t n, const double* runtime, const int64_
     CT_CUDA(ctx->counters.ensure((size_t)n * CT_N_REQUIRED));
     CT_CUDA(ctx->has_record.ensure(n));
     cudaStream_t s = ctx->stream;
-    CT_CUDA(cudaMemcpyAsync(ctx->runtime.p, runtime, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-    CT_CUDA(cudaMemcpyAsync(ctx->threads.p, threads, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
-    CT_CUDA(cudaMemcpyAsync(ctx->counters.p, counters, sizeof(double) * n * CT_N_REQUIRED,
+    // one pinned stage: runtime | threads | counters | has_record | stop bits
+    const size_t words = (size_t)((n + 31) / 32);
+    const size_t b_rt = sizeof(double) * n, b_th = sizeof(int64_t) * n;
+    const size_t b_cn = sizeof(double) * n * CT_N_REQUIRED;
+    const size_t b_hr = ((size_t)n + 7) & ~(size_t)7;
+    CT_CUDA(ctx->stage_replay.acquire(b_rt + b_th + b_cn + b_hr + 4 * words));
+    unsigned char* st = static_cast<unsigned char*>(ctx->stage_replay.p);
+    std::memcpy(st, runtime, b_rt);
+    std::memcpy(st + b_rt, threads, b_th);
+    std::memcpy(st + b_rt + b_th, counters, b_cn);
+    std::memcpy(st + b_rt + b_th + b_cn, has_record, (size_t)n);
+    CT_CUDA(cudaMemcpyAsync(ctx->runtime.p, st, b_rt, cudaMemcpyHostToDevice, s));
+    CT_CUDA(cudaMemcpyAsync(ctx->threads.p, st + b_rt, b_th, cudaMemcpyHostToDevice, s));
+    CT_CUDA(cudaMemcpyAsync(ctx->counters.p, st + b_rt + b_th, b_cn, cudaMemcpyHostToDevice, s));
+    CT_CUDA(cudaMemcpyAsync(ctx->has_record.p, st + b_rt + b_th + b_cn, (size_t)n,
                             cudaMemcpyHostToDevice, s));
-    CT_CUDA(cudaMemcpyAsync(ctx->has_record.p, has_record, n, cudaMemcpyHostToDevice, s));
     ctx->has_stop = stop_mask != nullptr;
     if (stop_mask) {
-        size_t words = (size_t)((n + 31) / 32);
-        std::vector<uint32_t> bits(words, 0u);
+        uint32_t* bits = reinterpret_cast<uint32_t*>(st + b_rt + b_th + b_cn + b_hr);
+        std::memset(bits, 0, 4 * words);
         for (int64_t i = 0; i < n; ++i)
             if (stop_mask[i]) bits[i >> 5] |= 1u << (i & 31);
         CT_CUDA(ctx->stop_bits.ensure(words));
-        CT_CUDA(cudaMemcpyAsync(ctx->stop_bits.p, bits.data(), words * 4, cudaMemcpyHostToDevice, s));
-        CT_CUDA(cudaStreamSynchronize(s));
+        CT_CUDA(cudaMemcpyAsync(ctx->stop_bits.p, bits, words * 4, cudaMemcpyHostToDevice, s));
     }
-    CT_CUDA(cudaStreamSynchronize(s));
+    CT_CUDA(cudaEventRecord(ctx->stage_replay.done, s));
     ctx->replay_n = n;
     return CT_OK;
 }
