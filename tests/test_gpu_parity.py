@@ -31,6 +31,24 @@ def _keys(traj):
 
 @pytest.mark.parametrize("name", TRAJ_SETS)
 def test_batched_profile_trajectories_match_reference(name):
+    _check_trajectories(name)
+
+
+# the alternative kernel builds selected by environment at launch time:
+# warp-specialised two-repetition kernel, in-row prefixes scanned per draw,
+# one-warp and four-warp CTA sizes
+@pytest.mark.parametrize("env", [{"CT_SEARCH_WS": "4"}, {"CT_SEARCH_WS": "6"},
+                                 {"CT_SEARCH_PRE": "0"}, {"CT_SEARCH_NT": "32"},
+                                 {"CT_SEARCH_NT": "256"}],
+                         ids=["ws4", "ws6", "pre0", "nt32", "nt256"])
+@pytest.mark.parametrize("name", ["gradient", "b200_transpose"])
+def test_kernel_variants_match_reference(name, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _check_trajectories(name)
+
+
+def _check_trajectories(name):
     from paper_2102_05297_b200 import _native
     from paper_2102_05297_b200.search import search_params
     from paper_2102_05297_b200.space import replay_arrays
