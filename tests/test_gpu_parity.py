@@ -331,3 +331,35 @@ def test_device_expert_system_bit_exact():
         np.testing.assert_array_equal(b, e["b"][k], err_msg=f"case {k}")
         np.testing.assert_array_equal(d, e["delta"][k], err_msg=f"case {k}")
         assert deg == bool(e["degenerate"][k])
+
+
+def test_reference_acceptance_criteria_3_and_4():
+    """The reference's own acceptance gate (pkg/tests/test_acceptance.py:104-142)
+    on the GPU harness.  Trajectories are bit-exact, so the numbers are the
+    ones the reference itself computes in this container,
+    to the last bit: C3 random-baseline calibration 48.3443 mean steps
+    (N=1000, k=20, 10,000 repetitions); C4 exact-model improvement
+    13.824442820606503x, literal sign 0.06455974815939666x (values from
+    countertune.harness.simulate / pair_with_baseline with the same specs,
+    recorded with PYTHONPATH=/root/reference/pkg/src)."""
+    from paper_2102_05297_b200 import ExactModelSet, ExperimentSpec, pair_with_baseline, simulate
+    calib = dataset_from_golden("calibration")
+    rep = simulate(ExperimentSpec(dataset=calib, searcher="random", name="rand",
+                                  repetitions=10_000, seed=42, time_repetitions=10))
+    expected = 1001.0 / 21.0
+    assert abs(rep.mean_steps - expected) / expected <= 0.05
+    assert rep.mean_steps == 48.3443
+    grad = dataset_from_golden("gradient")
+    exact = ExactModelSet(grad)
+    prof = simulate(ExperimentSpec(dataset=grad, searcher="profile", model=exact, name="profile",
+                                   repetitions=1000, seed=42, time_repetitions=10))
+    rand = simulate(ExperimentSpec(dataset=grad, searcher="random", name="random",
+                                   repetitions=1000, seed=42, time_repetitions=10))
+    improvement = pair_with_baseline(prof, rand).improvement
+    literal = simulate(ExperimentSpec(dataset=grad, searcher="profile", model=exact,
+                                      name="literal", repetitions=1000, seed=42,
+                                      literal_sign=True, time_repetitions=10))
+    degraded = pair_with_baseline(literal, rand).improvement
+    assert improvement >= 2.0 and degraded < 1.2
+    assert improvement == 13.824442820606503
+    assert degraded == 0.06455974815939666
