@@ -363,3 +363,25 @@ def test_reference_acceptance_criteria_3_and_4():
     assert improvement >= 2.0 and degraded < 1.2
     assert improvement == 13.824442820606503
     assert degraded == 0.06455974815939666
+
+
+def test_reference_acceptance_criterion_6_portability():
+    """C6 (pkg/tests/test_acceptance.py:178-196): a tree model trained on
+    gradient (seed 0) steers the 3x-rescaled gradient3x space; the GPU
+    harness reproduces the reference's improvement to the last bit
+    (tests/golden/make_c6_golden.py)."""
+    from paper_2102_05297_b200 import ExperimentSpec, pair_with_baseline, simulate
+    from paper_2102_05297_b200.models import train_model_set
+    g = golden("ds_gradient3x.npz")
+    train_ds = dataset_from_golden("gradient")
+    target_ds = dataset_from_golden("gradient3x")
+    ms = train_model_set(train_ds, "tree", 0)
+    prof = simulate(ExperimentSpec(dataset=target_ds, searcher="profile", model=ms, name="ported",
+                                   repetitions=1000, seed=7, time_repetitions=10))
+    rand = simulate(ExperimentSpec(dataset=target_ds, searcher="random", name="random",
+                                   repetitions=1000, seed=7, time_repetitions=10))
+    improvement = pair_with_baseline(prof, rand).improvement
+    assert improvement > 1.5
+    assert prof.mean_steps == float(g["c6_prof_mean"])
+    assert rand.mean_steps == float(g["c6_rand_mean"])
+    assert improvement == float(g["c6_improvement"])
