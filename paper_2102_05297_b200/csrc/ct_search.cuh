@@ -529,29 +529,53 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
         const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cs);
         __syncwarp();
         CT_SUB(4);
-        // the reference's bookkeeping, draw by draw
-        for (int j = 0; j < made; ++j) {
-            const int64_t cj = __shfl_sync(FULL, (long long)my_choice, j);
-            const bool okj = __shfl_sync(FULL, rec_ok, j);
-            const double rtj = __shfl_sync(FULL, rt, j);
-            const bool stj = __shfl_sync(FULL, is_stop, j);
-            if (!okj) {
-                if (lane == 0) {
-                    rs.st = CT_STATUS_ERROR; rs.err = -4;
-                    if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)cj;
-                }
-                done = 1; break;
+        // the reference's bookkeeping (search.py:164-186), all draws of the
+        // chunk at once: draw j is recorded iff no earlier draw was an error
+        // or a stop; the first missing record ends the repetition unrecorded
+        // (stored at out_idx[ns] as the reference's trajectory shows it), a
+        // stop configuration is recorded and ends it too.  The profiled
+        // candidate is the LAST draw attaining the running minimum runtime
+        // (the reference's `<=`), which only matters while the repetition goes on.
+        const unsigned in_chunk = made >= 32 ? FULL : ((1u << made) - 1u);
+        const unsigned bad_m = __ballot_sync(FULL, lane < made && !rec_ok) & in_chunk;
+        const unsigned stop_m = __ballot_sync(FULL, rec_ok && is_stop) & in_chunk & ~bad_m;
+        const int first_bad = bad_m ? __ffs(bad_m) - 1 : 32;
+        const int first_stop = stop_m ? __ffs(stop_m) - 1 : 32;
+        const int nrec = min(made, min(first_bad, first_stop + 1));
+        const int ns0 = rs.ns;
+        bool fresh = false;
+        if (lane < nrec) {
+            out_idx[ns0 + lane] = (int32_t)my_choice;
+            out_prof[ns0 + lane] = 0;
+            const uint32_t m = 1u << (my_choice & 31);
+            fresh = !(atomicOr(&expl[my_choice >> 5], m) & m);
+        }
+        const int n_fresh = __popc(__ballot_sync(FULL, fresh));
+        const int64_t c_bad = __shfl_sync(FULL, (long long)my_choice, first_bad & 31);
+        __syncwarp();
+        if (lane == 0) {
+            rs.ns = ns0 + nrec;
+            rs.n_expl += n_fresh;
+            if (first_bad < first_stop && first_bad < made) {
+                rs.st = CT_STATUS_ERROR; rs.err = -4;
+                if (rs.ns < a.max_steps) out_idx[rs.ns] = (int32_t)c_bad;
+            } else if (first_stop < made) {
+                rs.st = CT_STATUS_STOPPED;
             }
-            if (lane == 0) {
-                out_idx[rs.ns] = (int32_t)cj; out_prof[rs.ns] = 0; ++rs.ns;
-                uint32_t m = 1u << (cj & 31);
-                if (!(expl[cj >> 5] & m)) { expl[cj >> 5] |= m; ++rs.n_expl; }
+        }
+        if (first_bad < made || first_stop < made) {
+            done = 1;
+        } else if (made > 0) {
+            double mn = lane < made ? rt : INFINITY;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) mn = fmin(mn, __shfl_xor_sync(FULL, mn, d));
+            if (mn <= t_best) {
+                const unsigned at = __ballot_sync(FULL, lane < made && rt == mn);
+                const int jw = 31 - __clz(at);
+                const int64_t cw = __shfl_sync(FULL, (long long)my_choice, jw);
+                t_best = mn;
+                if (lane == 0) rs.c_prof = cw;
             }
-            if (stj) {
-                if (lane == 0) rs.st = CT_STATUS_STOPPED;
-                done = 1; break;
-            }
-            if (rtj <= t_best) { t_best = rtj; if (lane == 0) rs.c_prof = cj; }
         }
         if (!done && exhausted) {
             if (lane == 0) rs.st = CT_STATUS_EXHAUSTED;
