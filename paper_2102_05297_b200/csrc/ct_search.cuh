@@ -302,11 +302,12 @@ __device__ __forceinline__ void rep_end(const SearchArgs& a, int rep, const RepS
 template <int NW>
 __device__ __forceinline__ void profile_step(const SearchArgs& a, RepState& rs, Ctl<NW>& ctl,
                                              uint32_t* expl, int32_t* out_idx, uint8_t* out_prof,
-                                             int lane) {
+                                             int lane, int col) {
+    // col: this lane's delta column (a.delta_col[lane], -1 past N_COMP),
+    // loaded once per kernel so that every load here depends on c_prof only
     const int64_t N = a.n;
     const int64_t cp = rs.c_prof;
     if (lane < N_REQ) ctl.cnt[lane] = a.counters[(size_t)cp * N_REQ + lane];
-    const int col = (lane < N_COMP) ? a.delta_col[lane] : -1;
     const double pv = (col >= 0) ? a.table[(size_t)col * a.ld + cp] : 0.0;
     const bool rec_ok = a.has_record[cp] != 0;
     const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cp);
@@ -625,19 +626,22 @@ k_profile_search(const SearchArgs a) {
 #else
 #define CT_CLK(acc) do { } while (0)
 #endif
+    const int pcol = (lane < N_COMP) ? a.delta_col[lane] : -1;
     for (int rep = blockIdx.x; rep < a.n_reps; rep += gridDim.x) {
         int32_t* out_idx = a.step_index + (size_t)rep * a.max_steps;
         uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
         if (warp == 0) rep_begin(a, seed_sh, rep, rs, ctl, expl, lane);
         __syncthreads();
 
-        for (int it = 0; it < a.outer; ++it) {
+        // warp 0 runs the draws and, without a CTA barrier in between, the
+        // next iteration's profile step (the other warps have nothing to do)
 #ifdef CT_PHASE_CLOCKS
-            if (tid == 0) clk_t = clock64();
+        if (tid == 0) clk_t = clock64();
 #endif
-            if (warp == 0) profile_step(a, rs, ctl, expl, out_idx, out_prof, lane);
-            __syncthreads();
-            CT_CLK(clk_p1);
+        if (warp == 0 && a.outer > 0) profile_step(a, rs, ctl, expl, out_idx, out_prof, lane, pcol);
+        __syncthreads();
+        CT_CLK(clk_p1);
+        for (int it = 0; it < a.outer; ++it) {
             if (ctl.done) break;
             score_phase<NT>(a, ctl, expl, w, tid);
             __syncthreads();
@@ -645,10 +649,14 @@ k_profile_search(const SearchArgs a) {
             weight_phase<PRE>(a, ctl, expl, w, pre, row_tot, warp);
             __syncthreads();
             CT_CLK(clk_weight);
-            if (warp == 0) draw_step<PRE>(a, rs, ctl, expl, w, pre, row_tot, jA, jC, out_idx, out_prof, lane);
+            if (warp == 0) {
+                draw_step<PRE>(a, rs, ctl, expl, w, pre, row_tot, jA, jC, out_idx, out_prof, lane);
+                CT_CLK(clk_p4);
+                if (!ctl.done && it + 1 < a.outer)
+                    profile_step(a, rs, ctl, expl, out_idx, out_prof, lane, pcol);
+            }
             __syncthreads();
-            CT_CLK(clk_p4);
-            if (ctl.done) break;
+            CT_CLK(clk_p1);
         }
         if (tid == 0) rep_end(a, rep, rs);
         __syncthreads();
@@ -724,6 +732,7 @@ k_profile_search_ws(const SearchArgs a) {
     if (warp == 0) {
         // ------------------------------ serial warp ------------------------
         int rep[2] = {0, 0}, it[2] = {-1, -1};
+        const int pcol = (lane < N_COMP) ? a.delta_col[lane] : -1;
 #ifdef CT_PHASE_CLOCKS
         long long clk_wait = 0, clk_work = 0, clk_t = clock64();
 #endif
@@ -734,7 +743,7 @@ k_profile_search_ws(const SearchArgs a) {
                 int32_t* out_idx = a.step_index + (size_t)rep[s] * a.max_steps;
                 uint8_t* out_prof = a.step_profiled + (size_t)rep[s] * a.max_steps;
                 if (it[s] < 0) { rep_begin(a, seed_sh, rep[s], rs[s], ctl[s], expl[s], lane); it[s] = 0; }
-                profile_step(a, rs[s], ctl[s], expl[s], out_idx, out_prof, lane);
+                profile_step(a, rs[s], ctl[s], expl[s], out_idx, out_prof, lane, pcol);
                 if (!ctl[s].done) { if (lane == 0) ctl[s].cmd = WS_RUN; __syncwarp(); return; }
                 if (lane == 0) rep_end(a, rep[s], rs[s]);
                 rep[s] += stride; it[s] = -1;
