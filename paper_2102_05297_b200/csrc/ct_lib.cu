@@ -372,13 +372,16 @@ __global__ void k_check_division(int64_t n, uint64_t seed, unsigned long long* b
 
 // ---- aggregation (harness.py:187-244) ---------------------------------
 // One thread per repetition: best-so-far and cumulative completion times.
-__global__ void k_agg_rows(const int32_t* step_index, const uint8_t* step_profiled,
-                           const int32_t* n_steps, int32_t reps, int64_t width,
-                           const double* runtime, double overhead, double* bsf, double* times,
-                           double* total, double* first) {
+__global__ void k_agg_rows(const int32_t* __restrict__ step_index,
+                           const uint8_t* __restrict__ step_profiled,
+                           const int32_t* __restrict__ n_steps, int32_t reps, int64_t width,
+                           const double* __restrict__ runtime, double overhead,
+                           double* __restrict__ bsf, double* __restrict__ times,
+                           double* __restrict__ total, double* __restrict__ first) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < reps; r += gridDim.x * blockDim.x) {
         const int n = n_steps[r];
         double best = INFINITY, t = 0.0;
+#pragma unroll 4
         for (int k = 0; k < n; ++k) {
             const size_t o = (size_t)r * width + k;
             const double rt = runtime[step_index[o]];
@@ -393,20 +396,50 @@ __global__ void k_agg_rows(const int32_t* step_index, const uint8_t* step_profil
     }
 }
 
-// One thread per step column: sums over repetitions in repetition order.
-__global__ void k_agg_cols(const double* bsf, const int32_t* n_steps, int32_t reps, int64_t width,
-                           int32_t max_len, const double* sum0, const double* sq0,
-                           double* sum, double* sq) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < max_len; k += gridDim.x * blockDim.x) {
-        double s = sum0 ? sum0[k] : 0.0, q = sq0 ? sq0[k] : 0.0;
-        for (int r = 0; r < reps; ++r) {
-            const int last = n_steps[r] - 1;
-            const double v = bsf[(size_t)r * width + (k < last ? k : last)];
-            s = add(s, v);
-            q = add(q, mul(v, v));
+// Step-curve column sums over repetitions, in repetition order (numpy's
+// axis-0 reduction adds row after row).  A block owns AGG_COLS columns: all
+// its threads gather a chunk of AGG_CHUNK repetitions' (padded) values into
+// shared memory in parallel, then one thread per column runs the sequential
+// sum over the chunk; the L2 round trips overlap instead of forming the chain.
+constexpr int AGG_COLS = 8, AGG_CHUNK = 256;
+__global__ void __launch_bounds__(AGG_CHUNK)
+k_agg_cols(const double* __restrict__ bsf, const int32_t* __restrict__ n_steps, int32_t reps,
+           int64_t width, int32_t max_len, const double* __restrict__ sum0,
+           const double* __restrict__ sq0, double* __restrict__ sum, double* __restrict__ sq) {
+    __shared__ double tile[AGG_CHUNK][AGG_COLS + 1];
+    const int k0 = blockIdx.x * AGG_COLS;
+    const int tid = threadIdx.x;
+    const int kc = k0 + tid;
+    double s = 0.0, q = 0.0;
+    if (tid < AGG_COLS && kc < max_len) {
+        s = sum0 ? sum0[kc] : 0.0;
+        q = sq0 ? sq0[kc] : 0.0;
+    }
+    for (int r0 = 0; r0 < reps; r0 += AGG_CHUNK) {
+        const int cnt = min(AGG_CHUNK, reps - r0);
+        if (tid < cnt) {
+            const int r = r0 + tid;
+            const int last = max(n_steps[r] - 1, 0);
+            const double* row = bsf + (size_t)r * width;
+#pragma unroll
+            for (int c = 0; c < AGG_COLS; ++c) {
+                const int k = k0 + c;
+                tile[tid][c] = (k < max_len) ? row[k < last ? k : last] : 0.0;
+            }
         }
-        sum[k] = s;
-        sq[k] = q;
+        __syncthreads();
+        if (tid < AGG_COLS) {
+            for (int j = 0; j < cnt; ++j) {
+                const double v = tile[j][tid];
+                s = add(s, v);
+                q = add(q, mul(v, v));
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < AGG_COLS && kc < max_len) {
+        sum[kc] = s;
+        sq[kc] = q;
     }
 }
 
@@ -431,10 +464,12 @@ __global__ void k_agg_sample(const double* bsf, const double* times, const int32
     }
 }
 
-__global__ void k_agg_time_sums(const double* sampled, int32_t reps, int32_t n_grid,
-                                const double* sum0, const double* sq0, double* sum, double* sq) {
+__global__ void k_agg_time_sums(const double* __restrict__ sampled, int32_t reps, int32_t n_grid,
+                                const double* __restrict__ sum0, const double* __restrict__ sq0,
+                                double* __restrict__ sum, double* __restrict__ sq) {
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n_grid; g += gridDim.x * blockDim.x) {
         double s = sum0 ? sum0[g] : 0.0, q = sq0 ? sq0[g] : 0.0;
+#pragma unroll 8
         for (int r = 0; r < reps; ++r) {
             const double v = sampled[(size_t)g * reps + r];
             s = add(s, v);
@@ -1136,7 +1171,7 @@ int ct_aggregate_steps(ct_ctx* ctx, double overhead, int32_t max_len, const doub
     if (max_len > 0) {
         if (sum0) CT_CUDA(cudaMemcpyAsync(d_sum0, sum0, 8 * (size_t)max_len, cudaMemcpyHostToDevice, s));
         if (sq0) CT_CUDA(cudaMemcpyAsync(d_sq0, sq0, 8 * (size_t)max_len, cudaMemcpyHostToDevice, s));
-        k_agg_cols<<<(max_len + 63) / 64, 64, 0, s>>>(ctx->agg_bsf.p, ctx->n_steps.p, (int32_t)R, W,
+        k_agg_cols<<<(max_len + AGG_COLS - 1) / AGG_COLS, AGG_CHUNK, 0, s>>>(ctx->agg_bsf.p, ctx->n_steps.p, (int32_t)R, W,
                                                       max_len, sum0 ? d_sum0 : nullptr,
                                                       sq0 ? d_sq0 : nullptr, d_sum, d_sq);
         CT_CUDA(cudaGetLastError());
