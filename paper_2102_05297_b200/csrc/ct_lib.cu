@@ -608,9 +608,7 @@ int launch_profile_ws(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int
 // PRE: in-row prefixes computed by all warps in the weight pass (default), or
 // the drawn row scanned by the drawing warp (CT_SEARCH_PRE=0)
 template <int NT>
-int launch_profile(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int n_reps) {
-    bool pre = true;
-    if (const char* env = std::getenv("CT_SEARCH_PRE")) pre = std::atoi(env) != 0;
+int launch_profile(ct_ctx* ctx, SearchArgs& a, bool pre, bool in_smem, size_t smem, int n_reps) {
     if (pre)
         return in_smem ? launch_profile_t<NT, true, true>(ctx, a, smem, n_reps)
                        : launch_profile_t<NT, false, true>(ctx, a, smem, n_reps);
@@ -1035,7 +1033,12 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     // otherwise a per-CTA slice of global scratch (L2-resident)
     const size_t budget = 200 * 1024;
     const size_t head_b = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
-    const size_t pref_b = 16 * 32 * (size_t)a.nrows;   // weights + in-row prefixes
+    // in-row prefixes stored by the weight pass (PRE) only pay off when the
+    // rows are few (the drawing warp then rescans nothing); otherwise the
+    // weight pass keeps just the row totals and the draw scans the drawn row
+    bool pre = a.nrows < 32;
+    if (const char* env = std::getenv("CT_SEARCH_PRE")) pre = std::atoi(env) != 0;
+    const size_t pref_b = (pre ? 16 : 8) * 32 * (size_t)a.nrows;   // weights [+ in-row prefixes]
     if (head_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the row index");
     const int64_t want_per_sm = std::min<int64_t>(std::min<int64_t>(
         (n_reps + ctx->sm_count - 1) / ctx->sm_count, 32), 2048 / nt);
@@ -1052,9 +1055,10 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
         const int64_t ctas_per_sm = std::max<int64_t>(1, (want_per_sm + 1) / 2);
         const size_t cap2 = std::min<size_t>(
             2 * budget, (size_t)(228 * 1024 / ctas_per_sm) - 3 * 1024);
-        bool ws_smem = 2 * (head_b + pref_b) <= cap2;
-        if (const char* env = std::getenv("CT_SEARCH_SMEM")) ws_smem = std::atoi(env) != 0 && 2 * (head_b + pref_b) <= 2 * budget;
-        const size_t smem2 = 2 * (head_b + (ws_smem ? pref_b : 0));
+        const size_t pref_ws = 16 * 32 * (size_t)a.nrows;   // this kernel always stores prefixes
+        bool ws_smem = 2 * (head_b + pref_ws) <= cap2;
+        if (const char* env = std::getenv("CT_SEARCH_SMEM")) ws_smem = std::atoi(env) != 0 && 2 * (head_b + pref_ws) <= 2 * budget;
+        const size_t smem2 = 2 * (head_b + (ws_smem ? pref_ws : 0));
         switch (ws) {
         case 2: return launch_profile_ws<2>(ctx, a, ws_smem, smem2, n_reps);
         case 3: return launch_profile_ws<3>(ctx, a, ws_smem, smem2, n_reps);
@@ -1064,11 +1068,11 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
         }
     }
     switch (nt) {
-    case 32: return launch_profile<32>(ctx, a, in_smem, smem, n_reps);
-    case 64: return launch_profile<64>(ctx, a, in_smem, smem, n_reps);
-    case 128: return launch_profile<128>(ctx, a, in_smem, smem, n_reps);
-    case 256: return launch_profile<256>(ctx, a, in_smem, smem, n_reps);
-    default: return launch_profile<512>(ctx, a, in_smem, smem, n_reps);
+    case 32: return launch_profile<32>(ctx, a, pre, in_smem, smem, n_reps);
+    case 64: return launch_profile<64>(ctx, a, pre, in_smem, smem, n_reps);
+    case 128: return launch_profile<128>(ctx, a, pre, in_smem, smem, n_reps);
+    case 256: return launch_profile<256>(ctx, a, pre, in_smem, smem, n_reps);
+    default: return launch_profile<512>(ctx, a, pre, in_smem, smem, n_reps);
     }
 }
 

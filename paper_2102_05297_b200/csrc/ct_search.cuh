@@ -251,12 +251,17 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
         w[e] = wt;
         bad |= !(wt <= SCORE_CEILING);
         double incl = wt;
+        if (PRE) {
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double v = __shfl_up_sync(FULL, incl, d);
-            if (lane >= d) incl = add(incl, v);
+            for (int d = 1; d < 32; d <<= 1) {
+                const double v = __shfl_up_sync(FULL, incl, d);
+                if (lane >= d) incl = add(incl, v);
+            }
+            pre[e] = incl;
+        } else {   // the row total only (any order: the draw certificate covers it)
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) incl = add(incl, __shfl_xor_sync(FULL, incl, d));
         }
-        if (PRE) pre[e] = incl;
         if (lane == 31) row_tot[t] = incl;
     }
 }

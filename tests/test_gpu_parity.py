@@ -35,12 +35,13 @@ def test_batched_profile_trajectories_match_reference(name):
 
 
 # the alternative kernel builds selected by environment at launch time:
-# warp-specialised two-repetition kernel, in-row prefixes scanned per draw,
-# one-warp and four-warp CTA sizes
+# warp-specialised two-repetition kernel, in-row prefixes stored by the
+# weight pass or scanned per draw (the default picks by row count), one-warp
+# and eight-warp CTA sizes
 @pytest.mark.parametrize("env", [{"CT_SEARCH_WS": "4"}, {"CT_SEARCH_WS": "6"},
-                                 {"CT_SEARCH_PRE": "0"}, {"CT_SEARCH_NT": "32"},
-                                 {"CT_SEARCH_NT": "256"}],
-                         ids=["ws4", "ws6", "pre0", "nt32", "nt256"])
+                                 {"CT_SEARCH_PRE": "0"}, {"CT_SEARCH_PRE": "1"},
+                                 {"CT_SEARCH_NT": "32"}, {"CT_SEARCH_NT": "256"}],
+                         ids=["ws4", "ws6", "pre0", "pre1", "nt32", "nt256"])
 @pytest.mark.parametrize("name", ["gradient", "b200_transpose"])
 def test_kernel_variants_match_reference(name, env, monkeypatch):
     for k, v in env.items():
