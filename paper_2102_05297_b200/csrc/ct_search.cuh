@@ -244,6 +244,48 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
     const double gamma = a.gamma;
     const double smin_e = (smin != 0.0) ? smin : 1.0;
     const double y_max = rcp_nv(smax), y_min = rcp_nv(smin_e);
+    if (!PRE) {
+        // row totals only, four rows of this warp at a time, reduced together:
+        // two exchange levels halve the rows a lane holds (lane 8r ends up
+        // with row r of the group), three butterfly levels finish the sums --
+        // 6 shuffles per 4 rows instead of 20.  Any order is fine: the draw
+        // certificate covers every summation order.
+        for (int t0 = pw; t0 < a.nrows; t0 += 4 * nw) {
+            double v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int t = t0 + i * nw;
+                const int64_t e = 32LL * t + lane;
+                double wt = 0.0;
+                if (t < a.nrows) {
+                    if (e < N && !bit_get(expl, e))
+                        wt = weight_of<CERT>(w[e], smax, smin_e, y_max, y_min, gamma);
+                    w[e] = wt;
+                }
+                bad |= !(wt <= SCORE_CEILING);
+                v[i] = wt;
+            }
+            const bool up16 = lane & 16, up8 = lane & 8;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {      // rows {i, i+2}: lower lanes keep i
+                const double send = up16 ? v[i] : v[i + 2];
+                const double keep = up16 ? v[i + 2] : v[i];
+                v[i] = add(keep, __shfl_xor_sync(FULL, send, 16));
+            }
+            {                                   // rows {0, 1} of what is left
+                const double send = up8 ? v[0] : v[1];
+                const double keep = up8 ? v[1] : v[0];
+                v[0] = add(keep, __shfl_xor_sync(FULL, send, 8));
+            }
+#pragma unroll
+            for (int d = 4; d > 0; d >>= 1) v[0] = add(v[0], __shfl_xor_sync(FULL, v[0], d));
+            // lane 8r holds row r = 2 (lane >> 4 & 1) + (lane >> 3 & 1)
+            const int r = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+            const int t = t0 + r * nw;
+            if ((lane & 7) == 0 && t < a.nrows) row_tot[t] = v[0];
+        }
+        return;
+    }
     for (int t = pw; t < a.nrows; t += nw) {
         const int64_t e = 32LL * t + lane;
         double wt = 0.0;
@@ -251,17 +293,12 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
         w[e] = wt;
         bad |= !(wt <= SCORE_CEILING);
         double incl = wt;
-        if (PRE) {
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const double v = __shfl_up_sync(FULL, incl, d);
-                if (lane >= d) incl = add(incl, v);
-            }
-            pre[e] = incl;
-        } else {   // the row total only (any order: the draw certificate covers it)
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) incl = add(incl, __shfl_xor_sync(FULL, incl, d));
+        for (int d = 1; d < 32; d <<= 1) {
+            const double v = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl = add(incl, v);
         }
+        pre[e] = incl;
         if (lane == 31) row_tot[t] = incl;
     }
 }
