@@ -244,7 +244,7 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
     const double gamma = a.gamma;
     const double smin_e = (smin != 0.0) ? smin : 1.0;
     const double y_max = rcp_nv(smax), y_min = rcp_nv(smin_e);
-    if (!PRE) {
+    if constexpr (!PRE) {
         // row totals only, four rows of this warp at a time, reduced together:
         // two exchange levels halve the rows a lane holds (lane 8r ends up
         // with row r of the group), three butterfly levels finish the sums --
@@ -284,22 +284,22 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
             const int t = t0 + r * nw;
             if ((lane & 7) == 0 && t < a.nrows) row_tot[t] = v[0];
         }
-        return;
-    }
-    for (int t = pw; t < a.nrows; t += nw) {
-        const int64_t e = 32LL * t + lane;
-        double wt = 0.0;
-        if (e < N && !bit_get(expl, e)) wt = weight_of<CERT>(w[e], smax, smin_e, y_max, y_min, gamma);
-        w[e] = wt;
-        bad |= !(wt <= SCORE_CEILING);
-        double incl = wt;
+    } else {
+        for (int t = pw; t < a.nrows; t += nw) {
+            const int64_t e = 32LL * t + lane;
+            double wt = 0.0;
+            if (e < N && !bit_get(expl, e)) wt = weight_of<CERT>(w[e], smax, smin_e, y_max, y_min, gamma);
+            w[e] = wt;
+            bad |= !(wt <= SCORE_CEILING);
+            double incl = wt;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double v = __shfl_up_sync(FULL, incl, d);
-            if (lane >= d) incl = add(incl, v);
+            for (int d = 1; d < 32; d <<= 1) {
+                const double v = __shfl_up_sync(FULL, incl, d);
+                if (lane >= d) incl = add(incl, v);
+            }
+            pre[e] = incl;
+            if (lane == 31) row_tot[t] = incl;
         }
-        pre[e] = incl;
-        if (lane == 31) row_tot[t] = incl;
     }
 }
 
