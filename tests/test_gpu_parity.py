@@ -37,11 +37,12 @@ def test_batched_profile_trajectories_match_reference(name):
 # the alternative kernel builds selected by environment at launch time:
 # warp-specialised two-repetition kernel, in-row prefixes stored by the
 # weight pass or scanned per draw (the default picks by row count), one-warp
-# and eight-warp CTA sizes
+# and eight-warp CTA sizes, weights in a global slice instead of shared memory
 @pytest.mark.parametrize("env", [{"CT_SEARCH_WS": "4"}, {"CT_SEARCH_WS": "6"},
                                  {"CT_SEARCH_PRE": "0"}, {"CT_SEARCH_PRE": "1"},
-                                 {"CT_SEARCH_NT": "32"}, {"CT_SEARCH_NT": "256"}],
-                         ids=["ws4", "ws6", "pre0", "pre1", "nt32", "nt256"])
+                                 {"CT_SEARCH_NT": "32"}, {"CT_SEARCH_NT": "256"},
+                                 {"CT_SEARCH_SMEM": "0"}],
+                         ids=["ws4", "ws6", "pre0", "pre1", "nt32", "nt256", "smem0"])
 @pytest.mark.parametrize("name", ["gradient", "b200_transpose"])
 def test_kernel_variants_match_reference(name, env, monkeypatch):
     for k, v in env.items():
