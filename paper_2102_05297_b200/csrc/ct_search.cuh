@@ -229,7 +229,8 @@ __device__ __forceinline__ double weight_of(double s, double smax, double smin_e
     if (!CERT) {
         if (__builtin_expect(!dvd_accept(s, den, r, ratio), 0)) ratio = dvd_term(s, den);
     }
-    const double w = pow8(pos ? add(1.0, ratio) : sub(1.0, ratio));
+    // 1 - ratio == 1 + (-ratio) exactly: one add, the sign by select
+    const double w = pow8(add(1.0, pos ? ratio : -ratio));
     if (pos) return (w > SCORE_CEILING) ? SCORE_CEILING : w;            // np.minimum
     if (s > gamma) return (w < SCORE_FLOOR) ? SCORE_FLOOR : w;          // np.maximum
     return (s <= gamma) ? SCORE_FLOOR : 0.0;                            // NaN: no branch
