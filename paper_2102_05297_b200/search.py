@@ -4,7 +4,7 @@ Same names, signatures, argument meaning and exceptions as the reference's
 `countertune.search`; every numeric step runs in libct_b200.so on the GPU:
 
     score_configurations  -> ct_score       (Eq. 16, bit-exact FP64)
-    normalize_scores      -> ct_normalize   (Eq. 17, correctly rounded x**8)
+    normalize_scores      -> ct_normalize   (Eq. 17, x**8 within 1 ulp, as numpy's pow)
     weighted_select       -> ct_select      (exact prefix, certified draw)
     run_profile_search    -> ct_profile_search_launch (whole search on device)
                              for replayed datasets; otherwise the host drives
