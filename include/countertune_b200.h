@@ -184,8 +184,10 @@ int ct_random_search_launch(ct_ctx* ctx, const ct_seed_spec* seeds, int32_t n_re
 /* Trajectories of the last launch.  step_index / step_profiled are
  * n_reps x max_steps (row-major, max_steps = ct_result_max_steps()),
  * n_steps / status / rep_error are n_reps each (rep_error: CT_ERR_* of a
- * repetition that stopped with CT_STATUS_ERROR, else 0).  Any pointer may
- * be NULL.  Synchronises. */
+ * repetition that stopped with CT_STATUS_ERROR, else 0).  Slots past a
+ * repetition's steps are 0, except that an error repetition's failing
+ * configuration index follows its steps.  Any pointer may be NULL.
+ * Synchronises. */
 int ct_result_max_steps(ct_ctx* ctx, int64_t* max_steps);
 int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled,
                      int32_t* n_steps, int32_t* status, int32_t* rep_error,

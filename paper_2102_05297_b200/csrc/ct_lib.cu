@@ -1117,6 +1117,25 @@ int ct_result_max_steps(ct_ctx* ctx, int64_t* max_steps) {
     return CT_OK;
 }
 
+// Zero the trajectory slots a launch did not write (past a repetition's
+// steps; an error repetition keeps the slot after them, its failing index),
+// so that a fetch copies defined bytes only.
+__global__ void k_clear_tails(int32_t* __restrict__ step_index, uint8_t* __restrict__ step_profiled,
+                              const int32_t* __restrict__ n_steps, const int32_t* __restrict__ status,
+                              int32_t reps, int64_t width) {
+    const int64_t total = (int64_t)reps * width;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / width);
+        const int64_t k = i % width;
+        const int64_t keep = n_steps[r] + (status[r] == CT_STATUS_ERROR ? 1 : 0);
+        if (k >= keep) {
+            step_index[i] = 0;
+            step_profiled[i] = 0;
+        }
+    }
+}
+
 int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled, int32_t* n_steps,
                      int32_t* status, int32_t* rep_error, ct_batch_stats* stats) {
     int rc = check_ctx(ctx); if (rc) return rc;
@@ -1124,6 +1143,13 @@ int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled, i
     cudaStream_t s = ctx->stream;
     size_t r = (size_t)ctx->res_reps, m = (size_t)ctx->res_max_steps;
     if (r) {
+        if ((step_index || step_profiled) && m) {
+            const int64_t total = (int64_t)(r * m);
+            k_clear_tails<<<(int)std::min<int64_t>((total + 255) / 256, 4 * 148), 256, 0, s>>>(
+                ctx->step_index.p, ctx->step_profiled.p, ctx->n_steps.p, ctx->status.p,
+                (int32_t)r, (int64_t)m);
+            CT_CUDA(cudaGetLastError());
+        }
         if (step_index)
             CT_CUDA(cudaMemcpyAsync(step_index, ctx->step_index.p, 4 * r * m, cudaMemcpyDeviceToHost, s));
         if (step_profiled)
