@@ -143,8 +143,10 @@ __device__ __forceinline__ void score_epilogue(double acc, int64_t e, const uint
                                                double* w, double& lmax, double& lmin,
                                                double& lamin, bool& nan) {
     // branch-free: an explored configuration contributes the neutral element
+    // and leaves a NaN, which Eq. 17 maps to weight 0 exactly as it maps an
+    // explored one (the weight pass then needs no explored test)
     const bool in = !bit_get(expl, e);
-    w[e] = in ? acc : 0.0;
+    w[e] = in ? acc : __longlong_as_double(0x7ff8000000000000ll);
     const double vmax = in ? acc : -INFINITY, vmin = in ? acc : INFINITY;
     lmax = (vmax > lmax) ? vmax : lmax;
     lmin = (vmin < lmin) ? vmin : lmin;
@@ -259,7 +261,7 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
                 const int64_t e = 32LL * t + lane;
                 double wt = 0.0;
                 if (t < a.nrows) {
-                    if (e < N && !bit_get(expl, e))
+                    if (e < N && (CERT || !bit_get(expl, e)))
                         wt = weight_of<CERT>(w[e], smax, smin_e, y_max, y_min, gamma);
                     w[e] = wt;
                 }
@@ -289,7 +291,7 @@ __device__ __forceinline__ void weight_pass(const SearchArgs& a, int pw, int nw,
         for (int t = pw; t < a.nrows; t += nw) {
             const int64_t e = 32LL * t + lane;
             double wt = 0.0;
-            if (e < N && !bit_get(expl, e)) wt = weight_of<CERT>(w[e], smax, smin_e, y_max, y_min, gamma);
+            if (e < N && (CERT || !bit_get(expl, e))) wt = weight_of<CERT>(w[e], smax, smin_e, y_max, y_min, gamma);
             w[e] = wt;
             bad |= !(wt <= SCORE_CEILING);
             double incl = wt;
