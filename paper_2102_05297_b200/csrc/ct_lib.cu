@@ -371,28 +371,49 @@ __global__ void k_check_division(int64_t n, uint64_t seed, unsigned long long* b
 }
 
 // ---- aggregation (harness.py:187-244) ---------------------------------
-// One thread per repetition: best-so-far and cumulative completion times.
-__global__ void k_agg_rows(const int32_t* __restrict__ step_index,
-                           const uint8_t* __restrict__ step_profiled,
-                           const int32_t* __restrict__ n_steps, int32_t reps, int64_t width,
-                           const double* __restrict__ runtime, double overhead,
-                           double* __restrict__ bsf, double* __restrict__ times,
-                           double* __restrict__ total, double* __restrict__ first) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < reps; r += gridDim.x * blockDim.x) {
+// One warp per repetition: best-so-far and cumulative completion times.
+// The lanes gather a chunk of 32 steps at once (coalesced index reads, the
+// runtime lookups in parallel); the completion-time sum and the running
+// minimum then fold through the chunk in step order by shuffles, so the sums
+// keep the reference's left-to-right order (harness.py:189-205).
+__global__ void __launch_bounds__(256)
+k_agg_rows(const int32_t* __restrict__ step_index, const uint8_t* __restrict__ step_profiled,
+           const int32_t* __restrict__ n_steps, int32_t reps, int64_t width,
+           const double* __restrict__ runtime, double overhead, double* __restrict__ bsf,
+           double* __restrict__ times, double* __restrict__ total, double* __restrict__ first) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < reps; r += warps) {
         const int n = n_steps[r];
-        double best = INFINITY, t = 0.0;
-#pragma unroll 4
-        for (int k = 0; k < n; ++k) {
+        double best = INFINITY, t = 0.0, t_first = 0.0;
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
             const size_t o = (size_t)r * width + k;
-            const double rt = runtime[step_index[o]];
-            const double cost = mul(rt, step_profiled[o] ? overhead : 1.0);
-            t = (k == 0) ? cost : add(t, cost);
-            best = (k == 0) ? rt : nmin(best, rt);
-            bsf[o] = best;
-            times[o] = t;
+            double rt = 0.0, cost = 0.0;
+            if (k < n) {
+                rt = runtime[step_index[o]];
+                cost = mul(rt, step_profiled[o] ? overhead : 1.0);
+            }
+            const int cnt = min(32, n - k0);
+            double my_t = 0.0, my_b = 0.0;
+            for (int j = 0; j < cnt; ++j) {
+                const double cj = __shfl_sync(0xffffffffu, cost, j);
+                const double rj = __shfl_sync(0xffffffffu, rt, j);
+                const bool head = (k0 + j == 0);
+                t = head ? cj : add(t, cj);
+                best = head ? rj : nmin(best, rj);
+                if (head) t_first = t;
+                if (lane == j) { my_t = t; my_b = best; }
+            }
+            if (k < n) {
+                bsf[o] = my_b;
+                times[o] = my_t;
+            }
         }
-        total[r] = t;
-        first[r] = times[(size_t)r * width];
+        if (lane == 0) {
+            total[r] = t;
+            first[r] = t_first;
+        }
     }
 }
 
@@ -1193,7 +1214,7 @@ int ct_aggregate_steps(ct_ctx* ctx, double overhead, int32_t max_len, const doub
     double* d_sum = d_sq0 + max_len;
     double* d_sq = d_sum + max_len;
     if (R > 0) {
-        k_agg_rows<<<(int)std::min<int64_t>((R + 127) / 128, 1184), 128, 0, s>>>(
+        k_agg_rows<<<(int)std::min<int64_t>((R + 7) / 8, 8 * 148), 256, 0, s>>>(
             ctx->step_index.p, ctx->step_profiled.p, ctx->n_steps.p, (int32_t)R, W, ctx->runtime.p,
             overhead, ctx->agg_bsf.p, ctx->agg_times.p, d_total, d_first);
         CT_CUDA(cudaGetLastError());
