@@ -204,21 +204,24 @@ class Context:
 
     # -- resident inputs ---------------------------------------------------
     def upload_table(self, matrix: np.ndarray, key=None):
-        if key is not None and key == self._table_key:
+        """key: an object identifying the contents (e.g. the array itself);
+        a call with the object the last upload was keyed by is a no-op.  The
+        context holds the key, so its identity cannot be reused meanwhile."""
+        if key is not None and key is self._table_key:
             return
         m = np.ascontiguousarray(matrix, dtype=np.float64)
         check(library().ct_table_upload(self.handle, ptr(m), m.shape[0], m.shape[1]))
         self._table_key = key
 
     def upload_space(self, assignments: np.ndarray, key=None):
-        if key is not None and key == self._space_key:
+        if key is not None and key is self._space_key:
             return
         a = np.ascontiguousarray(assignments, dtype=np.float64)
         check(library().ct_space_upload(self.handle, ptr(a), a.shape[0], a.shape[1]))
         self._space_key = key
 
     def upload_replay(self, runtime, threads, counters, has_record, stop_mask=None, key=None):
-        if key is not None and key == self._replay_key:
+        if key is not None and key is self._replay_key:
             return
         rt = np.ascontiguousarray(runtime, dtype=np.float64)
         th = np.ascontiguousarray(threads, dtype=np.int64)

@@ -53,14 +53,22 @@ class DeviceShard:
             launch(self.ctx, spec, params, first, n)
 
     def status(self):
+        """(n_steps, status, configs scored, uncertified draws, error).
+
+        error is None, or (global repetition, status code, failing index) of
+        the range's first failed repetition.  It is returned, not raised: the
+        caller exchanges it with the other ranks first, so that every rank
+        raises the same exception instead of one rank leaving its peers
+        blocked in a collective."""
         if self.n == 0:
-            return (np.zeros(0, np.int32), np.zeros(0, np.int32), 0, 0)
+            return (np.zeros(0, np.int32), np.zeros(0, np.int32), 0, 0, None)
         nst, status, err, stats = self.ctx.fetch_status(self.n)
         bad = np.flatnonzero(status == _native.CT_STATUS_ERROR)
+        error = None
         if bad.size:
             r = int(bad[0])
-            raise rep_error(int(err[r]), self.ctx.failing_index(r, self.n))
-        return nst, status, int(stats.configs_scored), int(stats.uncertified)
+            error = (self.first + r, int(err[r]), self.ctx.failing_index(r, self.n))
+        return nst, status, int(stats.configs_scored), int(stats.uncertified), error
 
     def aggregate_steps(self, overhead, max_len, sum0, sq0):
         if self.n == 0:
@@ -138,8 +146,17 @@ def simulate_distributed(spec: ExperimentSpec, device: int = 0,
     reps = spec.repetitions
     first, n = rep_range(reps, world, rank)
     shard = (shard_factory or (lambda s, f, c: DeviceShard(s, f, c, device)))(spec, first, n)
-    nst_local, status_local, scored, uncert = shard.status()
+    nst_local, status_local, scored, uncert, error = shard.status()
     counts = [rep_range(reps, world, k)[1] for k in range(world)]
+
+    # every rank learns of any rank's failed repetition before the report's
+    # collectives start, and all raise the error of the lowest failed
+    # repetition (the one a sequential run meets first)
+    mine = np.array(error if error is not None else (reps, 0, -1), dtype=np.int64)
+    errs = _all_gather_1d(dist, mine, [3] * world, dev).reshape(world, 3)
+    worst = errs[int(np.argmin(errs[:, 0]))]
+    if int(worst[0]) < reps:
+        raise rep_error(int(worst[1]), int(worst[2]))
 
     nst = _all_gather_1d(dist, nst_local.astype(np.int64), counts, dev)
     status = _all_gather_1d(dist, status_local.astype(np.int64), counts, dev)

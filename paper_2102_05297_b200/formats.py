@@ -128,7 +128,8 @@ def _check_range(idx, abbr, value):
 
 
 def load_measurements(path, space: TuningSpace, arch: ArchProfile):
-    """space.py:286-350 -> (runtime[n], threads[n], names, matrix[n x k], has_record[n])."""
+    """space.py:286-350 -> (runtime[n], threads[n], names, matrix[n x k], has_record[n],
+    config indices in file order)."""
     n = len(space)
     with open(path, "r", encoding="utf-8", newline="") as fh:
         reader = csv.reader(fh)
@@ -161,6 +162,7 @@ def load_measurements(path, space: TuningSpace, arch: ArchProfile):
         cm = np.zeros((n, len(names)))
         hr = np.zeros(n, dtype=bool)
         seen = {}
+        order = []
         for lineno, row in enumerate(reader, start=2):
             if not row:
                 continue
@@ -197,9 +199,10 @@ def load_measurements(path, space: TuningSpace, arch: ArchProfile):
             except ValueError as exc:
                 raise DatasetFormatError(path, lineno, str(exc))
             rt[idx], th[idx], hr[idx] = runtime, threads, True
+            order.append(idx)
         if not hr.any():
             raise DatasetFormatError(path, 2, "no records")
-    return rt, th, names, cm, hr
+    return rt, th, names, cm, hr, np.array(order, dtype=np.int64)
 
 
 def save_measurements(dataset: Dataset, path) -> None:
@@ -283,11 +286,11 @@ def load_dataset(space_path, measurements_path, arch_path,
                  input_label: Optional[str] = None) -> Dataset:
     space = load_space(space_path)
     arch = load_arch(arch_path)
-    rt, th, names, cm, hr = load_measurements(measurements_path, space, arch)
+    rt, th, names, cm, hr, order = load_measurements(measurements_path, space, arch)
     if input_label is None:
         input_label = os.path.basename(os.path.dirname(os.path.abspath(measurements_path)))
     return Dataset(space, arch, input_label, runtime_us=rt, global_threads=th,
-                   counter_names=names, counter_matrix=cm, has_record=hr)
+                   counter_names=names, counter_matrix=cm, has_record=hr, record_order=order)
 
 
 def load_dataset_dir(directory, input_label: Optional[str] = None) -> Dataset:

@@ -153,7 +153,13 @@ def prepare_device(ctx: "_native.Context", spec: ExperimentSpec, table=None):
     stop = well_performing_mask(ds, spec.slack)
     if not spec.stop_at_well_performing:
         stop[:] = False
-    ctx.upload_replay(rt, th, np.nan_to_num(req), hr, stop.astype(np.uint8))
+    if spec.searcher == SEARCHER_RANDOM:
+        # random search never reads counters; a dataset without some of them
+        # has NaN columns there, which must not reach the device
+        req = np.nan_to_num(req, nan=0.0, posinf=np.inf, neginf=-np.inf)
+    # the profile searcher sees the counters as recorded (+-inf included, as
+    # the reference's analyze() does; a missing counter raises below)
+    ctx.upload_replay(rt, th, req, hr, stop.astype(np.uint8))
     params = None
     if spec.searcher == SEARCHER_PROFILE:
         missing = missing_required(ds)

@@ -13,6 +13,7 @@ Same names, signatures, argument meaning and exceptions as the reference's
     run_random_search     -> ct_random_search_launch for replayed datasets.
 """
 
+import copy
 import shlex
 import subprocess
 from dataclasses import dataclass
@@ -177,9 +178,11 @@ def score_configurations(models, c_profile, delta: Dict[str, float], space,
     if len(cols) > MAX_SCORE_KEYS:
         raise ValueError(f"at most {MAX_SCORE_KEYS} scored counters are supported")
     ctx = _ctx()
-    ctx.upload_table(table.matrix)
+    # keyed by the array objects: the host-driven, live and ask/tell loops
+    # call this every outer iteration with the same table and space
+    ctx.upload_table(table.matrix, key=table.matrix)
     if score_top_k is not None and score_top_k < int((~explored_mask).sum()):
-        ctx.upload_space(assignments_of(space))
+        ctx.upload_space(assignments_of(space), key=space)
     raw, scoreable = ctx.score(c_profile.index, cols, vals, explored_mask, literal_sign,
                                score_top_k, n)
     return ScoreVector(raw=raw, explored=explored_mask, scoreable=scoreable)
@@ -506,7 +509,15 @@ def _profile_search_batches(space, arch, table, total, *, i, n, seed, inst_react
     recorded steps, the stop test and the later-ties-win argmin follow the
     reference's order.  That is what lets several GPUs time one iteration's
     candidates concurrently (dist_live.py)."""
-    rng = np.random.default_rng(seed)
+    # A caller-owned Generator is drawn from through a private copy: the n
+    # draws of an iteration are made before any is measured, so on an early
+    # stop the copy has consumed draws the reference never makes.  The
+    # caller's Generator is advanced by exactly the reference's draws when
+    # the search ends (one integers(), then one random() per recorded draw;
+    # SURVEY F7: random(k) consumes the stream as k single calls do).
+    caller = seed if isinstance(seed, np.random.Generator) else None
+    rng = (np.random.Generator(copy.deepcopy(caller.bit_generator)) if caller is not None
+           else np.random.default_rng(seed))
     explored = np.zeros(total, dtype=bool)
     steps: List[TraceStep] = []
     c_profile = space.configurations[int(rng.integers(0, total))]
@@ -519,16 +530,24 @@ def _profile_search_batches(space, arch, table, total, *, i, n, seed, inst_react
         explored[idx] = True
         return stop_indices is not None and idx in stop_indices
 
+    def finish(status: str) -> SearchTrace:
+        if caller is not None:
+            caller.integers(0, total)
+            drawn = sum(1 for s in steps if not s.profiled)
+            if drawn:
+                caller.random(drawn)
+        return SearchTrace(steps=steps, seed=seed, status=status)
+
     for _ in range(i):
         m = (yield ([c_profile.index], True))[0]
         if record(c_profile.index, m.runtime_us, True):
-            return SearchTrace(steps=steps, seed=seed, status=STATUS_STOPPED)
+            return finish(STATUS_STOPPED)
         _check_inst_reaction(inst_reaction)
         _, deltas, _ = ctx.analyze_react(_counters23(m), gen, arch.cores,
                                          m.global_threads, inst_reaction)
         delta = dict(zip(cc.DELTA_KEYS, map(float, deltas)))
         if not (~explored).any():
-            return SearchTrace(steps=steps, seed=seed, status=STATUS_EXHAUSTED)
+            return finish(STATUS_EXHAUSTED)
         scores = score_configurations(table, c_profile, delta, space, explored,
                                       literal_sign=literal_sign, score_top_k=score_top_k)
         scores = normalize_scores(scores)
@@ -548,15 +567,15 @@ def _profile_search_batches(space, arch, table, total, *, i, n, seed, inst_react
         t_best = np.inf
         for c, meas in zip(chosen, got):
             if record(c, meas.runtime_us, False):
-                return SearchTrace(steps=steps, seed=seed, status=STATUS_STOPPED)
+                return finish(STATUS_STOPPED)
             if meas.runtime_us <= t_best:
                 t_best = meas.runtime_us
                 c_profile = space.configurations[c]
         if len(got) < len(chosen):
             raise CounterTuneError("a measurement batch was cut short before a stop configuration")
         if exhausted:
-            return SearchTrace(steps=steps, seed=seed, status=STATUS_EXHAUSTED)
-    return SearchTrace(steps=steps, seed=seed, status=STATUS_BUDGET)
+            return finish(STATUS_EXHAUSTED)
+    return finish(STATUS_BUDGET)
 
 
 def _profile_search_steps(space, arch, table, total, *, i, n, seed, inst_reaction,

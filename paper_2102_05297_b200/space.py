@@ -123,7 +123,7 @@ class Dataset:
 
     def __init__(self, space, arch: ArchProfile, input_label: str, records=None, *,
                  runtime_us=None, global_threads=None, counter_names=None,
-                 counter_matrix=None, has_record=None):
+                 counter_matrix=None, has_record=None, record_order=None):
         self.space = space
         self.arch = arch
         self.input_label = input_label
@@ -151,6 +151,7 @@ class Dataset:
                 th[i] = rec.global_threads
                 cm[i] = [rec.counters[a] for a in names]
             self._records = records
+            order = np.array([rec.config_index for rec in records], dtype=np.int64)
         else:
             names = tuple(counter_names)
             rt = np.ascontiguousarray(runtime_us, dtype=np.float64)
@@ -165,11 +166,19 @@ class Dataset:
             if np.any(rt[hr] <= 0) or np.any(th[hr] < 1):
                 raise ValueError("runtime_us must be > 0 and global_threads >= 1")
             self._records = None
+            order = (np.flatnonzero(hr) if record_order is None
+                     else np.ascontiguousarray(record_order, dtype=np.int64))
+            if record_order is not None and not np.array_equal(np.sort(order), np.flatnonzero(hr)):
+                raise ValueError("record_order must list every recorded configuration once")
         self.runtime_us = rt
         self.global_threads = th
         self.counter_names = names
         self.counter_matrix = cm
         self.has_record = hr
+        # configuration indices of the records in file order (the reference
+        # keeps Dataset.records in measurements.csv order, space.py:286-350;
+        # model training and counter errors iterate records in that order)
+        self.record_order = order
 
     @property
     def records(self) -> Tuple[MeasurementRecord, ...]:
@@ -179,7 +188,7 @@ class Dataset:
                 MeasurementRecord(config_index=int(i), runtime_us=float(self.runtime_us[i]),
                                   global_threads=int(self.global_threads[i]),
                                   counters=dict(zip(names, map(float, self.counter_matrix[i]))))
-                for i in np.flatnonzero(self.has_record))
+                for i in self.record_order)
         return self._records
 
     @property

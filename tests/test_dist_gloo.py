@@ -50,7 +50,7 @@ class HostShard:
         nst = np.array([len(s) for s, _ in self.traj], dtype=np.int32)
         code = {"budget": 0, "stopped": 1, "exhausted": 2}
         status = np.array([code[st] for _, st in self.traj], dtype=np.int32)
-        return nst, status, 0, 0
+        return nst, status, 0, 0, None
 
     def _rows(self, overhead):
         out = []
@@ -114,6 +114,40 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
+class FailingShard(HostShard):
+    """Rank 1's range holds a repetition whose replay lookup failed."""
+
+    def status(self):
+        nst, status, a, b, _ = super().status()
+        if self.first > 0:
+            return nst, status, a, b, (self.first + 1, -4, 123)
+        return nst, status, a, b, None
+
+
+def _error_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2102_05297_b200 import ExperimentSpec
+        from paper_2102_05297_b200.dist import simulate_distributed
+        ds = dataset_from_golden("gradient")
+        spec = ExperimentSpec(dataset=ds, searcher="random", repetitions=10, seed=7)
+        try:
+            simulate_distributed(spec, shard_factory=FailingShard)
+            msg = "no error"
+        except Exception as e:     # noqa: BLE001 - the message is the result
+            msg = f"{type(e).__name__}: {e}"
+        with open(os.path.join(out_dir, f"err{rank}.txt"), "w") as f:
+            f.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -138,3 +172,14 @@ def test_distributed_report_matches_reference(world, tmp_path):
         got = np.load(tmp_path / f"rank{rank}.npz")
         for key in got.files:
             np.testing.assert_array_equal(got[key], gold[key], err_msg=f"rank {rank}: {key}")
+
+
+@pytest.mark.timeout(120)
+def test_failed_repetition_raises_on_every_rank(tmp_path):
+    """A failed repetition on one rank is raised by all ranks (no rank is
+    left waiting in a collective)."""
+    world = 2
+    mp.spawn(_error_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    msgs = [open(tmp_path / f"err{r}.txt").read() for r in range(world)]
+    assert msgs[0] == msgs[1]
+    assert msgs[0] == "CounterTuneError: dataset holds no measurement for configuration 123"

@@ -217,6 +217,34 @@ def test_host_driven_profile_search_matches_reference():
         assert [s.config_index for s in tr.steps] == want[r]
 
 
+def test_host_driven_generator_seed_advances_like_reference():
+    """A caller-owned numpy Generator as the seed: the searcher draws a whole
+    iteration's candidates before measuring them, but on an early stop the
+    caller's Generator must end where the reference leaves it (one
+    integers() plus one random() per recorded draw)."""
+    from paper_2102_05297_b200 import DatasetReplaySource, run_profile_search
+
+    class LiveLike(DatasetReplaySource):
+        pass
+
+    traj = golden("traj_gradient.npz")
+    ds, table = _table("gradient", "exact")
+    seeds = np.random.SeedSequence(42).spawn(int(traj["reps"]))
+    want = ragged(traj, "exact_stop")
+    stop = set(traj["well"].tolist())
+    for r in range(4):
+        g = np.random.default_rng(seeds[r])
+        tr = run_profile_search(LiveLike(ds), table, i=int(traj["i"]), n=5, seed=g,
+                                stop_indices=stop)
+        assert [s.config_index for s in tr.steps] == want[r]
+        n = len(want[r])
+        drawn = n - ((n - 1) // 6 + 1)
+        ref = np.random.default_rng(seeds[r])
+        ref.integers(0, len(ds.space))
+        ref.random(drawn)
+        assert g.bit_generator.state == ref.bit_generator.state
+
+
 def test_large_space_properties():
     """GEMM-full (205,216 configurations): global-scratch path; cadence, no
     redraw, later-ties-win argmin, and identical results for any rep split."""

@@ -101,3 +101,37 @@ def test_model_program_flattening():
                            else prog.node_right[node])
             v = prog.node_value[node]
             assert (v if v > 0.0 else 0.0) == want[i, c]
+
+
+ORDER = os.path.join(GOLDEN, "order")
+
+
+@pytest.mark.parametrize("family", ["tree", "regression"])
+def test_training_follows_measurement_file_order(family, tmp_path, caplog):
+    """A measurements.csv whose rows are not sorted by config_index trains the
+    reference's models (make_order_golden.py): rows are used in file order,
+    as the reference's Dataset.records are (models.py:160-171, 237)."""
+    import json
+    from paper_2102_05297_b200 import formats, models
+    caplog.set_level(logging.ERROR)
+    ds = formats.load_dataset_dir(os.path.join(ORDER, "coulomb_shuffled"))
+    assert ds.record_order[:5].tolist() != [0, 1, 2, 3, 4]
+    ms = models.train_model_set(ds, family=family, seed=0)
+    out = tmp_path / "m.json"
+    models.save_model_set(ms, out)
+    assert filecmp.cmp(out, os.path.join(ORDER, f"coulomb_shuffled_{family}.json"),
+                       shallow=False)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("family", ["tree", "regression"])
+def test_counter_errors_follow_measurement_file_order(family):
+    """counter_prediction_errors (harness.py:268-289) averages over records in
+    file order; the GPU prediction table reproduces the reference's values."""
+    import json
+    from paper_2102_05297_b200 import formats, harness, models
+    ds = formats.load_dataset_dir(os.path.join(ORDER, "coulomb_shuffled"))
+    ms = models.load_model_set(os.path.join(ORDER, f"coulomb_shuffled_{family}.json"))
+    want = json.load(open(os.path.join(ORDER, "coulomb_shuffled_errors.json")))[family]
+    got = harness.counter_prediction_errors(ms, ds)
+    assert {k: [repr(a), repr(b)] for k, (a, b) in got.items()} == want
