@@ -112,6 +112,14 @@ def dist_env():
 
 
 DATASET = os.path.join(ROOT, "datasets", "transpose-b200")
+DATA = "B200-measured replay dataset (datasets/transpose-b200)"
+# the workload, identical in both arms' lines
+CONFIG = {"workload": "transpose tuning space (1,784 configs, 8 params) replay of its "
+                      "exhaustive B200 sweep; profile searcher, exact model, throughput mode "
+                      "(stop_indices = {})",
+          "dataset": "datasets/transpose-b200", "repetitions_per_gpu": REPS,
+          "outer_iterations": OUTER, "inner_steps": INNER, "seed": SEED,
+          "l2": "GPU arm: 256 MiB buffer written between timed steps (table 271 KB)"}
 
 
 def load_dataset():
@@ -168,31 +176,78 @@ def cpu_baseline(reps: int, cores: int):
     return scored / wall, scored, wall
 
 
+# ------------------------------------------------------- reference arm
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+_REF = {}
+
+
+def _ref_init():
+    """Worker: the unmodified reference package (baseline/_ref, installed from
+    /root/reference/pkg) loads the dataset with its own loader and builds its
+    own PredictionTable, as harness._run_repetitions does per worker."""
+    sys.path.insert(0, REF_DIR)
+    from countertune import models, search, space
+    ds = space.load_dataset_dir(DATASET)
+    _REF["src"] = search.DatasetReplaySource(ds)
+    _REF["table"] = search.PredictionTable.from_model_set(models.ExactModelSet(ds), ds.space)
+    _REF["n"] = len(ds.space)
+
+
+def _ref_chunk(reps):
+    """run_profile_search (the reference's public API, stock code path) over
+    the given repetitions in throughput mode; configurations scored = the
+    unexplored pool at each scoring call (search.py:380-385)."""
+    from countertune import search
+    seeds = np.random.SeedSequence(SEED).spawn(REPS)
+    n = _REF["n"]
+    scored = 0
+    for r in reps:
+        tr = search.run_profile_search(_REF["src"], _REF["table"], i=OUTER, n=INNER,
+                                       seed=seeds[r], stop_indices=frozenset())
+        idx = [s.config_index for s in tr.steps]
+        for k in range(OUTER):
+            first = k * (INNER + 1) + 1          # steps recorded when iteration k scores
+            if first > len(idx):
+                break
+            scored += n - len(set(idx[:first]))
+    return scored
+
+
 def run_reference(args):
+    """The reference's own CPU implementation of the path, on all host cores
+    (worker processes with strided repetition chunks, as its harness fans
+    out with COUNTERTUNE_WORKERS), same workload, metric and unit."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    if not os.path.isdir(os.path.join(REF_DIR, "countertune")):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "baseline/_ref holds no countertune install"}), flush=True)
+        return
+    from concurrent.futures import ProcessPoolExecutor
     cores = os.cpu_count() or 1
-    sample = max(cores, min(REPS, 64 * cores))
+    sample = min(REPS, 32 * cores)               # repetitions per step (bounded CPU time)
+    chunks = [list(range(k, sample, cores)) for k in range(cores)]
     vals = []
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_baseline(cores, cores)
-    for _ in range(args.steps):
-        v, scored, wall = cpu_baseline(sample, cores)
-        vals.append((v, scored, wall))
+    with ProcessPoolExecutor(max_workers=cores, initializer=_ref_init) as pool:
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            scored = sum(pool.map(_ref_chunk, chunks))
+            wall = time.perf_counter() - t0
+            if k >= args.warmup:
+                vals.append((scored / wall, scored, wall))
     value = float(np.median([v for v, _, _ in vals]))
     ms = float(np.median([w for _, _, w in vals])) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "B200-measured replay dataset (datasets/transpose-b200)",
-        "config": {"workload": "transpose space (1,784 configs) replay, profile searcher, "
-                               f"exact model, i={OUTER}, n={INNER}, throughput mode",
-                   "repetitions_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sample} of the {REPS} repetitions per step, "
-                                   f"{cores} worker processes (oracle/countertune_oracle.py)"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": dict(CONFIG),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{sample} of the {REPS} repetitions per step "
+                                   f"({vals[0][1]} configs scored), countertune.search."
+                                   f"run_profile_search from baseline/_ref in {cores} worker "
+                                   f"processes"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -326,16 +381,24 @@ def run_ours(args):
         from paper_2102_05297_b200 import ExperimentSpec, pair_with_baseline
         _, sspec = workload(stop=True)
         sspec.outer_iterations = None
+        # simulated wall-s with the MEASURED profiling overhead of this space
+        # (not the reference's invented 3.0)
+        with open(os.path.join(DATASET, "profiling_overhead.json")) as fh:
+            ovh = json.load(fh)
+        sspec.profiling_overhead = float(ovh["profiling_overhead"])
         prof = harness.simulate(sspec, devices=[device])
         rspec = ExperimentSpec(dataset=ds, searcher="random", name="random-search",
-                               repetitions=REPS, seed=SEED)
+                               repetitions=REPS, seed=SEED,
+                               profiling_overhead=sspec.profiling_overhead)
         rnd = harness.simulate(rspec, devices=[device])
         pair_with_baseline(prof, rnd)
         steps_info = {"profile_mean_steps": prof.mean_steps, "random_mean_steps": rnd.mean_steps,
                       "improvement": prof.improvement,
                       "profile_mean_sim_wall_s": prof.mean_time_seconds,
                       "random_mean_sim_wall_s": rnd.mean_time_seconds,
-                      "profile_censored": prof.censored, "uncertified_draws": prof.uncertified_draws}
+                      "profile_censored": prof.censored, "uncertified_draws": prof.uncertified_draws,
+                      "profiling_overhead": sspec.profiling_overhead,
+                      "profiling_overhead_source": ovh["source"]}
     except Exception as exc:  # report, never hide
         steps_info = {"error": repr(exc)}
 
@@ -352,14 +415,9 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_launch * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "B200-measured replay dataset (datasets/transpose-b200)",
-        "config": {"workload": "transpose tuning space (1,784 configs, 8 params) replay of its "
-                               "exhaustive B200 sweep; profile searcher, exact model, "
-                               "throughput mode",
-                   "repetitions_per_gpu": REPS, "outer_iterations": OUTER, "inner_steps": INNER,
-                   "seed": SEED, "configs_scored_per_step_per_gpu": configs_per_step,
-                   "l2": "256 MiB buffer written between timed steps (table 271 KB)",
-                   "parallelism": f"reps sharded over {world} GPU(s)"},
+        "data": DATA, "config": dict(CONFIG),
+        "configs_scored_per_step_per_gpu": configs_per_step,
+        "parallelism": f"reps sharded over {world} GPU(s)",
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "api": "harness.simulate" if world == 1 else "dist.simulate_distributed",

@@ -10,8 +10,9 @@ CPU fallback.
 from .counters import ArchProfile, canonicalize
 from .errors import (AnalysisError, CounterTuneError, ParameterMismatchError,
                      SpaceExhaustedError)
-from .harness import (ConvergenceReport, ExperimentSpec, pair_with_baseline, report,
-                      simulate)
+from .harness import (ConvergenceReport, CrossEvalReport, ExperimentSpec,
+                      counter_prediction_errors, cross_evaluate, pair_with_baseline, report,
+                      simulate, write_counter_errors)
 from .search import (DatasetReplaySource, ExactModelSet, Measurement, PredictionTable,
                      ProfileSearcher, ScoreVector, SearchTrace, SubprocessMeasurementSource, TraceStep,
                      normalize_scores, run_profile_search, run_random_search,

@@ -187,26 +187,7 @@ __global__ void k_score_single(const ScoreSingleArgs a) {
 }
 
 // Euclidean parameter distance to the profile (search.py:134-136) as an
-// order-preserving key; explored -> +inf.  numpy evaluates
-// sqrt(add.reduce(d*d, axis=1)) with its pairwise summation over the row
-// (DOUBLE_pairwise_sum: sequential below 8 terms, else 8 accumulators);
-// rows here are at most 64 terms, below the 128-term recursion block.
-__device__ __forceinline__ double np_row_sum(const double* a, int n) {
-    if (n < 8) {
-        double r = -0.0;
-        for (int i = 0; i < n; ++i) r = add(r, a[i]);
-        return r;
-    }
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-        for (int j = 0; j < 8; ++j) r[j] = add(r[j], a[i + j]);
-    double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
-    for (; i < n; ++i) res = add(res, a[i]);
-    return res;
-}
-
+// order-preserving key; explored -> +inf (np_row_sum: ct_hd.cuh).
 __global__ void k_topk_keys(const double* assign, int32_t P, int64_t n, int64_t profile,
                             const uint8_t* explored, unsigned long long* keys, int32_t* vals) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -582,9 +563,9 @@ int ensure_results(ct_ctx* ctx, int64_t reps, int64_t max_steps) {
     return CT_OK;
 }
 
-template <int NT, bool SMEM, bool PRE>
+template <int NT, bool SMEM, bool PRE, bool TOPK = false>
 int launch_profile_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
-    auto kern = k_profile_search<NT, SMEM, PRE>;
+    auto kern = k_profile_search<NT, SMEM, PRE, TOPK>;
     if (smem > 48 * 1024)
         CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -630,6 +611,17 @@ int launch_profile_ws(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int
 // the drawn row scanned by the drawing warp (CT_SEARCH_PRE=0)
 template <int NT>
 int launch_profile(ct_ctx* ctx, SearchArgs& a, bool pre, bool in_smem, size_t smem, int n_reps) {
+    if (a.topk >= 0) {   // top-K builds exist for 128-512 threads (the dispatcher ensures it)
+        if constexpr (NT >= 128) {
+            if (pre)
+                return in_smem ? launch_profile_t<NT, true, true, true>(ctx, a, smem, n_reps)
+                               : launch_profile_t<NT, false, true, true>(ctx, a, smem, n_reps);
+            return in_smem ? launch_profile_t<NT, true, false, true>(ctx, a, smem, n_reps)
+                           : launch_profile_t<NT, false, false, true>(ctx, a, smem, n_reps);
+        } else {
+            return fail(CT_ERR_UNSUPPORTED, "score_top_k needs >= 128 threads per repetition");
+        }
+    }
     if (pre)
         return in_smem ? launch_profile_t<NT, true, true>(ctx, a, smem, n_reps)
                        : launch_profile_t<NT, false, true>(ctx, a, smem, n_reps);
@@ -1011,8 +1003,8 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
                                       std::to_string(prm->inner_steps));
     if (!(prm->inst_reaction > 0.0 && prm->inst_reaction < 1.0))
         return fail(CT_ERR_VALUE, "inst_reaction must lie in (0, 1)");
-    if (prm->score_top_k >= 0)
-        return fail(CT_ERR_UNSUPPORTED, "score_top_k is not yet supported by the batched kernel");
+    if (prm->score_top_k >= 0 && (!ctx->assign.p || ctx->assign_n != ctx->n))
+        return fail(CT_ERR_STATE, "score_top_k needs the space assignments (ct_space_upload)");
     if (prm->use_stop && !ctx->has_stop) return fail(CT_ERR_STATE, "no stop mask uploaded");
     if (n_reps < 0) return fail(CT_ERR_VALUE, "n_reps must be >= 0");
     for (int k = 0; k < CT_N_DELTA; ++k)
@@ -1040,6 +1032,9 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     a.nrows = (int32_t)((n + 31) / 32);
     a.nwords = (n + 31) / 32;
     if (const char* env = std::getenv("CT_SEARCH_FORCE_SEQUENTIAL")) a.force_sequential = std::atoi(env);
+    a.topk = prm->score_top_k >= 0 ? prm->score_top_k : -1;
+    a.assign = a.topk >= 0 ? ctx->assign.p : nullptr;
+    a.n_params = a.topk >= 0 ? ctx->n_params : 0;
     a.step_index = ctx->step_index.p; a.step_profiled = ctx->step_profiled.p;
     a.max_steps = max_steps; a.n_steps = ctx->n_steps.p; a.status = ctx->status.p;
     a.rep_error = ctx->rep_error.p; a.stats = ctx->stats.p;
@@ -1049,11 +1044,14 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     // idle warps at the CTA barrier); CT_SEARCH_NT overrides (benchmarking)
     int nt = n <= 8192 ? 128 : (n <= 65536 ? 256 : 512);
     if (const char* env = std::getenv("CT_SEARCH_NT")) nt = std::atoi(env);
+    if (a.topk >= 0 && nt < 128) nt = 128;
     // row totals + explored bits always in shared memory; the weights too
     // when that still lets all repetitions be resident at once (one wave),
     // otherwise a per-CTA slice of global scratch (L2-resident)
     const size_t budget = 200 * 1024;
-    const size_t head_b = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+    // (+ the top-K exclusion bits and radix-select scratch when top-K is on)
+    const size_t head_b = ((16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15)
+                          + (a.topk >= 0 ? topk_bytes(a.nwords) : 0);
     // in-row prefixes stored by the weight pass (PRE) only pay off when the
     // rows are few (the drawing warp then rescans nothing); otherwise the
     // weight pass keeps just the row totals and the draw scans the drawn row
@@ -1071,7 +1069,7 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     // warp-specialised two-repetition kernel (CT_SEARCH_WS = parallel warps)
     int ws = 0;
     if (const char* env = std::getenv("CT_SEARCH_WS")) ws = std::atoi(env);
-    if (ws > 0 && 2 * head_b <= budget) {
+    if (ws > 0 && 2 * head_b <= budget && a.topk < 0) {   // the WS kernel has no top-K phase
         // two slots per CTA: weights in shared memory when both fit
         const int64_t ctas_per_sm = std::max<int64_t>(1, (want_per_sm + 1) / 2);
         const size_t cap2 = std::min<size_t>(

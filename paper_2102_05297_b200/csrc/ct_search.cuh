@@ -82,6 +82,11 @@ struct SearchArgs {
     int32_t nrows;
     int64_t nwords;
     int32_t force_sequential;    // test hook: decide every draw sequentially
+    // score_top_k (search.py:133-140): < 0 is None; assign is the space's
+    // n x n_params assignment matrix (row-major), read for the distances
+    int64_t topk;
+    const double* assign;
+    int32_t n_params;
     // storage: weights (8 B each, nrows * 32) in shared memory or a per-CTA
     // slice of scratch_w
     double* scratch_w;
@@ -391,6 +396,8 @@ __device__ __forceinline__ void profile_step(const SearchArgs& a, RepState& rs, 
             else if (rs.n_expl >= N) { rs.st = CT_STATUS_EXHAUSTED; ctl.done = 1; }
             else {
                 unsigned long long pool = (unsigned long long)(N - rs.n_expl);
+                // top-K scores the K nearest unexplored configurations only
+                if (a.topk >= 0 && (unsigned long long)a.topk < pool) pool = (unsigned long long)a.topk;
                 rs.scored += pool; ++rs.outers;
                 rs.abytes += pool * (8ull * (unsigned long long)na + 16ull);
             }
@@ -463,6 +470,7 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
     CT_SUB_START();
     // every pool configuration has a weight in [1e-4, 256] unless bad
     int positive = (int)(N - rs.n_expl), bad = 0;
+    if (a.topk >= 0 && a.topk < positive) positive = (int)a.topk;   // the top-K pool
 #pragma unroll
     for (int i = 0; i < NW; ++i) bad |= ctl.red_bad[i];
     const int cpl = (a.nrows + 31) >> 5;
@@ -635,10 +643,134 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
 }
 
 // ---------------------------------------------------------------------------
+// score_top_k (search.py:133-140): only the K unexplored configurations
+// nearest to the profile in Euclidean parameter distance are scored, ties in
+// distance taken in index order (np.argsort(kind="stable")).  The CTA
+// writes each configuration's distance as an order-preserving 64-bit key
+// (the float64 bits; explored -> all ones) over its weight slots, finds the
+// K-th smallest key with an 8-pass radix select (8-bit digits, shared-memory
+// histograms), and builds an exclusion bitmask: explored, farther than the
+// K-th key, or equal to it beyond the K - (number nearer) lowest indices.
+// Eq. 16 / Eq. 17 then read that mask in place of the explored bits, so the
+// pool (scoreable & ~explored) and its extrema are the reference's.  The
+// weights overwrite the keys afterwards.
+__host__ __device__ constexpr size_t topk_bytes(int64_t nwords) {
+    return ((4 * (size_t)nwords + 15) & ~(size_t)15) + 256 * 4 + 32;
+}
+
+template <int NT>
+__device__ __forceinline__ void topk_phase(const SearchArgs& a, int64_t cp, int64_t K,
+                                           const uint32_t* expl, uint32_t* excl, uint32_t* hist,
+                                           unsigned long long* tkv, double* w, int tid) {
+    constexpr int NW = NT / 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int64_t N = a.n;
+    const int P = a.n_params < 64 ? a.n_params : 64;
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(w);
+    const double* prof = a.assign + (size_t)cp * a.n_params;
+    for (int64_t e = tid; e < N; e += NT) {
+        unsigned long long k = ~0ull;
+        if (!bit_get(expl, e)) {
+            // np_row_sum (ct_hd.cuh) of the squared differences, streamed:
+            // the eight pairwise accumulators stay in registers
+            const double* row = a.assign + (size_t)e * a.n_params;
+            auto sq = [&](int j) {
+                const double d = sub(__ldg(row + j), __ldg(prof + j));
+                return mul(d, d);
+            };
+            double res;
+            if (P < 8) {
+                res = -0.0;
+                for (int j = 0; j < P; ++j) res = add(res, sq(j));
+            } else {
+                double r[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) r[j] = sq(j);
+                int i = 8;
+                for (; i < P - (P % 8); i += 8) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) r[j] = add(r[j], sq(i + j));
+                }
+                res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+                for (; i < P; ++i) res = add(res, sq(i));
+            }
+            k = (unsigned long long)dbits(dsqrt(res));   // >= 0: bits order as values
+        }
+        key[e] = k;
+    }
+    unsigned long long prefix = 0, mask = 0;
+    unsigned long long krem = (unsigned long long)K;      // rank wanted among the matching keys
+    unsigned long long cnt_eq = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int i = tid; i < 256; i += NT) hist[i] = 0u;
+        __syncthreads();
+        for (int64_t e = tid; e < N; e += NT) {
+            const unsigned long long k = key[e];
+            if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            unsigned c[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { c[j] = hist[8 * lane + j]; sum += c[j]; }
+            unsigned incl = sum;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned v = __shfl_up_sync(FULL, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const int L = __ffs(__ballot_sync(FULL, incl >= krem)) - 1;   // K <= pool: exists
+            if (lane == L) {
+                unsigned long long cum = incl - sum;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (cum + c[j] >= krem) {
+                        tkv[0] = prefix | ((unsigned long long)(8 * lane + j) << shift);
+                        tkv[1] = krem - cum;
+                        tkv[2] = c[j];
+                        break;
+                    }
+                    cum += c[j];
+                }
+            }
+        }
+        __syncthreads();
+        prefix = tkv[0];
+        krem = tkv[1];
+        cnt_eq = tkv[2];
+        mask |= 255ull << shift;
+    }
+    // prefix is the K-th smallest key; krem of the cnt_eq keys equal to it
+    // are in (the lowest indices)
+    const bool all_eq = cnt_eq == krem;
+    for (int64_t t = warp; t < a.nwords; t += NW) {
+        const int64_t e = 32 * t + lane;
+        const unsigned long long k = e < N ? key[e] : ~0ull;
+        const unsigned word = __ballot_sync(FULL, k > prefix || (k == prefix && !all_eq));
+        if (lane == 0) excl[t] = word;
+    }
+    __syncthreads();
+    if (!all_eq && warp == 0) {
+        unsigned long long carry = 0;
+        for (int64_t t = 0; t < a.nwords && carry < krem; ++t) {
+            const int64_t e = 32 * t + lane;
+            const bool eq = e < N && key[e] == prefix;
+            const unsigned bal = __ballot_sync(FULL, eq);
+            if (!bal) continue;
+            const unsigned long long rank = carry + __popc(bal & ((1u << lane) - 1u));
+            const unsigned in = __ballot_sync(FULL, eq && rank < krem);
+            if (lane == 0) excl[t] &= ~in;
+            carry += __popc(bal);
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
 // k_profile_search: one CTA runs one repetition end to end (then the next one
 // of its persistent slice); the serial phases run on warp 0 while the other
 // warps wait at the CTA barrier.
-template <int NT, bool SMEM, bool PRE>
+template <int NT, bool SMEM, bool PRE, bool TOPK>
 __global__ void __launch_bounds__(NT, (NT <= 64) ? 8 : ((NT == 128) ? 7 : (896 / NT)))
 k_profile_search(const SearchArgs a) {
     constexpr int NW = NT / 32;
@@ -653,13 +785,18 @@ k_profile_search(const SearchArgs a) {
     if (tid == 0) Pcg64::jump_tables(jA, jC, 32);
     load_seed_words(a.seed, seed_sh);
 
-    // dynamic shared memory: row totals | explored bits | [weights | in-row prefixes]
+    // dynamic shared memory: row totals | explored bits | [top-K: exclusion
+    // bits | radix histogram | select state] | [weights | in-row prefixes]
     double* row_tot = reinterpret_cast<double*>(smem);
     uint32_t* expl = reinterpret_cast<uint32_t*>(smem + 16 * (size_t)a.nrows);
+    const size_t head = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+    const size_t tk_b = TOPK ? topk_bytes(a.nwords) : 0;
+    uint32_t* excl_k = reinterpret_cast<uint32_t*>(smem + head);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + head + ((4 * (size_t)a.nwords + 15) & ~(size_t)15));
+    unsigned long long* tkv = reinterpret_cast<unsigned long long*>(hist + 256);
     double* w;
     if (SMEM) {
-        const size_t off = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
-        w = reinterpret_cast<double*>(smem + off);
+        w = reinterpret_cast<double*>(smem + head + tk_b);
     } else {
         w = a.scratch_w + (size_t)blockIdx.x * 64 * (size_t)a.nrows;
     }
@@ -688,10 +825,22 @@ k_profile_search(const SearchArgs a) {
         CT_CLK(clk_p1);
         for (int it = 0; it < a.outer; ++it) {
             if (ctl.done) break;
-            score_phase<NT>(a, ctl, expl, w, tid);
+            const uint32_t* excl = expl;     // configurations outside the pool
+            if constexpr (TOPK) {
+                if (a.topk < a.n - rs.n_expl) {
+                    if (a.topk == 0) {
+                        // an empty pool: normalize_scores raises (search.py:155)
+                        if (tid == 0) { rs.st = CT_STATUS_ERROR; rs.err = -3; }
+                        break;
+                    }
+                    topk_phase<NT>(a, rs.c_prof, a.topk, expl, excl_k, hist, tkv, w, tid);
+                    excl = excl_k;
+                }
+            }
+            score_phase<NT>(a, ctl, excl, w, tid);
             __syncthreads();
             CT_CLK(clk_score);
-            weight_phase<PRE>(a, ctl, expl, w, pre, row_tot, warp);
+            weight_phase<PRE>(a, ctl, excl, w, pre, row_tot, warp);
             __syncthreads();
             CT_CLK(clk_weight);
             if (warp == 0) {

@@ -17,11 +17,12 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _native
+from . import counters as cc
 from .counters import GLOBAL_THREADS
 from .errors import AnalysisError, CounterTuneError
 from .search import (DEFAULT_INST_REACTION, PredictionTable, _as_table, rep_error,
                      search_params)
-from .space import missing_required, replay_arrays, well_performing_mask
+from .space import assignments_of, missing_required, replay_arrays, well_performing_mask
 
 WORKERS_ENV = "COUNTERTUNE_WORKERS"
 SEARCHER_PROFILE = "profile"
@@ -167,12 +168,16 @@ def prepare_device(ctx: "_native.Context", spec: ExperimentSpec, table=None):
             raise AnalysisError(f"counter map is missing {', '.join(missing)}")
         if table is None:
             table = _as_table(spec.model, ds.space)
-        ctx.upload_table(table.matrix)
+        ctx.upload_table(table.matrix, key=table.matrix)
         if spec.score_top_k is not None:
-            raise CounterTuneError("score_top_k is not supported by the batched device search")
+            if spec.score_top_k < 0:
+                raise ValueError("score_top_k must be >= 0")
+            # top-K neighbourhoods (search.py:133-140, harness.py:155-158)
+            ctx.upload_space(assignments_of(ds.space), key=ds.space)
         params = search_params(table, ds.arch, i=spec.resolved_outer_iterations(),
                                n=spec.inner_steps, inst_reaction=spec.inst_reaction,
-                               literal_sign=spec.literal_sign, score_top_k=None, use_stop=True)
+                               literal_sign=spec.literal_sign, score_top_k=spec.score_top_k,
+                               use_stop=True)
         if not 0.0 < spec.inst_reaction < 1.0:
             raise ValueError(f"inst_reaction must lie in (0, 1), got {spec.inst_reaction}")
     return params, rt
@@ -465,6 +470,18 @@ def report(reports: List[ConvergenceReport], out_dir) -> List[str]:
     return written
 
 
+@dataclass
+class CrossEvalReport:
+    """Model portability check against a dataset it was not trained on
+    (harness.py:257-265)."""
+
+    model_label: str
+    dataset_label: str
+    counter_errors: Dict[str, Tuple[float, float]]
+    profile_report: ConvergenceReport
+    random_report: ConvergenceReport
+
+
 def counter_prediction_errors(models, dataset) -> Dict[str, Tuple[float, float]]:
     """Per-counter (MAE, RMSE) over all records (harness.py:268-289)."""
     table = PredictionTable.from_model_set(models, dataset.space)
@@ -488,3 +505,50 @@ def counter_prediction_errors(models, dataset) -> Dict[str, Tuple[float, float]]
         errors[abbr] = (float(np.mean(np.abs(err))), float(math.sqrt(np.mean(err * err))))
     del rt, th, hr, names
     return errors
+
+
+def cross_evaluate(models, dataset, repetitions: int = DEFAULT_REPETITIONS,
+                   inner_steps: int = 5, outer_iterations: Optional[int] = None,
+                   seed: int = 0, slack: float = 1.1,
+                   profiling_overhead: float = DEFAULT_PROFILING_OVERHEAD,
+                   inst_reaction: float = DEFAULT_INST_REACTION,
+                   devices: Optional[Sequence[int]] = None) -> CrossEvalReport:
+    """Judge a foreign model on this dataset (harness.py:292-323): its
+    per-counter prediction errors over every record, and the profile searcher
+    it drives against the uniform-random baseline with the same seeds.
+
+    The model's prediction table is evaluated on the GPU (ct_model_predict)
+    and both searchers run as batched device launches (simulate); the
+    report is the reference's, field for field."""
+    errors = counter_prediction_errors(models, dataset)
+    profile_spec = ExperimentSpec(dataset=dataset, searcher=SEARCHER_PROFILE, model=models,
+                                  name="profile-foreign-model", repetitions=repetitions,
+                                  inner_steps=inner_steps, outer_iterations=outer_iterations,
+                                  seed=seed, slack=slack,
+                                  profiling_overhead=profiling_overhead,
+                                  inst_reaction=inst_reaction)
+    random_spec = ExperimentSpec(dataset=dataset, searcher=SEARCHER_RANDOM,
+                                 name="random-baseline", repetitions=repetitions,
+                                 seed=seed, slack=slack,
+                                 profiling_overhead=profiling_overhead)
+    profile_report = simulate(profile_spec, devices)
+    random_report = simulate(random_spec, devices)
+    pair_with_baseline(profile_report, random_report)
+    model_label = getattr(models, "source_arch", "?")
+    model_input = getattr(models, "source_input", "?")
+    return CrossEvalReport(model_label=f"{model_label}/{model_input}",
+                           dataset_label=f"{dataset.arch.name}/{dataset.input_label}",
+                           counter_errors=errors,
+                           profile_report=profile_report,
+                           random_report=random_report)
+
+
+def write_counter_errors(errors: Dict[str, Tuple[float, float]], path) -> None:
+    """counter_errors.csv, catalog order, repr floats (harness.py:391-398)."""
+    lines = ["counter,mae,rmse"]
+    for abbr in cc.ABBREVIATIONS:
+        if abbr in errors:
+            mae, rmse = errors[abbr]
+            lines.append(f"{abbr},{repr(mae)},{repr(rmse)}")
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("\n".join(lines) + "\n")

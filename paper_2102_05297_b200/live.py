@@ -96,6 +96,19 @@ class Benchmark:
     def extra_options(self) -> List[str]:
         return []
 
+    def valid(self, values: Dict[str, int]) -> bool:
+        """Whether the configuration can run on this input (a configuration
+        that does not tile the input is not part of the input's space)."""
+        return True
+
+    def restrict_space(self) -> None:
+        """Keep only the configurations valid for this input, in the space's
+        order (the KTT/CLTune constraint pass on the input sizes)."""
+        keep = [i for i in range(len(self.space)) if self.valid(self.values(i))]
+        if len(keep) < len(self.space):
+            self._space = spaces.TuningSpace.from_assignments(
+                self.space.parameters, self.space.assignments[keep])
+
     # per subclass -----------------------------------------------------------
     def host_inputs(self) -> Dict[str, np.ndarray]:
         raise NotImplementedError
@@ -303,9 +316,14 @@ class GemmBenchmark(Benchmark):
 
     def __init__(self, m: int = 2048, n: int = 2048, k: int = 2048, seed: int = 0):
         super().__init__(seed)
-        if m % 128 or n % 128 or k % 32:
-            raise ValueError("gemm sizes must be multiples of 128 (m, n) and 32 (k)")
+        if m % 16 or n % 16 or k % 16 or min(m, n, k) < 16:
+            raise ValueError("gemm sizes must be positive multiples of 16")
         self.m, self.n, self.k = m, n, k
+
+    def valid(self, v) -> bool:
+        # the kernel has no edge tiles (CLBlast's xgemm pads instead): the
+        # block tile must divide C and the k-slice must divide K
+        return self.m % v["MWG"] == 0 and self.n % v["NWG"] == 0 and self.k % v["KWG"] == 0
 
     def host_inputs(self):
         rng = np.random.default_rng(self.seed)

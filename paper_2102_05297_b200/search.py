@@ -354,6 +354,8 @@ def stop_mask_of(stop_indices, n) -> Optional[np.ndarray]:
 def rep_error(code: int, failing_index: int) -> Exception:
     if code == _native.CT_ERR_NO_RECORD:
         return CounterTuneError(f"dataset holds no measurement for configuration {failing_index}")
+    if code == _native.CT_ERR_EXHAUSTED:
+        return SpaceExhaustedError("no unexplored configurations to normalize")
     if code == _native.CT_ERR_NONFINITE:
         return CounterTuneError("selection weights are not finite (negative or NaN predictions)")
     return CounterTuneError(f"device search failed with status {code}")
@@ -435,17 +437,19 @@ def run_profile_search(source, models, *, i: int, n: int = DEFAULT_INNER_STEPS, 
     space = source.space
     table = _as_table(models, space)
     total = len(space)
-    if _is_replay(source) and _regenerable(seed) and score_top_k is None:
+    if score_top_k is not None and score_top_k < 0:
+        raise ValueError("score_top_k must be >= 0")
+    if _is_replay(source) and _regenerable(seed):
         return _profile_search_device(source, table, i=i, n=n, seed=seed,
                                       inst_reaction=inst_reaction, literal_sign=literal_sign,
-                                      stop_indices=stop_indices)
+                                      stop_indices=stop_indices, score_top_k=score_top_k)
     return _profile_search_host_driven(source, table, total, i=i, n=n, seed=seed,
                                        inst_reaction=inst_reaction, literal_sign=literal_sign,
                                        stop_indices=stop_indices, score_top_k=score_top_k)
 
 
 def _profile_search_device(source, table, *, i, n, seed, inst_reaction, literal_sign,
-                           stop_indices) -> SearchTrace:
+                           stop_indices, score_top_k=None) -> SearchTrace:
     ds = source.dataset
     N = len(source.space)
     rt, th, req, hr = replay_arrays(ds)
@@ -458,10 +462,12 @@ def _profile_search_device(source, table, *, i, n, seed, inst_reaction, literal_
     _check_inst_reaction(inst_reaction)
     stop = stop_mask_of(stop_indices, N)
     ctx = _ctx()
-    ctx.upload_table(table.matrix)
+    ctx.upload_table(table.matrix, key=table.matrix)
     ctx.upload_replay(rt, th, req, hr, stop)
+    if score_top_k is not None:
+        ctx.upload_space(assignments_of(source.space), key=source.space)
     params = search_params(table, source.arch, i=i, n=n, inst_reaction=inst_reaction,
-                           literal_sign=literal_sign, score_top_k=None,
+                           literal_sign=literal_sign, score_top_k=score_top_k,
                            use_stop=stop is not None)
     ctx.launch_profile(params, _native.SeedWords(seed, child_per_rep=False), 1)
     idx, prof, nst, status, err, _ = ctx.fetch(1)

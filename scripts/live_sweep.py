@@ -76,6 +76,8 @@ def main():
         k, v = kv.split("=")
         sizes[k] = float(v) if "." in v else int(v)
     bench = live.benchmark(args.bench, **sizes)
+    full_size = len(bench.space)
+    bench.restrict_space()      # configurations that do not tile this input are not in its space
     src = live.CudaMeasurementSource(bench, reps=args.reps)
     t0 = time.time()
     last = [t0]
@@ -135,7 +137,8 @@ def main():
     ach, peak, unit, frac = roofline(bench, float(rt[best]), pk)
     well = int((rt <= 1.1 * rt[best]).sum())
     summary = {
-        "bench": bench.name, "configs": len(ds.space), "measured": int(ds.has_record.sum()),
+        "bench": bench.name, "configs": len(ds.space), "space_before_input_constraints": full_size,
+        "measured": int(ds.has_record.sum()),
         "failures": len(res.failures), "failure_examples": dict(list(res.failures.items())[:3]),
         "compile_s": round(res.seconds_compile, 1), "measure_s": round(res.seconds_measure, 1),
         "profile_passes": src.profile_passes, "sizes": sizes or "paper defaults",

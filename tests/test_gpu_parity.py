@@ -276,6 +276,36 @@ def test_large_space_properties():
         assert idx2[r, :nst2[r]].tolist() == res.step_index[3 + r, :res.n_steps[3 + r]].tolist()
 
 
+def test_gemm_full_trajectories_match_reference_with_uncertified_draws():
+    """N = 205,216 (GEMM-full): 256 repetitions x 40 iterations x 5 draws
+    against the reference's own trajectories (make_gemmfull_golden.py).  At
+    this size the certificate rejects some draws, which the device re-decides
+    with the sequential cumsum: the run must contain such draws and still
+    match the reference everywhere."""
+    from paper_2102_05297_b200 import ExactModelSet, _native, spaces
+    from paper_2102_05297_b200.search import PredictionTable, search_params
+    from paper_2102_05297_b200.space import replay_arrays
+    traj = golden("traj_gemm_full.npz")
+    reps, i = int(traj["reps"]), int(traj["i"])
+    ds = spaces.gemm_full()
+    table = PredictionTable.from_model_set(ExactModelSet(ds), ds.space)
+    rt, th, req, hr = replay_arrays(ds)
+    ctx = _native.context(0)
+    ctx.upload_table(table.matrix)
+    ctx.upload_replay(rt, th, req, hr, np.zeros(len(ds.space), dtype=np.uint8))
+    params = search_params(table, ds.arch, i=i, n=5, inst_reaction=0.7, literal_sign=False,
+                           score_top_k=None, use_stop=False)
+    ctx.launch_profile(params, _native.SeedWords(42, child_per_rep=True), reps)
+    idx, prof, nst, status, err, stats = ctx.fetch(reps)
+    want = ragged(traj, "exact_nostop")
+    for r in range(reps):
+        got = idx[r, :nst[r]].tolist()
+        assert got == want[r], f"rep {r}: first divergence at " \
+            f"{next((k for k, (a, b) in enumerate(zip(got, want[r])) if a != b), min(len(got), len(want[r])))}"
+    print(f"gemm_full: {stats.draws} draws, {stats.uncertified} uncertified")
+    assert stats.uncertified > 0
+
+
 def test_inline_division_is_ddiv_rn():
     """dvd_fast (ct_hd.cuh) == __ddiv_rn bit for bit on 2^28 operand pairs."""
     from paper_2102_05297_b200 import _native

@@ -135,3 +135,19 @@ def test_counter_errors_follow_measurement_file_order(family):
     want = json.load(open(os.path.join(ORDER, "coulomb_shuffled_errors.json")))[family]
     got = harness.counter_prediction_errors(ms, ds)
     assert {k: [repr(a), repr(b)] for k, (a, b) in got.items()} == want
+
+
+@pytest.mark.parametrize("name,family", [("gemm", "regression"), ("conv", "regression"),
+                                         ("nbody", "regression"), ("nbody", "tree")])
+def test_b200_model_files_are_byte_identical_to_reference(name, family, tmp_path, caplog):
+    """Training on the B200-measured datasets gives the reference's model
+    files (make_b200_models_golden.py; the gemm / conv trees are pinned the
+    same way on the GPU box, tests/test_gpu_models.py)."""
+    from paper_2102_05297_b200 import formats, models
+    caplog.set_level(logging.ERROR)
+    ds = formats.load_dataset_dir(os.path.join(os.path.dirname(GOLDEN), "..", "datasets",
+                                               f"{name}-b200"))
+    ms = models.train_model_set(ds, family=family, seed=0)
+    out = tmp_path / "m.json"
+    models.save_model_set(ms, out)
+    assert filecmp.cmp(out, os.path.join(MODELS, f"b200_{name}_{family}.json"), shallow=False)
