@@ -261,6 +261,21 @@ int ct_aggregate_time(ct_ctx* ctx, int32_t time_reps, const double* grid, int32_
                       const double* sum_init, const double* sq_init,
                       double* sum_out, double* sq_out);
 
+/* ct_report: the whole report of the last launch (one experiment on one
+ * device) in one call and ONE stream synchronisation: the per-repetition
+ * n_steps / status / rep_error and the batch stats (as ct_fetch_results),
+ * max_len = the longest trajectory, the step-curve column sums (as
+ * ct_aggregate_steps; col_sum / col_sq hold max_steps of the launch, the
+ * first max_len are written), total_times (R), and the time curve over the
+ * first time_reps repetitions with its grid computed on the device as
+ * harness.py:207-213 does it (np.linspace of 100 points, or the single
+ * point t_start); grid / tc_sum / tc_sq hold 100, the first n_grid are
+ * written.  Replaces harness.simulate's aggregation (harness.py:187-244). */
+int ct_report(ct_ctx* ctx, double overhead, int32_t time_reps, int32_t* n_steps,
+              int32_t* status, int32_t* rep_error, ct_batch_stats* stats, int32_t* max_len,
+              double* col_sum, double* col_sq, double* total_times, int32_t* n_grid,
+              double* grid, double* tc_sum, double* tc_sq);
+
 #ifdef __cplusplus
 }
 #endif

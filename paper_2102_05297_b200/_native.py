@@ -122,6 +122,8 @@ SIGNATURES = {
     "ct_model_predict": (ctypes.c_int, [_vp, _P(ModelProgramC), _vp, _i64, _i32, _vp]),
     "ct_aggregate_steps": (ctypes.c_int, [_vp, _dbl, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ct_aggregate_time": (ctypes.c_int, [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
+    "ct_report": (ctypes.c_int, [_vp, _dbl, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                 _vp, _vp, _vp]),
 }
 
 _lib = None
@@ -364,6 +366,32 @@ class Context:
         check(library().ct_aggregate_time(self.handle, int(time_reps), ptr(g), g.size, ptr(s0),
                                           ptr(q0), ptr(out_s), ptr(out_q)))
         return out_s, out_q
+
+    def report(self, overhead: float, n_reps: int, time_reps: int):
+        """ct_report: everything harness.simulate aggregates, one sync."""
+        msv = ctypes.c_int64(0)
+        check(library().ct_result_max_steps(self.handle, ctypes.byref(msv)))
+        ms = msv.value
+        nst = np.empty(n_reps, dtype=np.int32)
+        status = np.empty(n_reps, dtype=np.int32)
+        err = np.empty(n_reps, dtype=np.int32)
+        stats = BatchStats()
+        max_len = ctypes.c_int32()
+        n_grid = ctypes.c_int32()
+        col_sum = np.empty(ms)
+        col_sq = np.empty(ms)
+        total = np.empty(n_reps)
+        grid = np.empty(100)
+        tcs = np.empty(100)
+        tcq = np.empty(100)
+        check(library().ct_report(self.handle, float(overhead), int(time_reps), ptr(nst),
+                                  ptr(status), ptr(err), ctypes.byref(stats),
+                                  ctypes.byref(max_len), ptr(col_sum), ptr(col_sq), ptr(total),
+                                  ctypes.byref(n_grid), ptr(grid), ptr(tcs), ptr(tcq)))
+        ml, ng = max_len.value, n_grid.value
+        return dict(n_steps=nst, status=status, rep_error=err, stats=stats, max_len=ml,
+                    col_sum=col_sum[:ml], col_sq=col_sq[:ml], total=total, grid=grid[:ng],
+                    tc_sum=tcs[:ng], tc_sq=tcq[:ng])
 
     def fetch_stats(self):
         stats = BatchStats()

@@ -99,8 +99,11 @@ struct ct_ctx {
     int64_t n = 0;
     int64_t ld = 0;          // padded column stride
     int32_t n_counters = 0;
-    uint64_t col_cert = 0;   // columns inside raw_term_cert's domain
-    uint64_t col_nz = 0;     // columns without an exact zero
+    // column flags on the device (the search kernel reads them): [0] columns
+    // inside raw_term_cert's domain, [1] columns without an exact zero
+    DevBuf<unsigned long long> col_flags;
+    DevBuf<double> table_rm;        // row-major upload staging
+    DevBuf<double> col_part;        // per-chunk column statistics
     // space assignments (row-major n x P)
     DevBuf<double> assign;
     int32_t n_params = 0;
@@ -130,7 +133,7 @@ struct ct_ctx {
     DevBuf<int32_t> val_a, val_b;
     DevBuf<unsigned char> cub_tmp;
     DevBuf<double> part_d;
-    PinnedStage stage_table, stage_replay;
+    PinnedStage stage_table, stage_replay, stage_report;
     DevBuf<int32_t> part_i;
     DevBuf<u128> tiles;
     DevBuf<long long> pick;
@@ -407,9 +410,12 @@ constexpr int AGG_COLS = 8, AGG_CHUNK = 256;
 __global__ void __launch_bounds__(AGG_CHUNK)
 k_agg_cols(const double* __restrict__ bsf, const int32_t* __restrict__ n_steps, int32_t reps,
            int64_t width, int32_t max_len, const double* __restrict__ sum0,
-           const double* __restrict__ sq0, double* __restrict__ sum, double* __restrict__ sq) {
+           const double* __restrict__ sq0, double* __restrict__ sum, double* __restrict__ sq,
+           const int32_t* __restrict__ max_len_dev = nullptr) {
     __shared__ double tile[AGG_CHUNK][AGG_COLS + 1];
+    if (max_len_dev) max_len = *max_len_dev;     // launched for the step capacity
     const int k0 = blockIdx.x * AGG_COLS;
+    if (k0 >= max_len) return;
     const int tid = threadIdx.x;
     const int kc = k0 + tid;
     double s = 0.0, q = 0.0;
@@ -445,10 +451,67 @@ k_agg_cols(const double* __restrict__ bsf, const int32_t* __restrict__ n_steps, 
     }
 }
 
+// The report's scalars computed on the device (harness.py:187-224): the
+// longest trajectory, the time axis' ends over the first time_reps
+// repetitions (max is exact in any order) and np.linspace's grid
+// (numpy 2.x: y = arange(num) * step + start, step = (stop - start) / (num - 1),
+// the last point = stop; a zero step goes through i / div * delta).
+constexpr int AGG_GRID = 100;    // TIME_GRID_POINTS (harness.py:46)
+struct AggMeta {
+    int32_t max_len, n_grid;
+    double t_start, t_end;
+    double grid[AGG_GRID];
+};
+
+__global__ void __launch_bounds__(1024)
+k_agg_meta(const int32_t* __restrict__ n_steps, const double* __restrict__ total,
+           const double* __restrict__ first, int32_t reps, int32_t time_reps,
+           AggMeta* __restrict__ meta) {
+    int mx = 0;
+    double ts = -INFINITY, te = -INFINITY;
+    for (int r = threadIdx.x; r < reps; r += blockDim.x) {
+        mx = max(mx, n_steps[r]);
+        if (r < time_reps) { ts = fmax(ts, first[r]); te = fmax(te, total[r]); }
+    }
+    __shared__ int smx[32];
+    __shared__ double sts[32], ste[32];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        ts = fmax(ts, __shfl_xor_sync(0xffffffffu, ts, d));
+        te = fmax(te, __shfl_xor_sync(0xffffffffu, te, d));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { smx[w] = mx; sts[w] = ts; ste[w] = te; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+            mx = max(mx, smx[k]); ts = fmax(ts, sts[k]); te = fmax(te, ste[k]);
+        }
+        meta->max_len = mx;
+        meta->t_start = ts;
+        meta->t_end = te;
+        if (te > ts) {
+            meta->n_grid = AGG_GRID;
+            const double delta = sub(te, ts), div = (double)(AGG_GRID - 1);
+            const double step = delta / div;
+            for (int i = 0; i < AGG_GRID; ++i) {
+                const double y = (step == 0.0) ? mul((double)i / div, delta) : mul((double)i, step);
+                meta->grid[i] = add(y, ts);
+            }
+            meta->grid[AGG_GRID - 1] = te;
+        } else {
+            meta->n_grid = 1;
+            meta->grid[0] = ts;
+        }
+    }
+}
+
 // One thread per (grid point, repetition): sampled best-so-far.
 __global__ void k_agg_sample(const double* bsf, const double* times, const int32_t* n_steps,
                              int32_t reps, int64_t width, const double* grid, int32_t n_grid,
-                             double* sampled) {
+                             double* sampled, const AggMeta* meta = nullptr) {
+    if (meta) { grid = meta->grid; n_grid = meta->n_grid; }
     const int64_t total = (int64_t)reps * n_grid;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -468,7 +531,9 @@ __global__ void k_agg_sample(const double* bsf, const double* times, const int32
 
 __global__ void k_agg_time_sums(const double* __restrict__ sampled, int32_t reps, int32_t n_grid,
                                 const double* __restrict__ sum0, const double* __restrict__ sq0,
-                                double* __restrict__ sum, double* __restrict__ sq) {
+                                double* __restrict__ sum, double* __restrict__ sq,
+                                const AggMeta* __restrict__ meta = nullptr) {
+    if (meta) n_grid = meta->n_grid;
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n_grid; g += gridDim.x * blockDim.x) {
         double s = sum0 ? sum0[g] : 0.0, q = sq0 ? sq0[g] : 0.0;
 #pragma unroll 8
@@ -482,35 +547,96 @@ __global__ void k_agg_time_sums(const double* __restrict__ sampled, int32_t reps
     }
 }
 
-// Per-column value range of a row-major n x c table -> bit j set when column
-// j is inside raw_term_cert's certified division domain.
-uint64_t certified_columns(const double* m, int64_t n, int32_t c) {
-    uint64_t cert = 0;
-    for (int32_t j = 0; j < c && j < 64; ++j) {
-        double vmin = INFINITY, vpos = INFINITY, vmax = -INFINITY;
-        bool finite = true;
-        for (int64_t i = 0; i < n; ++i) {
-            const double v = m[(size_t)i * c + j];
-            if (!(v == v) || std::isinf(v)) { finite = false; break; }
-            vmin = std::min(vmin, v);
-            vmax = std::max(vmax, v);
-            if (v > 0.0) vpos = std::min(vpos, v);
+// ---- prediction-table preparation on the device ----------------------
+// Row-major n x c (the reference's PredictionTable.matrix) -> column-major
+// with the stride padded to ld (zeros), through a shared-memory tile of 32
+// rows: the reads are the rows' contiguous bytes, the writes 32 consecutive
+// configurations of one column (256 B).
+constexpr int TT_ROWS = 32, TT_MAXC = 64;
+__global__ void __launch_bounds__(256)
+k_table_transpose(const double* __restrict__ rm, int64_t n, int32_t c, double* __restrict__ cm,
+                  int64_t ld) {
+    __shared__ double tile[TT_ROWS * (TT_MAXC + 1)];
+    const int per = TT_ROWS * c;
+    for (int64_t t = blockIdx.x; t * TT_ROWS < ld; t += gridDim.x) {
+        const int64_t r0 = t * TT_ROWS;
+        for (int k = threadIdx.x; k < per; k += blockDim.x) {
+            const int i = k / c, j = k - i * c;
+            tile[i * (TT_MAXC + 1) + j] = (r0 + i < n) ? rm[(size_t)r0 * c + k] : 0.0;
         }
-        if (vpos == INFINITY) vpos = 0.0;
-        if (finite && column_certified(vmin, vpos, vmax)) cert |= 1ull << j;
+        __syncthreads();
+        for (int k = threadIdx.x; k < per; k += blockDim.x) {
+            const int j = k / TT_ROWS, i = k - j * TT_ROWS;
+            cm[(size_t)j * ld + r0 + i] = tile[i * (TT_MAXC + 1) + j];
+        }
+        __syncthreads();
     }
-    return cert;
 }
 
-// bit j set when column j of a row-major n x c table holds no exact zero
-uint64_t nonzero_columns(const double* m, int64_t n, int32_t c) {
-    uint64_t nz = 0;
-    for (int32_t j = 0; j < c && j < 64; ++j) {
-        bool any_zero = false;
-        for (int64_t i = 0; i < n && !any_zero; ++i) any_zero = (m[(size_t)i * c + j] == 0.0);
-        if (!any_zero) nz |= 1ull << j;
+// Column statistics of the column-major table for the search kernel's fast
+// paths: block (g, j) reduces chunk g of column j to (min, max, smallest
+// positive, non-finite seen, zero seen); k_col_flags folds the chunks and
+// sets bit j of [certified, no-zero] (column_certified, ct_hd.cuh).  min /
+// max are exact in any order.
+struct ColPart { double vmin, vmax, vpos; int bad, zero; };
+
+__global__ void __launch_bounds__(256)
+k_col_stats(const double* __restrict__ cm, int64_t ld, int64_t n, int32_t chunks,
+            ColPart* __restrict__ part) {
+    const int j = blockIdx.y, g = blockIdx.x;
+    const int64_t per = (n + chunks - 1) / chunks;
+    const int64_t lo = g * per, hi = min(n, lo + per);
+    double vmin = INFINITY, vmax = -INFINITY, vpos = INFINITY;
+    int bad = 0, zero = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double v = cm[(size_t)j * ld + i];
+        if (!(v == v) || isinf(v)) { bad = 1; continue; }
+        vmin = fmin(vmin, v);
+        vmax = fmax(vmax, v);
+        if (v > 0.0) vpos = fmin(vpos, v);
+        zero |= (v == 0.0);
     }
-    return nz;
+    __shared__ ColPart red[8];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, d));
+        vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
+        vpos = fmin(vpos, __shfl_xor_sync(0xffffffffu, vpos, d));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+        zero |= __shfl_xor_sync(0xffffffffu, zero, d);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) red[w] = ColPart{vmin, vmax, vpos, bad, zero};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ColPart p = red[0];
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+            p.vmin = fmin(p.vmin, red[k].vmin); p.vmax = fmax(p.vmax, red[k].vmax);
+            p.vpos = fmin(p.vpos, red[k].vpos); p.bad |= red[k].bad; p.zero |= red[k].zero;
+        }
+        part[(size_t)j * chunks + g] = p;
+    }
+}
+
+__global__ void k_col_flags(const ColPart* __restrict__ part, int32_t chunks, int32_t c,
+                            unsigned long long* __restrict__ flags) {
+    __shared__ unsigned long long f[2];
+    if (threadIdx.x == 0) { f[0] = 0ull; f[1] = 0ull; }
+    __syncthreads();
+    const int j = threadIdx.x;
+    if (j < c && j < 64) {
+        ColPart p = part[(size_t)j * chunks];
+        for (int g = 1; g < chunks; ++g) {
+            const ColPart q = part[(size_t)j * chunks + g];
+            p.vmin = fmin(p.vmin, q.vmin); p.vmax = fmax(p.vmax, q.vmax);
+            p.vpos = fmin(p.vpos, q.vpos); p.bad |= q.bad; p.zero |= q.zero;
+        }
+        const double vpos = (p.vpos == INFINITY) ? 0.0 : p.vpos;
+        if (!p.bad && column_certified(p.vmin, vpos, p.vmax)) atomicOr(&f[0], 1ull << j);
+        if (!p.zero) atomicOr(&f[1], 1ull << j);   // (a non-finite value is not a zero)
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { flags[0] = f[0]; flags[1] = f[1]; }
 }
 
 int rows_for(int64_t n) {
@@ -520,9 +646,9 @@ int rows_for(int64_t n) {
     return std::max(2, rows);
 }
 
-int grid_for(int64_t n, int threads) {
+int grid_for(int64_t n, int threads, int sm_count) {
     int64_t g = (n + threads - 1) / threads;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sm_count * 16));
 }
 
 int check_ctx(ct_ctx* ctx) {
@@ -677,7 +803,7 @@ int ct_destroy(ct_ctx* ctx) {
     ctx->part_d.release(); ctx->part_i.release(); ctx->tiles.release(); ctx->pick.release();
     ctx->agg_bsf.release(); ctx->agg_times.release(); ctx->agg_vec.release();
     ctx->agg_sampled.release(); ctx->model_blob.release(); ctx->model_out.release();
-    ctx->stage_table.release(); ctx->stage_replay.release();
+    ctx->stage_table.release(); ctx->stage_replay.release(); ctx->stage_report.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     return CT_OK;
@@ -696,33 +822,47 @@ int ct_synchronize(ct_ctx* ctx) {
     return CT_OK;
 }
 
+// the search kernel's column flags of the resident column-major table
+static int table_flags(ct_ctx* ctx, int64_t n, int32_t c) {
+    cudaStream_t s = ctx->stream;
+    const int32_t chunks = (int32_t)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 64));
+    CT_CUDA(ctx->col_part.ensure(sizeof(ColPart) / 8 * (size_t)chunks * c));
+    CT_CUDA(ctx->col_flags.ensure(2));
+    k_col_stats<<<dim3(chunks, c), 256, 0, s>>>(ctx->table.p, ctx->ld, n, chunks,
+                                                reinterpret_cast<ColPart*>(ctx->col_part.p));
+    CT_CUDA(cudaGetLastError());
+    k_col_flags<<<1, 64, 0, s>>>(reinterpret_cast<const ColPart*>(ctx->col_part.p), chunks, c,
+                                  ctx->col_flags.p);
+    CT_CUDA(cudaGetLastError());
+    return CT_OK;
+}
+
 int ct_table_upload(ct_ctx* ctx, const double* matrix, int64_t n, int32_t c) {
     int rc = check_ctx(ctx); if (rc) return rc;
     if (!matrix || n < 1 || c < 1) return fail(CT_ERR_VALUE, "table needs n >= 1 and counters >= 1");
     if (n > INT32_MAX) return fail(CT_ERR_VALUE, "spaces above 2^31-1 configurations are not supported");
-    // transpose to column-major on the host (one pass over the borrowed matrix)
-    // columns padded with zeros to a multiple of 2048 configurations: the
-    // search kernel's unrolled loads (4 x up to 512 threads) never need a
-    // bounds test
+    if (c > TT_MAXC) return fail(CT_ERR_UNSUPPORTED, "tables of more than 64 counters are not supported");
+    // the borrowed row-major matrix goes to the device as it is (one
+    // contiguous copy through the pinned stage); the column-major layout with
+    // its stride padded to a multiple of 2048 configurations (the search
+    // kernel's unrolled loads never need a bounds test) and the column flags
+    // are made there
     const int64_t ld = (n + 2047) / 2048 * 2048;
-    CT_CUDA(ctx->stage_table.acquire(sizeof(double) * (size_t)ld * c));
-    double* colmajor = static_cast<double*>(ctx->stage_table.p);
-    for (int32_t j = 0; j < c; ++j) {
-        double* col = colmajor + (size_t)j * ld;
-        for (int64_t i = 0; i < n; ++i) col[i] = matrix[(size_t)i * c + j];
-        for (int64_t i = n; i < ld; ++i) col[i] = 0.0;
-    }
-    const uint64_t cert = certified_columns(matrix, n, c);
-    CT_CUDA(ctx->table.ensure((size_t)ld * c));
-    CT_CUDA(cudaMemcpyAsync(ctx->table.p, colmajor, sizeof(double) * ld * c,
-                            cudaMemcpyHostToDevice, ctx->stream));
+    const size_t bytes = sizeof(double) * (size_t)n * c;
+    CT_CUDA(ctx->stage_table.acquire(bytes));
+    std::memcpy(ctx->stage_table.p, matrix, bytes);
+    CT_CUDA(ctx->table_rm.ensure((size_t)n * c));
+    CT_CUDA(cudaMemcpyAsync(ctx->table_rm.p, ctx->stage_table.p, bytes, cudaMemcpyHostToDevice,
+                            ctx->stream));
     CT_CUDA(cudaEventRecord(ctx->stage_table.done, ctx->stream));
+    CT_CUDA(ctx->table.ensure((size_t)ld * c));
+    k_table_transpose<<<(int)std::min<int64_t>(ld / TT_ROWS, (int64_t)ctx->sm_count * 8), 256, 0,
+                        ctx->stream>>>(ctx->table_rm.p, n, c, ctx->table.p, ld);
+    CT_CUDA(cudaGetLastError());
     ctx->n = n;
     ctx->ld = ld;
     ctx->n_counters = c;
-    ctx->col_cert = cert;
-    ctx->col_nz = nonzero_columns(matrix, n, c);
-    return CT_OK;
+    return table_flags(ctx, n, c);
 }
 
 int ct_model_predict(ct_ctx* ctx, const ct_model_program* pg, const double* assign, int64_t n,
@@ -786,9 +926,7 @@ int ct_model_predict(ct_ctx* ctx, const ct_model_program* pg, const double* assi
     ctx->n = n;
     ctx->ld = ld;
     ctx->n_counters = pg->n_cols;
-    ctx->col_cert = certified_columns(dst, n, pg->n_cols);
-    ctx->col_nz = nonzero_columns(dst, n, pg->n_cols);
-    return CT_OK;
+    return table_flags(ctx, n, pg->n_cols);
 }
 
 int ct_space_upload(ct_ctx* ctx, const double* assign, int64_t n, int32_t p) {
@@ -870,7 +1008,7 @@ int ct_score(ct_ctx* ctx, int64_t profile, const int32_t* cols, const double* va
         CT_CUDA(ctx->key_a.ensure(n)); CT_CUDA(ctx->key_b.ensure(n));
         CT_CUDA(ctx->val_a.ensure(n)); CT_CUDA(ctx->val_b.ensure(n));
         CT_CUDA(ctx->mask_b.ensure(n));
-        k_topk_keys<<<grid_for(n, 256), 256, 0, s>>>(ctx->assign.p, ctx->n_params, n, profile,
+        k_topk_keys<<<grid_for(n, 256, ctx->sm_count), 256, 0, s>>>(ctx->assign.p, ctx->n_params, n, profile,
                                                       ctx->mask_a.p, ctx->key_a.p, ctx->val_a.p);
         size_t tmp = 0;
         CT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ctx->key_a.p, ctx->key_b.p,
@@ -880,7 +1018,7 @@ int ct_score(ct_ctx* ctx, int64_t profile, const int32_t* cols, const double* va
                                                 ctx->val_a.p, ctx->val_b.p, (int)n, 0, 64, s));
         CT_CUDA(cudaMemsetAsync(ctx->mask_b.p, 0, n, s));
         if (top_k > 0)
-            k_topk_mark<<<grid_for(top_k, 256), 256, 0, s>>>(ctx->val_b.p, top_k, ctx->mask_b.p, n);
+            k_topk_mark<<<grid_for(top_k, 256, ctx->sm_count), 256, 0, s>>>(ctx->val_b.p, top_k, ctx->mask_b.p, n);
     }
     ScoreSingleArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -888,7 +1026,7 @@ int ct_score(ct_ctx* ctx, int64_t profile, const int32_t* cols, const double* va
     for (int k = 0; k < n_delta; ++k) { a.cols[k] = cols[k]; a.vals[k] = vals[k]; }
     a.explored = ctx->mask_a.p; a.scoreable = topk ? ctx->mask_b.p : nullptr;
     a.literal_sign = literal_sign; a.raw = ctx->vec_a.p;
-    k_score_single<<<grid_for(n, 256), 256, 0, s>>>(a);
+    k_score_single<<<grid_for(n, 256, ctx->sm_count), 256, 0, s>>>(a);
     CT_CUDA(cudaGetLastError());
     CT_CUDA(cudaMemcpyAsync(raw_out, ctx->vec_a.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     if (topk && scoreable_out)
@@ -906,13 +1044,13 @@ int ct_normalize(ct_ctx* ctx, const double* raw, const uint8_t* pool, int64_t n,
     if (cnt == 0) return fail(CT_ERR_EXHAUSTED, "no unexplored configurations to normalize");
     cudaStream_t s = ctx->stream;
     CT_CUDA(ctx->vec_a.ensure(n)); CT_CUDA(ctx->vec_b.ensure(n)); CT_CUDA(ctx->mask_a.ensure(n));
-    int g = std::min(grid_for(n, 256), 512);
+    int g = std::min(grid_for(n, 256, ctx->sm_count), 512);
     CT_CUDA(ctx->part_d.ensure(2 * (size_t)g)); CT_CUDA(ctx->part_i.ensure(g));
     CT_CUDA(cudaMemcpyAsync(ctx->vec_a.p, raw, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     CT_CUDA(cudaMemcpyAsync(ctx->mask_a.p, pool, n, cudaMemcpyHostToDevice, s));
     k_minmax<<<g, 256, 0, s>>>(ctx->vec_a.p, ctx->mask_a.p, n, ctx->part_d.p, ctx->part_d.p + g,
                                ctx->part_i.p);
-    k_weights<<<grid_for(n, 256), 256, 0, s>>>(ctx->vec_a.p, ctx->mask_a.p, n, ctx->part_d.p,
+    k_weights<<<grid_for(n, 256, ctx->sm_count), 256, 0, s>>>(ctx->vec_a.p, ctx->mask_a.p, n, ctx->part_d.p,
                                                ctx->part_d.p + g, g, gamma, ctx->vec_b.p);
     CT_CUDA(cudaGetLastError());
     CT_CUDA(cudaMemcpyAsync(norm_out, ctx->vec_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
@@ -1026,8 +1164,7 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     a.inst_reaction = prm->inst_reaction; a.issue_sign = prm->issue_delta_sign; a.gamma = prm->gamma;
     a.literal_sign = prm->literal_sign; a.generation = prm->generation; a.cores = prm->cores;
     for (int k = 0; k < CT_N_DELTA; ++k) a.delta_col[k] = prm->delta_columns[k];
-    a.col_cert = ctx->col_cert;
-    a.col_nz = ctx->col_nz;
+    a.col_flags = ctx->col_flags.p;
     a.seed = seed_inline; a.n_reps = n_reps;
     a.nrows = (int32_t)((n + 31) / 32);
     a.nwords = (n + 31) / 32;
@@ -1164,7 +1301,7 @@ int ct_fetch_results(ct_ctx* ctx, int32_t* step_index, uint8_t* step_profiled, i
     if (r) {
         if ((step_index || step_profiled) && m) {
             const int64_t total = (int64_t)(r * m);
-            k_clear_tails<<<(int)std::min<int64_t>((total + 255) / 256, 4 * 148), 256, 0, s>>>(
+            k_clear_tails<<<(int)std::min<int64_t>((total + 255) / 256, 4 * (int64_t)ctx->sm_count), 256, 0, s>>>(
                 ctx->step_index.p, ctx->step_profiled.p, ctx->n_steps.p, ctx->status.p,
                 (int32_t)r, (int64_t)m);
             CT_CUDA(cudaGetLastError());
@@ -1212,7 +1349,7 @@ int ct_aggregate_steps(ct_ctx* ctx, double overhead, int32_t max_len, const doub
     double* d_sum = d_sq0 + max_len;
     double* d_sq = d_sum + max_len;
     if (R > 0) {
-        k_agg_rows<<<(int)std::min<int64_t>((R + 7) / 8, 8 * 148), 256, 0, s>>>(
+        k_agg_rows<<<(int)std::min<int64_t>((R + 7) / 8, 8 * (int64_t)ctx->sm_count), 256, 0, s>>>(
             ctx->step_index.p, ctx->step_profiled.p, ctx->n_steps.p, (int32_t)R, W, ctx->runtime.p,
             overhead, ctx->agg_bsf.p, ctx->agg_times.p, d_total, d_first);
         CT_CUDA(cudaGetLastError());
@@ -1255,7 +1392,7 @@ int ct_aggregate_time(ct_ctx* ctx, int32_t time_reps, const double* grid, int32_
     if (sq0) CT_CUDA(cudaMemcpyAsync(d_sq0, sq0, 8 * (size_t)n_grid, cudaMemcpyHostToDevice, s));
     if (R > 0) {
         const int64_t pairs = (int64_t)R * n_grid;
-        k_agg_sample<<<(int)std::min<int64_t>((pairs + 255) / 256, 2368), 256, 0, s>>>(
+        k_agg_sample<<<(int)std::min<int64_t>((pairs + 255) / 256, 16 * (int64_t)ctx->sm_count), 256, 0, s>>>(
             ctx->agg_bsf.p, ctx->agg_times.p, ctx->n_steps.p, R, W, d_grid, n_grid,
             ctx->agg_sampled.p);
         CT_CUDA(cudaGetLastError());
@@ -1267,6 +1404,91 @@ int ct_aggregate_time(ct_ctx* ctx, int32_t time_reps, const double* grid, int32_
     CT_CUDA(cudaMemcpyAsync(sum_out, d_sum, 8 * (size_t)n_grid, cudaMemcpyDeviceToHost, s));
     CT_CUDA(cudaMemcpyAsync(sq_out, d_sq, 8 * (size_t)n_grid, cudaMemcpyDeviceToHost, s));
     CT_CUDA(cudaStreamSynchronize(s));
+    return CT_OK;
+}
+
+int ct_report(ct_ctx* ctx, double overhead, int32_t time_reps, int32_t* n_steps,
+              int32_t* status, int32_t* rep_error, ct_batch_stats* stats, int32_t* max_len,
+              double* col_sum, double* col_sq, double* total_times, int32_t* n_grid,
+              double* grid, double* tc_sum, double* tc_sq) {
+    int rc = check_ctx(ctx); if (rc) return rc;
+    if (!ctx->res_valid) return fail(CT_ERR_STATE, "no batched search launched");
+    if (!ctx->runtime.p) return fail(CT_ERR_STATE, "no replay data uploaded");
+    if (!n_steps || !status || !rep_error || !stats || !max_len || !col_sum || !col_sq ||
+        !total_times || !n_grid || !grid || !tc_sum || !tc_sq)
+        return fail(CT_ERR_VALUE, "null report buffer");
+    const int64_t R = ctx->res_reps, W = ctx->res_max_steps;
+    if (R < 1) return fail(CT_ERR_VALUE, "the report needs at least one repetition");
+    const int32_t TR = (int32_t)std::min<int64_t>(std::max(time_reps, 1), R);
+    cudaStream_t s = ctx->stream;
+    CT_CUDA(ctx->agg_bsf.ensure((size_t)R * W));
+    CT_CUDA(ctx->agg_times.ensure((size_t)R * W));
+    // agg_vec: total[R] | first[R] | sum[W] | sq[W] | tc_sum[G] | tc_sq[G] | meta
+    const size_t meta_d = (sizeof(AggMeta) + 7) / 8;
+    CT_CUDA(ctx->agg_vec.ensure(2 * (size_t)R + 2 * (size_t)W + 2 * AGG_GRID + meta_d));
+    double* d_total = ctx->agg_vec.p;
+    double* d_first = d_total + R;
+    double* d_sum = d_first + R;
+    double* d_sq = d_sum + W;
+    double* d_tcs = d_sq + W;
+    double* d_tcq = d_tcs + AGG_GRID;
+    AggMeta* d_meta = reinterpret_cast<AggMeta*>(d_tcq + AGG_GRID);
+    CT_CUDA(ctx->agg_sampled.ensure((size_t)TR * AGG_GRID));
+    k_agg_rows<<<(int)std::min<int64_t>((R + 7) / 8, 8 * (int64_t)ctx->sm_count), 256, 0, s>>>(
+        ctx->step_index.p, ctx->step_profiled.p, ctx->n_steps.p, (int32_t)R, W, ctx->runtime.p,
+        overhead, ctx->agg_bsf.p, ctx->agg_times.p, d_total, d_first);
+    CT_CUDA(cudaGetLastError());
+    k_agg_meta<<<1, 1024, 0, s>>>(ctx->n_steps.p, d_total, d_first, (int32_t)R, TR, d_meta);
+    CT_CUDA(cudaGetLastError());
+    k_agg_cols<<<(int)((W + AGG_COLS - 1) / AGG_COLS), AGG_CHUNK, 0, s>>>(
+        ctx->agg_bsf.p, ctx->n_steps.p, (int32_t)R, W, (int32_t)W, nullptr, nullptr, d_sum, d_sq,
+        &d_meta->max_len);
+    CT_CUDA(cudaGetLastError());
+    const int64_t pairs = (int64_t)TR * AGG_GRID;
+    k_agg_sample<<<(int)std::min<int64_t>((pairs + 255) / 256, 16 * (int64_t)ctx->sm_count), 256, 0, s>>>(
+        ctx->agg_bsf.p, ctx->agg_times.p, ctx->n_steps.p, TR, W, nullptr, AGG_GRID,
+        ctx->agg_sampled.p, d_meta);
+    CT_CUDA(cudaGetLastError());
+    k_agg_time_sums<<<(AGG_GRID + 63) / 64, 64, 0, s>>>(ctx->agg_sampled.p, TR, AGG_GRID, nullptr,
+                                                        nullptr, d_tcs, d_tcq, d_meta);
+    CT_CUDA(cudaGetLastError());
+    // one page-locked landing area, several async copies, ONE synchronisation
+    const size_t b_i = 3 * 4 * (size_t)R, b_st = 5 * 8, b_v = 8 * (2 * (size_t)W + R + 2 * AGG_GRID);
+    const size_t b_all = ((b_i + 7) & ~(size_t)7) + b_st + b_v + sizeof(AggMeta);
+    CT_CUDA(ctx->stage_report.acquire(b_all));
+    unsigned char* h = static_cast<unsigned char*>(ctx->stage_report.p);
+    int32_t* h_i = reinterpret_cast<int32_t*>(h);
+    unsigned long long* h_st = reinterpret_cast<unsigned long long*>(h + ((b_i + 7) & ~(size_t)7));
+    double* h_v = reinterpret_cast<double*>(h_st + 5);
+    AggMeta* h_meta = reinterpret_cast<AggMeta*>(h_v + 2 * W + R + 2 * AGG_GRID);
+    CT_CUDA(cudaMemcpyAsync(h_i, ctx->n_steps.p, 4 * R, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaMemcpyAsync(h_i + R, ctx->status.p, 4 * R, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaMemcpyAsync(h_i + 2 * R, ctx->rep_error.p, 4 * R, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaMemcpyAsync(h_st, ctx->stats.p, b_st, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaMemcpyAsync(h_v, d_sum, 8 * 2 * (size_t)W, cudaMemcpyDeviceToHost, s));  // sum | sq
+    CT_CUDA(cudaMemcpyAsync(h_v + 2 * W, d_total, 8 * (size_t)R, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaMemcpyAsync(h_v + 2 * W + R, d_tcs, 8 * 2 * AGG_GRID, cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaMemcpyAsync(h_meta, d_meta, sizeof(AggMeta), cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaEventRecord(ctx->stage_report.done, s));
+    CT_CUDA(cudaEventSynchronize(ctx->stage_report.done));
+    std::memcpy(n_steps, h_i, 4 * R);
+    std::memcpy(status, h_i + R, 4 * R);
+    std::memcpy(rep_error, h_i + 2 * R, 4 * R);
+    stats->configs_scored = (int64_t)h_st[0];
+    stats->draws = (int64_t)h_st[1];
+    stats->uncertified = (int64_t)h_st[2];
+    stats->outer_iterations = (int64_t)h_st[3];
+    stats->algorithmic_bytes = (int64_t)h_st[4];
+    const int32_t ml = h_meta->max_len, ng = h_meta->n_grid;
+    *max_len = ml;
+    *n_grid = ng;
+    std::memcpy(col_sum, h_v, 8 * (size_t)ml);
+    std::memcpy(col_sq, h_v + W, 8 * (size_t)ml);
+    std::memcpy(total_times, h_v + 2 * W, 8 * (size_t)R);
+    std::memcpy(tc_sum, h_v + 2 * W + R, 8 * (size_t)ng);
+    std::memcpy(tc_sq, h_v + 2 * W + R + AGG_GRID, 8 * (size_t)ng);
+    std::memcpy(grid, h_meta->grid, 8 * (size_t)ng);
+    ctx->agg_valid = true;
     return CT_OK;
 }
 

@@ -74,8 +74,9 @@ struct SearchArgs {
     int32_t literal_sign, generation;
     int64_t cores;
     int32_t delta_col[18];
-    uint64_t col_cert;           // bit j: table column j admits raw_term_cert
-    uint64_t col_nz;             // bit j: table column j holds no exact zero
+    // device words written by the table upload: [0] bit j = table column j
+    // admits raw_term_cert, [1] bit j = column j holds no exact zero
+    const unsigned long long* col_flags;
     SeedInline seed;
     int32_t n_reps;
     // rows of 32 configurations
@@ -362,6 +363,7 @@ __device__ __forceinline__ void profile_step(const SearchArgs& a, RepState& rs, 
     const bool rec_ok = a.has_record[cp] != 0;
     const bool is_stop = a.stop_bits && bit_get(a.stop_bits, cp);
     const int64_t thr = a.threads[cp];
+    const unsigned long long col_cert = a.col_flags[0], col_nz = a.col_flags[1];
     __syncwarp();
     double dk = 0.0;
     const double bk = analyze_component_warp(ctl.cnt, lane < N_COMP ? lane : N_COMP - 1,
@@ -372,14 +374,14 @@ __device__ __forceinline__ void profile_step(const SearchArgs& a, RepState& rs, 
     if (act) {
         const int slot = __popc(amask & ((1u << lane) - 1u));
         ctl.act[slot].col = col;
-        ctl.act[slot].nz = (col < 64 && ((a.col_nz >> col) & 1ull)) ? 1 : 0;
+        ctl.act[slot].nz = (col < 64 && ((col_nz >> col) & 1ull)) ? 1 : 0;
         ctl.act[slot].p = pv;
         // literal sign: (-d)(c - p) == d(p - c) exactly
         ctl.act[slot].d = a.literal_sign ? -dk : dk;
     }
     // certified division domain for every active term
     const double two_m200 = 6.223015277861142e-61;
-    const bool cert_ok = !act || (col < 64 && ((a.col_cert >> col) & 1ull) && fabs(dk) >= two_m200);
+    const bool cert_ok = !act || (col < 64 && ((col_cert >> col) & 1ull) && fabs(dk) >= two_m200);
     const bool cert_all = __all_sync(FULL, cert_ok);
     if (lane == 0) {
         const int na = __popc(amask);

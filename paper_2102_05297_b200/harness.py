@@ -338,6 +338,8 @@ def simulate(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None) -> C
     devices = list(devices) if devices else [0]
     launched, _ = _launch_all(spec, devices)
     reps = spec.repetitions
+    if len(launched) == 1:
+        return _report_one_device(spec, launched[0][0])
     nst_l, status_l, scored, uncert = [], [], 0, 0
     for ctx, first, n in launched:
         nst, status, err, stats = ctx.fetch_status(n)
@@ -393,6 +395,37 @@ def simulate(spec: ExperimentSpec, devices: Optional[Sequence[int]] = None) -> C
         step_curve_mean=mean, step_curve_std=step_std, time_grid_seconds=grid / 1e6,
         time_curve_mean=tmean, time_curve_std=np.sqrt(tvar),
         configs_scored=int(scored), uncertified_draws=int(uncert))
+
+
+def _report_one_device(spec: ExperimentSpec, ctx) -> ConvergenceReport:
+    """simulate() of a launch on one device: the report's sums, maxima and
+    time grid come back from one ct_report call (one synchronisation); the
+    final divisions are the reference's numpy operations (harness.py:202-224)."""
+    reps = spec.repetitions
+    tr = reps if spec.time_repetitions is None else min(reps, spec.time_repetitions)
+    out = ctx.report(spec.profiling_overhead, reps, tr)
+    status = out["status"]
+    bad = np.flatnonzero(status == _native.CT_STATUS_ERROR)
+    if bad.size:
+        r = int(bad[0])
+        raise rep_error(int(out["rep_error"][r]), ctx.failing_index(r, reps))
+    nst = out["n_steps"].astype(np.int64)
+    mean = out["col_sum"] / reps
+    var = np.maximum(0.0, out["col_sq"] / reps - mean * mean)
+    tmean = out["tc_sum"] / tr
+    tvar = np.maximum(0.0, out["tc_sq"] / tr - tmean * tmean)
+    ds = spec.dataset
+    stats = out["stats"]
+    return ConvergenceReport(
+        name=spec.name, searcher=spec.searcher,
+        dataset_label=f"{ds.arch.name}/{ds.input_label}", repetitions=reps,
+        inner_steps=spec.inner_steps, outer_iterations=spec.resolved_outer_iterations(),
+        seed=spec.seed, slack=spec.slack, profiling_overhead=spec.profiling_overhead,
+        steps=nst.astype(float), censored=int(np.count_nonzero(status != _native.CT_STATUS_STOPPED)),
+        mean_time_seconds=float(np.mean(out["total"])) / 1e6,
+        step_curve_mean=mean, step_curve_std=np.sqrt(var), time_grid_seconds=out["grid"] / 1e6,
+        time_curve_mean=tmean, time_curve_std=np.sqrt(tvar),
+        configs_scored=int(stats.configs_scored), uncertified_draws=int(stats.uncertified))
 
 
 def simulate_host_aggregate(spec: ExperimentSpec,
