@@ -104,6 +104,13 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l,
 int ct_tuner_profile_passes(ct_tuner* t, const char* const* metrics, int32_t n_metrics,
                             int32_t* passes);
 
+/* Accumulated wall time of ct_tuner_profile by phase, microseconds:
+ * [0] counter-data init + SetConfig, [1] replay passes (range + launch),
+ * [2] stream sync, [3] DecodeData, [4] metric evaluation, [5] number of
+ * calls, [6] replay passes, [7] host-configuration builds.  reset != 0
+ * clears the counters after reading. */
+int ct_tuner_profile_timing(ct_tuner* t, double* out8, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

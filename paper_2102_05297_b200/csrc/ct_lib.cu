@@ -125,6 +125,7 @@ struct ct_ctx {
     bool res_valid = false;
     // scratch
     DevBuf<double> scratch_w;
+    DevBuf<unsigned char> scratch_head;
     DevBuf<int32_t> scratch_perm;
     // single-call buffers
     DevBuf<double> vec_a, vec_b;
@@ -689,9 +690,9 @@ int ensure_results(ct_ctx* ctx, int64_t reps, int64_t max_steps) {
     return CT_OK;
 }
 
-template <int NT, bool SMEM, bool PRE, bool TOPK = false>
+template <int NT, bool SMEM, bool PRE, bool TOPK = false, bool HG = false>
 int launch_profile_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
-    auto kern = k_profile_search<NT, SMEM, PRE, TOPK>;
+    auto kern = k_profile_search<NT, SMEM, PRE, TOPK, HG>;
     if (smem > 48 * 1024)
         CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -701,6 +702,11 @@ int launch_profile_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
     if (!SMEM) {
         CT_CUDA(ctx->scratch_w.ensure((size_t)grid * 64 * (size_t)a.nrows));
         a.scratch_w = ctx->scratch_w.p;
+    }
+    if (HG) {
+        const size_t head = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+        CT_CUDA(ctx->scratch_head.ensure((size_t)grid * head));
+        a.scratch_head = ctx->scratch_head.p;
     }
     kern<<<grid, NT, smem, ctx->stream>>>(a);
     CT_CUDA(cudaGetLastError());
@@ -796,7 +802,8 @@ int ct_destroy(ct_ctx* ctx) {
     ctx->threads.release(); ctx->counters.release(); ctx->has_record.release();
     ctx->stop_bits.release(); ctx->step_index.release(); ctx->step_profiled.release();
     ctx->n_steps.release(); ctx->status.release(); ctx->rep_error.release();
-    ctx->stats.release(); ctx->scratch_w.release();
+    ctx->stats.release(); ctx->scratch_w.release(); ctx->scratch_head.release();
+    ctx->col_flags.release(); ctx->table_rm.release(); ctx->col_part.release();
     ctx->scratch_perm.release(); ctx->vec_a.release();
     ctx->vec_b.release(); ctx->mask_a.release(); ctx->mask_b.release(); ctx->key_a.release();
     ctx->key_b.release(); ctx->val_a.release(); ctx->val_b.release(); ctx->cub_tmp.release();
@@ -1195,7 +1202,13 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     bool pre = a.nrows < 32;
     if (const char* env = std::getenv("CT_SEARCH_PRE")) pre = std::atoi(env) != 0;
     const size_t pref_b = (pre ? 16 : 8) * 32 * (size_t)a.nrows;   // weights [+ in-row prefixes]
-    if (head_b > budget) return fail(CT_ERR_UNSUPPORTED, "space too large for the row index");
+    if (head_b > budget) {
+        // the row index (row totals + explored bits) outgrows shared memory:
+        // all per-repetition state in a per-CTA slice of global scratch
+        if (a.topk >= 0)
+            return fail(CT_ERR_UNSUPPORTED, "score_top_k on spaces above ~300k configurations");
+        return launch_profile_t<512, false, false, false, true>(ctx, a, 0, n_reps);
+    }
     const int64_t want_per_sm = std::min<int64_t>(std::min<int64_t>(
         (n_reps + ctx->sm_count - 1) / ctx->sm_count, 32), 2048 / nt);
     const size_t per_cta_cap = std::min<size_t>(

@@ -91,6 +91,7 @@ struct SearchArgs {
     // storage: weights (8 B each, nrows * 32) in shared memory or a per-CTA
     // slice of scratch_w
     double* scratch_w;
+    unsigned char* scratch_head;   // HG kernels: per-CTA row totals + explored bits
     // outputs
     int32_t* step_index;
     uint8_t* step_profiled;
@@ -463,7 +464,7 @@ __device__ __forceinline__ void weight_phase(const SearchArgs& a, Ctl<NW>& ctl, 
 // difference adds 2 2^-53 T; r and the zeroing updates a few 2^-53 T more),
 // so P(i-1) + B < r and r + B < P(i) imply that the reference picks i too.
 // Otherwise the draw is re-decided with the sequential float64 cumsum.
-template <bool PRE, int NW>
+template <bool PRE, int NW, bool COOP = false>
 __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl<NW>& ctl,
                                           uint32_t* expl, double* w, double* pre, double* row_tot,
                                           const u128* jA, const u128* jC, int32_t* out_idx,
@@ -520,15 +521,44 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
                 const int L = __ffs(bal) - 1;
                 double carry = __shfl_up_sync(FULL, lane_pref, 1);
                 if (lane == 0) carry = 0.0;
-                if (lane == L) {
-                    for (int t = t0; t < t1; ++t) {
-                        const double nxt = add(carry, row_tot[t]);
-                        if (nxt > r) { row = t; break; }
-                        carry = nxt;
+                if constexpr (COOP) {
+                    // long chunks (large spaces): the whole warp walks lane
+                    // L's chunk 32 rows at a time -- a warp scan of the row
+                    // totals and a ballot per slab instead of one dependent
+                    // add per row (any summation order is certified)
+                    carry = __shfl_sync(FULL, carry, L);
+                    const int c0 = L * cpl, c1 = min(c0 + cpl, a.nrows);
+                    for (int base = c0; base < c1; base += 32) {
+                        const int t = base + lane;
+                        double incl = (t < c1) ? row_tot[t] : 0.0;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const double v = __shfl_up_sync(FULL, incl, d);
+                            if (lane >= d) incl = add(incl, v);
+                        }
+                        const double cand = add(carry, incl);
+                        const unsigned fb = __ballot_sync(FULL, t < c1 && cand > r);
+                        if (fb) {
+                            const int l = __ffs(fb) - 1;
+                            double prev = __shfl_up_sync(FULL, cand, 1);
+                            if (lane == 0) prev = carry;
+                            row = base + l;
+                            carry = __shfl_sync(FULL, prev, l);
+                            break;
+                        }
+                        carry = __shfl_sync(FULL, cand, 31);
                     }
+                } else {
+                    if (lane == L) {
+                        for (int t = t0; t < t1; ++t) {
+                            const double nxt = add(carry, row_tot[t]);
+                            if (nxt > r) { row = t; break; }
+                            carry = nxt;
+                        }
+                    }
+                    row = __shfl_sync(FULL, row, L);
+                    carry = __shfl_sync(FULL, carry, L);
                 }
-                row = __shfl_sync(FULL, row, L);
-                carry = __shfl_sync(FULL, carry, L);
                 if (row >= 0) {
                     double incl;
                     if (PRE) {
@@ -772,9 +802,10 @@ __device__ __forceinline__ void topk_phase(const SearchArgs& a, int64_t cp, int6
 // k_profile_search: one CTA runs one repetition end to end (then the next one
 // of its persistent slice); the serial phases run on warp 0 while the other
 // warps wait at the CTA barrier.
-template <int NT, bool SMEM, bool PRE, bool TOPK>
+template <int NT, bool SMEM, bool PRE, bool TOPK, bool HG = false>
 __global__ void __launch_bounds__(NT, (NT <= 64) ? 8 : ((NT == 128) ? 7 : (896 / NT)))
 k_profile_search(const SearchArgs a) {
+    static_assert(!HG || (!SMEM && !TOPK), "global row index: weights in global scratch, no top-K");
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ Ctl<NW> ctl;
@@ -789,9 +820,15 @@ k_profile_search(const SearchArgs a) {
 
     // dynamic shared memory: row totals | explored bits | [top-K: exclusion
     // bits | radix histogram | select state] | [weights | in-row prefixes]
-    double* row_tot = reinterpret_cast<double*>(smem);
-    uint32_t* expl = reinterpret_cast<uint32_t*>(smem + 16 * (size_t)a.nrows);
     const size_t head = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
+    // HG (spaces whose row index outgrows shared memory, >~ 300k
+    // configurations): row totals and explored bits in a per-CTA slice of
+    // global scratch as well
+    unsigned char* head_base = HG ? reinterpret_cast<unsigned char*>(a.scratch_head) +
+                                        (size_t)blockIdx.x * head
+                                  : smem;
+    double* row_tot = reinterpret_cast<double*>(head_base);
+    uint32_t* expl = reinterpret_cast<uint32_t*>(head_base + 16 * (size_t)a.nrows);
     const size_t tk_b = TOPK ? topk_bytes(a.nwords) : 0;
     uint32_t* excl_k = reinterpret_cast<uint32_t*>(smem + head);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + head + ((4 * (size_t)a.nwords + 15) & ~(size_t)15));
@@ -846,7 +883,8 @@ k_profile_search(const SearchArgs a) {
             __syncthreads();
             CT_CLK(clk_weight);
             if (warp == 0) {
-                draw_step<PRE>(a, rs, ctl, expl, w, pre, row_tot, jA, jC, out_idx, out_prof, lane);
+                draw_step<PRE, NW, (NT >= 512)>(a, rs, ctl, expl, w, pre, row_tot, jA, jC, out_idx,
+                                                out_prof, lane);
                 CT_CLK(clk_p4);
                 if (!ctl.done && it + 1 < a.outer)
                     profile_step(a, rs, ctl, expl, out_idx, out_prof, lane, pcol);

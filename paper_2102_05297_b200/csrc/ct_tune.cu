@@ -21,6 +21,7 @@
 #include <cupti_target.h>
 
 #include <algorithm>
+#include <chrono>
 #include <map>
 #include <memory>
 #include <atomic>
@@ -151,6 +152,11 @@ struct ct_tuner {
     CUpti_RangeProfiler_Object* rp = nullptr;
     // host configurations by metric set (building one costs milliseconds)
     std::map<std::string, std::unique_ptr<HostConfig>> configs;
+    // wall time of ct_tuner_profile by phase (microseconds, accumulated):
+    // [0] counter-data init + SetConfig, [1] replay passes (range + launch),
+    // [2] stream sync, [3] DecodeData, [4] evaluation, [5] calls, [6] passes,
+    // [7] host-config build (first use of a metric set)
+    double prof_us[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -535,8 +541,15 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     Variant* v = nullptr;
     rc = get_variant(t, variant, &v); if (rc) return rc;
     rc = cupti_init(t); if (rc) return rc;
+    using clk = std::chrono::steady_clock;
+    auto us = [](clk::time_point a, clk::time_point b) {
+        return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    const auto t0 = clk::now();
     HostConfig* hc = nullptr;
     rc = host_config_cached(t, metrics, n, &hc); if (rc) return rc;
+    const auto t1 = clk::now();
+    t->prof_us[7] += us(t0, t1);
     // counter data image for one range (re-initialised per collection)
     if (hc->counter_data.empty()) {
         CUpti_RangeProfiler_GetCounterDataSize_Params cs = {CUpti_RangeProfiler_GetCounterDataSize_Params_STRUCT_SIZE};
@@ -568,6 +581,7 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     sc.passIndex = 0;
     sc.targetNestingLevel = 1;
     TU_CUPTI(cuptiRangeProfilerSetConfig(&sc));
+    const auto t2 = clk::now();
     int used = 0;
     for (;;) {
         CUpti_RangeProfiler_Start_Params st = {CUpti_RangeProfiler_Start_Params_STRUCT_SIZE};
@@ -589,10 +603,13 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
         if (sp.isAllPassSubmitted) break;
         if (used > 64) return fail(CT_TUNE_ERR_PROFILER, "range profiler did not finish its passes");
     }
+    const auto t3 = clk::now();
     TU_RT(cudaStreamSynchronize(t->stream));
+    const auto t4 = clk::now();
     CUpti_RangeProfiler_DecodeData_Params dd = {CUpti_RangeProfiler_DecodeData_Params_STRUCT_SIZE};
     dd.pRangeProfilerObject = t->rp;
     TU_CUPTI(cuptiRangeProfilerDecodeData(&dd));
+    const auto t5 = clk::now();
     CUpti_Profiler_Host_EvaluateToGpuValues_Params ev = {sizeof(CUpti_Profiler_Host_EvaluateToGpuValues_Params)};
     ev.pHostObject = hc->host;
     ev.pCounterDataImage = data.data();
@@ -602,7 +619,23 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     ev.numMetrics = (size_t)n;
     ev.pMetricValues = values;
     TU_CUPTI(cuptiProfilerHostEvaluateToGpuValues(&ev));
+    const auto t6 = clk::now();
+    t->prof_us[0] += us(t1, t2);
+    t->prof_us[1] += us(t2, t3);
+    t->prof_us[2] += us(t3, t4);
+    t->prof_us[3] += us(t4, t5);
+    t->prof_us[4] += us(t5, t6);
+    t->prof_us[5] += 1;
+    t->prof_us[6] += used;
     if (passes) *passes = used;
+    return CT_TUNE_OK;
+}
+
+int ct_tuner_profile_timing(ct_tuner* t, double* out8, int32_t reset) {
+    if (!t || !out8) return fail(CT_TUNE_ERR_VALUE, "null argument");
+    for (int i = 0; i < 8; ++i) out8[i] = t->prof_us[i];
+    if (reset)
+        for (int i = 0; i < 8; ++i) t->prof_us[i] = 0;
     return CT_TUNE_OK;
 }
 

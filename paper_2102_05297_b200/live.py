@@ -44,6 +44,14 @@ _KDIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "kernels")
 TABLE1_ABBRS: Sequence[str] = tuple(a for a in cc.ABBREVIATIONS if a in cc.VOLTA_METRICS)
 TABLE1_METRICS: Sequence[str] = tuple(cc.VOLTA_METRICS[a][0] for a in TABLE1_ABBRS)
 
+# The largest single-replay-pass subset of Table 1 on GB100 (SURVEY F13 group
+# 1, 13 metrics): DRAM / L2 sectors, global load requests, executed and
+# issued instructions, the four utilisations, warp / predication efficiency.
+GROUP1_ABBRS: Sequence[str] = ("DRAM_RT", "DRAM_WT", "L2_RT", "L2_WT", "TEX_RWT", "INST_EXE",
+                               "INST_ISSUE_U", "DRAM_U", "L2_U", "TEX_U", "SM_E", "WARP_E",
+                               "WARP_NP_E")
+GROUP1_METRICS: Sequence[str] = tuple(cc.VOLTA_METRICS[a][0] for a in GROUP1_ABBRS)
+
 _u64 = ctypes.c_uint64
 _i32 = ctypes.c_int32
 _f32 = ctypes.c_float

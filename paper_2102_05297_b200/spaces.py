@@ -16,6 +16,8 @@ reproducible byte for byte.
     conv       3,928 configs, 10 params (4096^2, 7x7 filter)
     gemm       5,788 configs, 10 params (2048^3 sgemm, CLBlast-style)
     gemm_full  205,216 configs, 14 params
+    stress(n)  n configs (BASELINE.md section 3 stress sizes 1,048,576 and
+               4,194,304): random counters, the scoring microbenchmark's table
 """
 
 import itertools
@@ -423,6 +425,37 @@ SPACES = {
     "gemm": gemm,
     "gemm_full": gemm_full,
 }
+
+
+def stress(n: int = 1 << 20, seed: int = 1) -> Dataset:
+    """The scoring microbenchmark's inputs (SURVEY
+    section 8d) as a replay dataset: every operation counter (the exact
+    model's table columns) uniform(1, 1e6) with 2% exact zeros, utilisations
+    uniform over their ranges, runtimes uniform(100, 1000) us.  The space is
+    the first n points of a 6-parameter grid of 16 values each.  At n >= 1M
+    the 19-column table (152 MB at 1M, 608 MB at 4M) no longer fits the
+    126 MB L2, so the search kernel's table reads come from HBM."""
+    if not 1 <= n <= 16 ** 6:
+        raise ValueError("stress spaces hold 1 .. 16^6 configurations")
+    rng = np.random.default_rng(seed)
+    idx = np.arange(n, dtype=np.int64)
+    grid = np.stack([(idx >> (4 * k)) & 15 for k in range(6)], axis=1).astype(np.float64)
+    tps = [TuningParameter(name=f"P{k}", values=tuple(float(v) for v in range(16)),
+                           is_binary=False) for k in range(6)]
+    cm = np.empty((n, len(COUNTER_NAMES)))
+    for j, name in enumerate(COUNTER_NAMES):
+        if name in ("DRAM_U", "TEX_U", "SHR_U"):
+            col = rng.uniform(0.0, 10.0, n)
+        elif name in ("L2_U", "SM_E", "WARP_E", "WARP_NP_E", "INST_ISSUE_U"):
+            col = rng.uniform(0.0, 100.0, n)
+        else:
+            col = rng.uniform(1.0, 1e6, n)
+            col[rng.random(n) < 0.02] = 0.0
+        cm[:, j] = col
+    threads = rng.integers(1 << 10, 1 << 24, n)
+    space = TuningSpace.from_assignments(tps, grid)
+    return Dataset(space, B200_ARCH, f"stress-{n}", runtime_us=rng.uniform(100.0, 1000.0, n),
+                   global_threads=threads, counter_names=COUNTER_NAMES, counter_matrix=cm)
 
 
 def required_present(ds: Dataset) -> bool:

@@ -74,6 +74,7 @@ SIGNATURES = {
     "ct_tuner_profile": (ctypes.c_int, [_vp, _i32, _P(LaunchC), _P(_cp), _i32,
                                         _P(ctypes.c_double), _P(_i32)]),
     "ct_tuner_profile_passes": (ctypes.c_int, [_vp, _P(_cp), _i32, _P(_i32)]),
+    "ct_tuner_profile_timing": (ctypes.c_int, [_vp, _P(ctypes.c_double), _i32]),
 }
 
 _lib = None
@@ -262,6 +263,16 @@ class Tuner:
                                           vals.ctypes.data_as(_P(ctypes.c_double)),
                                           ctypes.byref(passes)))
         return vals, passes.value
+
+    PROFILE_PHASES = ("setconfig_us", "passes_us", "sync_us", "decode_us", "evaluate_us",
+                      "calls", "replay_passes", "host_config_us")
+
+    def profile_timing(self, reset: bool = False) -> dict:
+        """Accumulated wall time of profile() by phase (ct_tuner_profile_timing)."""
+        out = np.zeros(8, dtype=np.float64)
+        _check(self._lib.ct_tuner_profile_timing(self._h, out.ctypes.data_as(_P(ctypes.c_double)),
+                                                 int(bool(reset))))
+        return dict(zip(self.PROFILE_PHASES, out.tolist()))
 
     def profile_passes(self, metrics: Sequence[str]) -> int:
         p = _i32()

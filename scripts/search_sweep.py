@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--reps", type=int, default=1000)
     ap.add_argument("--outer", type=int, default=40)
     ap.add_argument("--runs", type=int, default=5)
+    ap.add_argument("--kernel-only", action="store_true", help="one launch per space (ncu)")
     a = ap.parse_args()
     import torch
     from paper_2102_05297_b200 import ExactModelSet, harness, spaces
@@ -29,10 +30,18 @@ def main():
     ctx.set_stream(stream.cuda_stream)
     from paper_2102_05297_b200 import formats
     hbm = 6548.5
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm = float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        pass
     for name in a.spaces.split(","):
         # "<name>" = synthetic stand-in, "b200:<name>" = datasets/<name>-b200
         if name.startswith("b200:"):
             ds = formats.load_dataset_dir(os.path.join(ROOT, "datasets", name[5:] + "-b200"))
+        elif name.startswith("stress:"):
+            # BASELINE.md section 3 stress sizes: the table exceeds the L2
+            ds = spaces.stress(int(name[7:]))
         else:
             ds = spaces.SPACES[name]()
         spec = harness.ExperimentSpec(dataset=ds, searcher="profile", model=ExactModelSet(ds),
@@ -41,10 +50,13 @@ def main():
         params, _ = harness.prepare_device(ctx, spec)
         ref = None
         for nt in a.nt.split(","):
-            os.environ["CT_SEARCH_NT"] = nt
+            if nt == "auto":
+                os.environ.pop("CT_SEARCH_NT", None)     # the launcher's choice
+            else:
+                os.environ["CT_SEARCH_NT"] = nt
             harness.launch(ctx, spec, params, 0, a.reps)   # warm-up
             times = []
-            for _ in range(a.runs):
+            for _ in range(0 if a.kernel_only else a.runs):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 harness.launch(ctx, spec, params, 0, a.reps)
@@ -57,9 +69,13 @@ def main():
                 ref = (idx.copy(), nst.copy())
             else:
                 same = bool((ref[1] == nst).all() and (ref[0] == idx).all())
+            if a.kernel_only:
+                continue
             ms = sorted(times)[len(times) // 2]
             gbs = stats.algorithmic_bytes / (ms / 1e3) / 1e9
-            print(json.dumps({"space": name, "n": len(ds.space), "nt": int(nt), "ms": ms,
+            print(json.dumps({"space": name, "n": len(ds.space), "nt": nt, "ms": ms,
+                              "reps": a.reps, "outer": a.outer,
+                              "algorithmic_bytes": int(stats.algorithmic_bytes),
                               "configs_per_s": stats.configs_scored / (ms / 1e3),
                               "algorithmic_GBps": gbs, "hbm_frac": gbs / hbm,
                               "uncertified": int(stats.uncertified),

@@ -445,3 +445,29 @@ def test_reference_acceptance_criterion_6_portability():
     assert prof.mean_steps == float(g["c6_prof_mean"])
     assert rand.mean_steps == float(g["c6_rand_mean"])
     assert improvement == float(g["c6_improvement"])
+
+
+def test_stress_space_global_row_index_matches_oracle():
+    """N = 1,048,576 (BASELINE.md stress size): the row index no longer fits
+    shared memory, so row totals, explored bits and weights live in global
+    scratch (HG kernel) and the draw walks long row chunks with the whole
+    warp.  Trajectories against the oracle (numpy restatement of the
+    reference, pinned by the golden tests) for a few repetitions."""
+    import countertune_oracle as oracle
+    from paper_2102_05297_b200 import ExactModelSet, harness, spaces
+    from paper_2102_05297_b200.space import replay_arrays
+    ds = spaces.stress(1 << 20)
+    spec = harness.ExperimentSpec(dataset=ds, searcher="profile", model=ExactModelSet(ds),
+                                  repetitions=3, outer_iterations=5, seed=9,
+                                  stop_at_well_performing=False)
+    res, rt = harness.run_batch(spec)
+    ms = ExactModelSet(ds)
+    matrix = ms.prediction_matrix(ds.space)
+    column = {c: j for j, c in enumerate(ms.counters)}
+    _, th, req, hr = replay_arrays(ds)
+    seeds = np.random.SeedSequence(9).spawn(3)
+    for r in range(3):
+        steps, status, _ = oracle.profile_search(matrix, column, rt, th, req, hr, pre_volta=False,
+                                                 cores=ds.arch.cores, i=5, n=5, seed=seeds[r],
+                                                 stop=None)
+        assert res.step_index[r, :res.n_steps[r]].tolist() == [s[0] for s in steps]
