@@ -21,6 +21,13 @@
 //               as an operand, no load instruction at all)
 //   REVERSE     filter traversal order (fx outer instead of fy outer)
 //
+// With LOCAL = 2 and WPTX even, each thread's output columns are processed in
+// adjacent pairs with Blackwell's packed FP32 FMA (FFMA2, PTX fma.rn.f32x2,
+// sm_100): output pair (2h, 2h+1) with filter column fx reads the window
+// pair (win[2h+fx], win[2h+fx+1]) and takes the filter tap as a broadcast
+// operand.  Every lane's FMA is the scalar path's, in the same order:
+// outputs are identical.
+//
 // The tile lives in dynamic shared memory: the host passes
 // smem_bytes() = 4 * ((TH + F - 1) * (TW + 8 + PAD) + CACHE_F * F * F).
 #ifndef TBX
@@ -59,7 +66,7 @@
 
 constexpr int F = FILTER, R = FILTER / 2;
 constexpr int TW = TBX * WPTX, TH = TBY * WPTY;
-constexpr int LW = TW + F - 1, LH = TH + F - 1;   // tile incl. halo
+constexpr int LH = TH + F - 1;                    // tile rows incl. halo
 constexpr int V4 = (TW + 8) / 4;                  // float4 per staged row: x0-4 .. x0+TW+3
 constexpr int SW = 4 * V4 + PAD;                  // shared row stride
 static_assert(F <= 9, "the staged row holds a halo of at most 4 columns per side");
@@ -122,7 +129,64 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter 
 #pragma unroll
         for (int i = 0; i < WPTX; ++i) acc[wy][i] = 0.0f;
 
-#if LOCAL == 2
+#if LOCAL == 2 && WPTX % 2 == 0
+    {
+        // output pairs (2h, 2h + 1); the window row as overlapping pairs
+        // pr[k] = (win[k], win[k + 1]): even k are the registers a vector
+        // LDS fills anyway, odd k cost two moves each, once per input row
+        constexpr int H = WPTX / 2, L = WPTX + F - 1;
+        typedef unsigned long long f2;
+        const int ly0 = ty * WPTY;
+        const int lx = tx * WPTX;
+        f2 accp[WPTY][H];
+#pragma unroll
+        for (int wy = 0; wy < WPTY; ++wy)
+#pragma unroll
+            for (int h = 0; h < H; ++h) accp[wy][h] = 0ull;
+#pragma unroll
+        for (int iy = 0; iy < WPTY + F - 1; ++iy) {
+            float win[L];
+#pragma unroll
+            for (int k = 0; k < L; ++k) win[k] = INPUT(ly0 + iy, lx + k);
+            f2 pr[L - 1];
+#pragma unroll
+            for (int k = 0; k < L - 1; ++k)
+                asm("mov.b64 %0, {%1, %2};" : "=l"(pr[k]) : "f"(win[k]), "f"(win[k + 1]));
+#pragma unroll
+            for (int wy = 0; wy < WPTY; ++wy) {
+                const int fy = iy - wy;
+                if (fy >= 0 && fy < F) {
+#if REVERSE
+#pragma unroll
+                    for (int h = 0; h < H; ++h)
+#pragma unroll kUnrollF
+                        for (int fx = 0; fx < F; ++fx) {
+                            const float f = FILT(fy, fx);
+                            f2 fp;
+                            asm("mov.b64 %0, {%1, %1};" : "=l"(fp) : "f"(f));
+                            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(accp[wy][h]) : "l"(pr[2 * h + fx]), "l"(fp));
+                        }
+#else
+#pragma unroll kUnrollF
+                    for (int fx = 0; fx < F; ++fx) {
+                        const float f = FILT(fy, fx);
+                        f2 fp;
+                        asm("mov.b64 %0, {%1, %1};" : "=l"(fp) : "f"(f));
+#pragma unroll
+                        for (int h = 0; h < H; ++h)
+                            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(accp[wy][h]) : "l"(pr[2 * h + fx]), "l"(fp));
+                    }
+#endif
+                }
+            }
+        }
+#pragma unroll
+        for (int wy = 0; wy < WPTY; ++wy)
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+                asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[wy][2 * h]), "=f"(acc[wy][2 * h + 1]) : "l"(accp[wy][h]));
+    }
+#elif LOCAL == 2
     {
         const int ly0 = ty * WPTY;         // first output row inside the tile
         const int lx = tx * WPTX;          // first output column inside the tile

@@ -20,6 +20,12 @@
 // idempotent under timing and profiler replay).
 //
 // 20 flops per interaction (the customary count); FP32/MUFU-bound.
+//
+// With OUTER even, a thread's bodies are processed in pairs with Blackwell's
+// packed FP32 instructions (FADD2 / FMUL2 / FFMA2, PTX add/mul/fma.rn.f32x2,
+// sm_100): one instruction advances two interactions, the j body's
+// coordinates enter as a broadcast scalar operand, and each lane's
+// operation is the scalar path's IEEE operation, so the sums are identical.
 #ifndef BLOCK
 #define BLOCK 256
 #endif
@@ -72,6 +78,46 @@ struct Body {
     }
 };
 
+#if OUTER % 2 == 0
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+    f2 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r;
+}
+__device__ __forceinline__ void upk(f2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+    f2 d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d;
+}
+
+// two of the thread's bodies, lane k of every register pair = body 2p + k
+struct BodyPair {
+    f2 px, py, pz, ax, ay, az;
+    __device__ __forceinline__ void interact(float qx, float qy, float qz, float m, float eps2) {
+        const f2 dx = sub2(pk(qx, qx), px), dy = sub2(pk(qy, qy), py), dz = sub2(pk(qz, qz), pz);
+        const f2 r2 = fma2(dz, dz, fma2(dy, dy, fma2(dx, dx, pk(eps2, eps2))));
+        float r0, r1;
+        upk(r2, r0, r1);
+#if FAST_RSQRT
+        float i0, i1;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(i0) : "f"(r0));
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(i1) : "f"(r1));
+#else
+        const float i0 = 1.0f / sqrtf(r0), i1 = 1.0f / sqrtf(r1);
+#endif
+        const f2 inv = pk(i0, i1);
+        const f2 s = mul2(mul2(pk(m, m), inv), mul2(inv, inv));
+        ax = fma2(dx, s, ax); ay = fma2(dy, s, ay); az = fma2(dz, s, az);
+    }
+};
+#endif
+
 extern "C" __global__ void __launch_bounds__(BLOCK * JS)
 nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* __restrict__ y,
       const float* __restrict__ z, const float* __restrict__ m, int n, float eps2,
@@ -96,6 +142,23 @@ nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* _
 #endif
         b[o].ax = b[o].ay = b[o].az = 0.0f;
     }
+#if OUTER % 2 == 0
+    // the interaction loops run on packed pairs; the scalar bodies are
+    // rebuilt from them for the reductions below
+    BodyPair bp[OUTER / 2];
+#pragma unroll
+    for (int p = 0; p < OUTER / 2; ++p) {
+        bp[p].px = pk(b[2 * p].px, b[2 * p + 1].px);
+        bp[p].py = pk(b[2 * p].py, b[2 * p + 1].py);
+        bp[p].pz = pk(b[2 * p].pz, b[2 * p + 1].pz);
+        bp[p].ax = bp[p].ay = bp[p].az = 0ull;
+    }
+#define INTERACT_ALL(qx, qy, qz, qm) \
+    _Pragma("unroll") for (int p = 0; p < OUTER / 2; ++p) bp[p].interact(qx, qy, qz, qm, eps2)
+#else
+#define INTERACT_ALL(qx, qy, qz, qm) \
+    _Pragma("unroll") for (int o = 0; o < OUTER; ++o) b[o].interact(qx, qy, qz, qm, eps2)
+#endif
 #if USE_SMEM
 #if SOA
     __shared__ __align__(16) float sx[JS][BLOCK], sy[JS][BLOCK], sz[JS][BLOCK], sm[JS][BLOCK];
@@ -121,15 +184,14 @@ nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* _
             const vec vz = *reinterpret_cast<const vec*>(&sz[ty][jj]);
             const vec vm = *reinterpret_cast<const vec*>(&sm[ty][jj]);
 #pragma unroll
-            for (int k = 0; k < VEC; ++k)
-#pragma unroll
-                for (int o = 0; o < OUTER; ++o) b[o].interact(get(vx, k), get(vy, k), get(vz, k), get(vm, k), eps2);
+            for (int k = 0; k < VEC; ++k) {
+                INTERACT_ALL(get(vx, k), get(vy, k), get(vz, k), get(vm, k));
+            }
 #else
 #pragma unroll
             for (int k = 0; k < VEC; ++k) {
                 const float4 q = sp[ty][jj + k];
-#pragma unroll
-                for (int o = 0; o < OUTER; ++o) b[o].interact(q.x, q.y, q.z, q.w, eps2);
+                INTERACT_ALL(q.x, q.y, q.z, q.w);
             }
 #endif
         }
@@ -143,17 +205,24 @@ nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* _
         const vec vz = __ldg(reinterpret_cast<const vec*>(z + j));
         const vec vm = __ldg(reinterpret_cast<const vec*>(m + j));
 #pragma unroll
-        for (int k = 0; k < VEC; ++k)
-#pragma unroll
-            for (int o = 0; o < OUTER; ++o) b[o].interact(get(vx, k), get(vy, k), get(vz, k), get(vm, k), eps2);
+        for (int k = 0; k < VEC; ++k) {
+            INTERACT_ALL(get(vx, k), get(vy, k), get(vz, k), get(vm, k));
+        }
 #else
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
             const float4 q = __ldg(pm + j + k);
-#pragma unroll
-            for (int o = 0; o < OUTER; ++o) b[o].interact(q.x, q.y, q.z, q.w, eps2);
+            INTERACT_ALL(q.x, q.y, q.z, q.w);
         }
 #endif
+    }
+#endif
+#if OUTER % 2 == 0
+#pragma unroll
+    for (int p = 0; p < OUTER / 2; ++p) {
+        upk(bp[p].ax, b[2 * p].ax, b[2 * p + 1].ax);
+        upk(bp[p].ay, b[2 * p].ay, b[2 * p + 1].ay);
+        upk(bp[p].az, b[2 * p].az, b[2 * p + 1].az);
     }
 #endif
 #if JS > 1

@@ -1,0 +1,86 @@
+"""The CUPTI range-profiler collector against independent readings
+(counters.py:58-105 metric set):
+
+* a known-answer probe kernel (kernels/probe.cu, straight-line inline PTX):
+  thread-level FP32 instruction count = threads x NFMA exactly, shared-load
+  wavefronts = warps x NLDS exactly, executed warp instructions exactly
+  linear in the grid size, full warps (WARP_E = WARP_NP_E = 100%);
+* the 8192^2 transpose: DRAM read / write sectors within 5% of the
+  algorithmic 4 n^2 / 32 each;
+* two collections of the same launch agree within 1% (the deterministic
+  counters exactly).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def tuner():
+    from paper_2102_05297_b200.tuner import Tuner
+    t = Tuner(0)
+    yield t
+    t.close()
+
+
+def _metrics(*abbrs):
+    from paper_2102_05297_b200 import counters as cc
+    return [cc.VOLTA_METRICS[a][0] for a in abbrs]
+
+
+def _probe(tuner, blocks, threads=256, nfma=64, nlds=8):
+    import ctypes
+    from paper_2102_05297_b200.tuner import Launch
+    src = open(os.path.join(ROOT, "paper_2102_05297_b200", "kernels", "probe.cu")).read()
+    v = tuner.compile(src, "probe", [f"-DNFMA={nfma}", f"-DNLDS={nlds}"])
+    out = tuner.alloc(4 * blocks * threads)
+    tag = tuner.alloc(4 * blocks * threads)
+    launch = Launch((blocks,), (threads,), [ctypes.c_uint64(out), ctypes.c_uint64(tag),
+                                            ctypes.c_float(0.5), ctypes.c_float(1.0001)])
+    return v, launch
+
+
+def test_probe_counts_are_exact(tuner):
+    names = ("INST_F32", "SHR_LT", "SHR_WT", "INST_EXE", "WARP_E", "WARP_NP_E")
+    ms = _metrics(*names)
+    got = {}
+    for blocks in (148, 296):
+        v, launch = _probe(tuner, blocks)
+        vals, _ = tuner.profile(v, launch, ms)
+        got[blocks] = dict(zip(names, vals.tolist()))
+    for blocks, g in got.items():
+        threads = blocks * 256
+        warps = threads // 32
+        assert g["INST_F32"] == threads * 64, g
+        assert g["SHR_LT"] == warps * 8, g
+        assert g["SHR_WT"] == warps * 1, g
+        assert g["WARP_E"] == pytest.approx(32.0) and g["WARP_NP_E"] == pytest.approx(100.0), g
+    # a straight-line kernel executes the same instructions per warp
+    assert got[296]["INST_EXE"] == 2 * got[148]["INST_EXE"]
+    assert got[148]["INST_EXE"] % (148 * 8) == 0
+
+
+def test_transpose_dram_sectors_match_algorithmic_bytes(tuner):
+    from paper_2102_05297_b200 import formats
+    from paper_2102_05297_b200.live import CudaMeasurementSource, benchmark
+    ds = formats.load_dataset_dir(os.path.join(ROOT, "datasets", "transpose-b200"))
+    best = int(np.argmin(np.where(ds.has_record, ds.runtime_us, np.inf)))
+    src = CudaMeasurementSource(benchmark("transpose"), tuner=tuner)
+    v = src.variant(best)
+    launch = src.launch_of(best)
+    ms = _metrics("DRAM_RT", "DRAM_WT", "L2_RT", "L2_WT", "INST_EXE", "INST_F32")
+    a, _ = tuner.profile(v, launch, ms)
+    b, _ = tuner.profile(v, launch, ms)
+    n = 8192
+    sectors = 4 * n * n / 32
+    assert abs(a[0] - sectors) / sectors < 0.05, a
+    assert abs(a[1] - sectors) / sectors < 0.05, a
+    assert a[2] >= 0.95 * sectors and a[3] >= 0.95 * sectors, a
+    np.testing.assert_allclose(a[:4], b[:4], rtol=0.01)
+    assert a[4] == b[4] and a[5] == b[5]        # instruction counts are deterministic
