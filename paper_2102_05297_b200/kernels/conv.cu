@@ -26,7 +26,9 @@
 // sm_100): output pair (2h, 2h+1) with filter column fx reads the window
 // pair (win[2h+fx], win[2h+fx+1]) and takes the filter tap as a broadcast
 // operand.  Every lane's FMA is the scalar path's, in the same order:
-// outputs are identical.
+// outputs are identical.  The tile is staged twice, the second copy shifted
+// by one float, so every window pair is one aligned 8-byte load (no register
+// moves); the row stride is then even (PAD pads by two floats).
 //
 // The tile lives in dynamic shared memory: the host passes
 // smem_bytes() = 4 * ((TH + F - 1) * (TW + 8 + PAD) + CACHE_F * F * F).
@@ -68,7 +70,10 @@ constexpr int F = FILTER, R = FILTER / 2;
 constexpr int TW = TBX * WPTX, TH = TBY * WPTY;
 constexpr int LH = TH + F - 1;                    // tile rows incl. halo
 constexpr int V4 = (TW + 8) / 4;                  // float4 per staged row: x0-4 .. x0+TW+3
-constexpr int SW = 4 * V4 + PAD;                  // shared row stride
+// packed-FMA path (see above): two copies of the tile, the second shifted by
+// one float, so that every window pair is one aligned 8-byte shared load
+constexpr bool PAIRED = (LOCAL == 2) && (WPTX % 2 == 0);
+constexpr int SW = PAIRED ? 4 * V4 + 2 * PAD : 4 * V4 + PAD;   // shared row stride (even if PAIRED)
 static_assert(F <= 9, "the staged row holds a halo of at most 4 columns per side");
 constexpr int NT = TBX * TBY;
 constexpr int kUnrollF = UNROLL_F ? F : 1;
@@ -95,7 +100,7 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TBX + tx;
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
 #if CACHE_F
-    float* sf = dsm + (LOCAL ? LH * SW : 0);
+    float* sf = dsm + (LOCAL ? (PAIRED ? 2 : 1) * LH * SW : 0);
     for (int i = tid; i < F * F; i += NT) sf[i] = filt[i];
 #define FILT(fy, fx) sf[(fy) * F + (fx)]
 #else
@@ -115,6 +120,11 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter 
             v = __ldg(reinterpret_cast<const float4*>(in + (size_t)gy * width + gx));
         float* d = tile + ry * SW + 4 * c4;
         d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        if (PAIRED) {       // tile2[i] = tile[i + 1]
+            float* d2 = dsm + LH * SW + ry * SW + 4 * c4 - 1;
+            if (c4 > 0) d2[0] = v.x;
+            d2[1] = v.y; d2[2] = v.z; d2[3] = v.w;
+        }
     }
 #define INPUT(ly, lx) tile[(ly) * SW + (lx) + (4 - R)]
 #else
@@ -132,8 +142,7 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter 
 #if LOCAL == 2 && WPTX % 2 == 0
     {
         // output pairs (2h, 2h + 1); the window row as overlapping pairs
-        // pr[k] = (win[k], win[k + 1]): even k are the registers a vector
-        // LDS fills anyway, odd k cost two moves each, once per input row
+        // pr[k] = (in[k], in[k + 1]), each one 8-byte shared load
         constexpr int H = WPTX / 2, L = WPTX + F - 1;
         typedef unsigned long long f2;
         const int ly0 = ty * WPTY;
@@ -143,15 +152,19 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter 
         for (int wy = 0; wy < WPTY; ++wy)
 #pragma unroll
             for (int h = 0; h < H; ++h) accp[wy][h] = 0ull;
+        const float* tile2 = dsm + LH * SW;
 #pragma unroll
         for (int iy = 0; iy < WPTY + F - 1; ++iy) {
-            float win[L];
-#pragma unroll
-            for (int k = 0; k < L; ++k) win[k] = INPUT(ly0 + iy, lx + k);
+            // pair k = (in[k], in[k+1]) of this input row: tile index
+            // row + lx + k + (4 - R) has the parity of k + 4 - R (row and lx
+            // are even), an odd index is read from the shifted copy
+            const int rowi = (ly0 + iy) * SW + lx + (4 - R);
             f2 pr[L - 1];
 #pragma unroll
-            for (int k = 0; k < L - 1; ++k)
-                asm("mov.b64 %0, {%1, %2};" : "=l"(pr[k]) : "f"(win[k]), "f"(win[k + 1]));
+            for (int k = 0; k < L - 1; ++k) {
+                const float* src = ((k + 4 - R) & 1) ? tile2 + rowi + k - 1 : tile + rowi + k;
+                pr[k] = *reinterpret_cast<const f2*>(src);
+            }
 #pragma unroll
             for (int wy = 0; wy < WPTY; ++wy) {
                 const int fy = iy - wy;

@@ -299,7 +299,9 @@ class ConvBenchmark(Benchmark):
     def smem_bytes(self, v) -> int:
         f = self.filt
         tw, th = v["TBX"] * v["WPTX"], v["TBY"] * v["WPTY"]
-        tile = (th + f - 1) * (tw + 8 + v["PAD"]) if v["LOCAL"] else 0
+        paired = v["LOCAL"] == 2 and v["WPTX"] % 2 == 0   # conv.cu PAIRED: two tile copies
+        tile = ((th + f - 1) * (tw + 8 + v["PAD"] * (2 if paired else 1)) * (2 if paired else 1)
+                if v["LOCAL"] else 0)
         return 4 * (tile + (f * f if v["CACHE_F"] else 0))
 
     def launch(self, v, bufs):

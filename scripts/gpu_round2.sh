@@ -15,5 +15,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pr
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_profile_search -c 1 -o gpurun_out/${TAG}_stress_full python scripts/search_sweep.py --nt auto --spaces stress:1048576 --reps 444 --outer 10 --kernel-only > gpurun_out/${TAG}_ncu_stress.log 2>&1
 ./scripts/micro/ffma2_rate > gpurun_out/${TAG}_ffma2.log 2>&1
 CT_LIB_PATH=paper_2102_05297_b200/libct_b200_clk.so timeout 300 python bench.py --steps 1 --warmup 3 --kernel-only > gpurun_out/${TAG}_clk.log 2>&1
+for r in 148 444 1000; do CT_LIB_PATH=paper_2102_05297_b200/libct_b200_clk.so timeout 300 python scripts/search_sweep.py --nt auto --spaces b200:transpose --reps $r --runs 1 > gpurun_out/${TAG}_clk_r$r.log 2>&1; done
 timeout 900 python scripts/profile_cost.py > gpurun_out/${TAG}_profile_cost.jsonl 2> gpurun_out/${TAG}_profile_cost.err
 for f in gpurun_out/${TAG}_*.log gpurun_out/${TAG}_*.err; do echo "== $f"; tail -n 3 "$f" | cut -c1-600; done
