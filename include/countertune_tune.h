@@ -109,6 +109,14 @@ int ct_tuner_profile_passes(ct_tuner* t, const char* const* metrics, int32_t n_m
  * [2] stream sync, [3] DecodeData, [4] metric evaluation, [5] number of
  * calls, [6] replay passes, [7] host-configuration builds.  reset != 0
  * clears the counters after reading. */
+/* A 2-D fp32 TMA tensor map (CUtensorMap, 128 bytes into out128) of the
+ * dim1 x dim0 row-major array at dev_ptr (dim0 contiguous, rows
+ * row_stride_bytes apart), box box1 x box0, no swizzle, no interleave --
+ * passed by value to kernels that load with cp.async.bulk.tensor. */
+int ct_tuner_tensor_map_2d(ct_tuner* t, uint64_t dev_ptr, uint64_t dim0, uint64_t dim1,
+                           uint64_t row_stride_bytes, uint32_t box0, uint32_t box1,
+                           void* out128);
+
 int ct_tuner_profile_timing(ct_tuner* t, double* out8, int32_t reset);
 
 #ifdef __cplusplus

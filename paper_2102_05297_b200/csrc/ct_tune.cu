@@ -43,6 +43,7 @@ struct DriverTable {
     CT_DRV(cuDevicePrimaryCtxRelease) CT_DRV(cuCtxSetCurrent) CT_DRV(cuGetErrorString)
     CT_DRV(cuModuleLoadData) CT_DRV(cuModuleGetFunction) CT_DRV(cuModuleUnload)
     CT_DRV(cuFuncGetAttribute) CT_DRV(cuFuncSetAttribute) CT_DRV(cuLaunchKernel)
+    CT_DRV(cuTensorMapEncodeTiled)
 #undef CT_DRV
     bool ready = false;
 };
@@ -66,6 +67,7 @@ bool load_driver() {
     CT_DRV(cuDevicePrimaryCtxRelease) CT_DRV(cuCtxSetCurrent) CT_DRV(cuGetErrorString)
     CT_DRV(cuModuleLoadData) CT_DRV(cuModuleGetFunction) CT_DRV(cuModuleUnload)
     CT_DRV(cuFuncGetAttribute) CT_DRV(cuFuncSetAttribute) CT_DRV(cuLaunchKernel)
+    CT_DRV(cuTensorMapEncodeTiled)
 #undef CT_DRV
     D.ready = ok;
     return ok;
@@ -628,6 +630,27 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     t->prof_us[5] += 1;
     t->prof_us[6] += used;
     if (passes) *passes = used;
+    return CT_TUNE_OK;
+}
+
+int ct_tuner_tensor_map_2d(ct_tuner* t, uint64_t dev_ptr, uint64_t dim0, uint64_t dim1,
+                           uint64_t row_stride_bytes, uint32_t box0, uint32_t box1,
+                           void* out128) {
+    int rc = activate(t); if (rc) return rc;
+    if (!dev_ptr || !out128 || !dim0 || !dim1 || !box0 || !box1 || (box0 * 4) % 16 ||
+        box0 > 256 || box1 > 256 || row_stride_bytes % 16)
+        return fail(CT_TUNE_ERR_VALUE, "bad tensor map geometry");
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {dim0, dim1};
+    const cuuint64_t strides[1] = {row_stride_bytes};
+    const cuuint32_t box[2] = {box0, box1};
+    const cuuint32_t estr[2] = {1, 1};
+    TU_CU(D.cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                   reinterpret_cast<void*>(dev_ptr), dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+    std::memcpy(out128, &map, sizeof(map));
     return CT_TUNE_OK;
 }
 

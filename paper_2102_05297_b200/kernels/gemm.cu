@@ -140,86 +140,143 @@ __device__ __forceinline__ void umma(unsigned tmem_d, unsigned long long da,
 #endif
 
 #if TC5
-// 5th-generation tensor-core path (see the header): per KWG slice the threads
-// stage A and B as tf32 big/small pairs in the K-major canonical layout, one
-// thread issues 3 x KWG/8 tcgen05.mma into the TMEM accumulator and commits
-// them to an mbarrier that every thread waits on before the next slice.
+// 5th-generation tensor-core path (see the header), a TMA-fed pipeline:
+//   * TMA (cp.async.bulk.tensor.2d) brings the fp32 slices A^T[k0:k0+KWG,
+//     m0:m0+128] and B[k0:k0+KWG, n0:n0+NWG] into a two-stage ring of raw
+//     tiles; an mbarrier per stage counts their bytes (expect_tx);
+//   * all threads split a landed slice into tf32 big / small halves in the
+//     K-major canonical operand layout (thread = one row x 4 k: four
+//     conflict-free scalar shared loads, two 16-byte shared stores), into a
+//     two-stage ring of operand buffers;
+//   * one thread issues the slice's 3 x KWG/8 tcgen05.mma into the TMEM
+//     accumulator and commits them to the stage's MMA mbarrier, then
+//     launches the TMA of slice s+2 into the raw stage just consumed.
+// The tensor core therefore works on slice s while the threads split slice
+// s+1 and the copy engine fetches slice s+2; an operand stage is rewritten
+// only after its MMAs completed (the MMA mbarrier of slice s-2).
+struct __align__(64) TensorMap { unsigned long long w[16]; };
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_wait(const unsigned long long* bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}\n"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void tma_2d(void* dst, const TensorMap* map, int c0, int c1,
+                                       unsigned long long* bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1, {%2, %3}], [%4];"
+                 :: "r"(smem_u32(dst)), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0),
+                    "r"(c1), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+constexpr int RAW_A = KWG * 128, RAW_B = KWG * NWG;          // floats per raw stage
+constexpr int OPS = 2 * 128 * KWG + 2 * NWG * KWG;           // big+small A, big+small B
+constexpr unsigned SLICE_BYTES = 4u * (RAW_A + RAW_B);
+
+// split raw [k][r] (row stride W floats) rows x KWG into big/small K-major
+template <int ROWS>
+__device__ __forceinline__ void split(const float* raw, float* big, float* small, int tid) {
+    constexpr int TASKS = ROWS * (KWG / 4);
+#pragma unroll
+    for (int t = tid; t < TASKS; t += NT) {
+        const int r = t % ROWS, kg = t / ROWS;
+        float v[4], hi[4], lo[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = raw[(4 * kg + j) * ROWS + r];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            hi[j] = __uint_as_float(tf32(v[j]));
+            lo[j] = __uint_as_float(tf32(v[j] - hi[j]));
+        }
+        const int o = kmaj(r, 4 * kg);
+        *reinterpret_cast<float4*>(big + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(small + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+}
+
 extern "C" __global__ void __launch_bounds__(NT)
 gemm(const float* __restrict__ at, const float* __restrict__ b, float* __restrict__ c, int M, int N,
-     int K) {
+     int K, const __grid_constant__ TensorMap tmA, const __grid_constant__ TensorMap tmB) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int m0 = blockIdx.x * MWG, n0 = blockIdx.y * NWG;
     extern __shared__ __align__(1024) float dsm[];
-    float* a_big = dsm;
-    float* a_small = a_big + 128 * KWG;
-    float* b_big = a_small + 128 * KWG;
-    float* b_small = b_big + NWG * KWG;
-    __shared__ __align__(8) unsigned long long mbar;
+    float* raw = dsm;                          // [2][RAW_A + RAW_B]
+    float* ops = dsm + 2 * (RAW_A + RAW_B);    // [2][OPS]
+    __shared__ __align__(8) unsigned long long full[2], done[2];
     __shared__ unsigned tmem_base;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"((unsigned)__cvta_generic_to_shared(&tmem_base)), "n"(TMEM_COLS));
+                     :: "r"(smem_u32(&tmem_base)), "n"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    const int nk = K / KWG;
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;"
-                     :: "r"((unsigned)__cvta_generic_to_shared(&mbar)));
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&done[i])));
+        }
         asm volatile("fence.mbarrier_init.release.cluster;");
+        asm volatile("fence.proxy.async.shared::cta;");
+        for (int s = 0; s < 2 && s < nk; ++s) {
+            float* rs = raw + s * (RAW_A + RAW_B);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         :: "r"(smem_u32(&full[s])), "r"(SLICE_BYTES) : "memory");
+            tma_2d(rs, &tmA, m0, s * KWG, &full[s]);
+            tma_2d(rs + RAW_A, &tmB, n0, s * KWG, &full[s]);
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const unsigned tmem_d = tmem_base;
-    unsigned phase = 0;
-    for (int k0 = 0; k0 < K; k0 += KWG) {
-        // stage: A(m, k) = at[k][m], B(n, k) = b[k][n]; coalesced reads along m / n
-        // a warp stages 8 rows x 4 k per step: lane l takes row 8q + l%8 and
-        // k 4p + l/8, so the loads are four full 32-byte sectors and the 32
-        // shared stores hit 32 different banks (bank = (r%8)*4 + k%4)
-        const int lr = lane & 7, lk = lane >> 3;
-        for (int blk = warp; blk < 16 * (KWG / 4); blk += NT / 32) {
-            const int m = (blk & 15) * 8 + lr, k = (blk >> 4) * 4 + lk;
-            const float v = at[(size_t)(k0 + k) * M + m0 + m];
-            const float hi = __uint_as_float(tf32(v));
-            a_big[kmaj(m, k)] = hi;
-            a_small[kmaj(m, k)] = __uint_as_float(tf32(v - hi));
-        }
-        for (int blk = warp; blk < (NWG / 8) * (KWG / 4); blk += NT / 32) {
-            const int n = (blk % (NWG / 8)) * 8 + lr, k = (blk / (NWG / 8)) * 4 + lk;
-            const float v = b[(size_t)(k0 + k) * N + n0 + n];
-            const float hi = __uint_as_float(tf32(v));
-            b_big[kmaj(n, k)] = hi;
-            b_small[kmaj(n, k)] = __uint_as_float(tf32(v - hi));
-        }
-        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+    for (int s = 0; s < nk; ++s) {
+        const int st = s & 1;
+        const unsigned ph = (unsigned)(s >> 1) & 1u;
+        float* rs = raw + st * (RAW_A + RAW_B);
+        float* os = ops + st * OPS;
+        float* a_big = os;
+        float* a_small = a_big + 128 * KWG;
+        float* b_big = a_small + 128 * KWG;
+        float* b_small = b_big + NWG * KWG;
+        mbar_wait(&full[st], ph);                       // slice s landed
+        if (s >= 2) mbar_wait(&done[st], ph ^ 1u);      // MMAs of slice s-2 done: stage free
+        split<128>(rs, a_big, a_small, tid);
+        split<NWG>(rs + RAW_A, b_big, b_small, tid);
+        // generic-proxy shared stores -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;");
         __syncthreads();
         if (tid == 0) {
+            if (s + 2 < nk) {      // every thread is done reading this raw stage
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             :: "r"(smem_u32(&full[st])), "r"(SLICE_BYTES) : "memory");
+                tma_2d(rs, &tmA, m0, (s + 2) * KWG, &full[st]);
+                tma_2d(rs + RAW_A, &tmB, n0, (s + 2) * KWG, &full[st]);
+            }
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
             for (int kk = 0; kk < KWG / 8; ++kk) {
                 const int off = kk * 64;   // 8 k = two 4-k core-matrix columns = 256 B
-                const unsigned acc0 = (k0 > 0 || kk > 0) ? 1u : 0u;
+                const unsigned acc0 = (s > 0 || kk > 0) ? 1u : 0u;
                 umma(tmem_d, sdesc(a_small + off), sdesc(b_big + off), acc0);
                 umma(tmem_d, sdesc(a_big + off), sdesc(b_small + off), 1u);
                 umma(tmem_d, sdesc(a_big + off), sdesc(b_big + off), 1u);
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                         :: "r"((unsigned)__cvta_generic_to_shared(&mbar)));
+                         :: "r"(smem_u32(&done[st])) : "memory");
         }
-        // the slice's MMAs are complete (smem reusable, accumulator current)
-        {
-            unsigned done = 0;
-            while (!done) {
-                asm volatile("{\n\t.reg .pred p;\n\t"
-                             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                             "selp.u32 %0, 1, 0, p;\n\t}\n"
-                             : "=r"(done) : "r"((unsigned)__cvta_generic_to_shared(&mbar)), "r"(phase));
-            }
-            phase ^= 1;
-        }
-        asm volatile("tcgen05.fence::after_thread_sync;");
     }
+    // the last commit completes after every earlier MMA
+    mbar_wait(&done[(nk - 1) & 1], (unsigned)((nk - 1) >> 1) & 1u);
+    asm volatile("tcgen05.fence::after_thread_sync;");
     // epilogue: warps 0..3 read rows 32q + lane of the accumulator
     if (warp < 4) {
         const int row = warp * 32 + lane;

@@ -342,6 +342,8 @@ class GemmBenchmark(Benchmark):
 
     def setup(self, tuner):
         h = self.host_inputs()
+        self._tuner = tuner
+        self._maps = {}
         return {"at": tuner.upload(h["at"]), "b": tuner.upload(h["b"]),
                 "c": tuner.alloc(4 * self.m * self.n)}
 
@@ -352,13 +354,30 @@ class GemmBenchmark(Benchmark):
         return v["TC"] == 1 and v["MWG"] == 128 and v["MDIMC"] * v["NDIMC"] >= 128
 
     def smem_bytes(self, v) -> int:
-        # tf32 big/small tiles of A (128 x KWG) and B (NWG x KWG) for tcgen05
-        return 4 * v["KWG"] * (2 * 128 + 2 * v["NWG"]) if self.tc5(v) else 0
+        # tcgen05 pipeline (gemm.cu): two raw fp32 stages of A^T (KWG x 128)
+        # and B (KWG x NWG) for the TMA, two stages of tf32 big/small operand
+        # tiles, after 1 KB of alignment for the static barriers
+        if not self.tc5(v):
+            return 0
+        return 1024 + 8 * v["KWG"] * (384 + 3 * v["NWG"])
+
+    def tensor_maps(self, v, bufs):
+        """TMA descriptors of A^T (box 128 x KWG) and B (box NWG x KWG)."""
+        key = (v["KWG"], v["NWG"])
+        if key not in self._maps:
+            t = self._tuner
+            self._maps[key] = (
+                t.tensor_map_2d(bufs["at"], self.m, self.k, 4 * self.m, 128, v["KWG"]),
+                t.tensor_map_2d(bufs["b"], self.n, self.k, 4 * self.n, v["NWG"], v["KWG"]))
+        return self._maps[key]
 
     def launch(self, v, bufs):
+        args = [_u64(bufs["at"]), _u64(bufs["b"]), _u64(bufs["c"]), _i32(self.m), _i32(self.n),
+                _i32(self.k)]
+        if self.tc5(v):
+            args += list(self.tensor_maps(v, bufs))
         return Launch((self.m // v["MWG"], self.n // v["NWG"]), (v["MDIMC"] * v["NDIMC"],),
-                      [_u64(bufs["at"]), _u64(bufs["b"]), _u64(bufs["c"]), _i32(self.m),
-                       _i32(self.n), _i32(self.k)], dynamic_smem=self.smem_bytes(v))
+                      args, dynamic_smem=self.smem_bytes(v))
 
     def output(self, tuner, bufs):
         return tuner.d2h(bufs["c"], np.empty((self.m, self.n), np.float32))
@@ -423,8 +442,12 @@ class CudaMeasurementSource:
         return bad
 
     def reset_variants(self) -> None:
-        """Forget the compiled variants (the next measure() compiles again,
-        as a fresh tuning session would)."""
+        """Unload the compiled variants (the next measure() compiles again,
+        as a fresh tuning session would).  The modules are unloaded, not just
+        forgotten: every module left loaded in the context would stay there
+        for the rest of the process."""
+        for v in self._variants.values():
+            self.tuner.unload(v)
         self._variants.clear()
 
     def variant(self, config_index: int) -> int:

@@ -75,6 +75,8 @@ SIGNATURES = {
                                         _P(ctypes.c_double), _P(_i32)]),
     "ct_tuner_profile_passes": (ctypes.c_int, [_vp, _P(_cp), _i32, _P(_i32)]),
     "ct_tuner_profile_timing": (ctypes.c_int, [_vp, _P(ctypes.c_double), _i32]),
+    "ct_tuner_tensor_map_2d": (ctypes.c_int, [_vp, _u64, _u64, _u64, _u64, ctypes.c_uint32,
+                                              ctypes.c_uint32, _vp]),
 }
 
 _lib = None
@@ -263,6 +265,16 @@ class Tuner:
                                           vals.ctypes.data_as(_P(ctypes.c_double)),
                                           ctypes.byref(passes)))
         return vals, passes.value
+
+    def tensor_map_2d(self, ptr: int, dim0: int, dim1: int, row_stride_bytes: int, box0: int,
+                      box1: int):
+        """128-byte fp32 TMA descriptor (ct_tuner_tensor_map_2d), as a kernel
+        argument (ctypes array of 16 uint64)."""
+        out = (ctypes.c_uint64 * 16)()
+        _check(self._lib.ct_tuner_tensor_map_2d(self._h, int(ptr), int(dim0), int(dim1),
+                                                int(row_stride_bytes), int(box0), int(box1),
+                                                ctypes.cast(out, _vp)))
+        return out
 
     PROFILE_PHASES = ("setconfig_us", "passes_us", "sync_us", "decode_us", "evaluate_us",
                       "calls", "replay_passes", "host_config_us")

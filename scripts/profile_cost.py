@@ -62,6 +62,20 @@ def main():
             out[f"{label}_passes"] = passes
             out[f"{label}_phases_us"] = {k: round(v_ / a.reps, 1) for k, v_ in
                                          t.profile_timing(reset=True).items()}
+        if name in ("coulomb", "transpose"):
+            # the same profiled step with the whole space's modules loaded
+            # in the context (the state a session without unloads reaches)
+            t0 = time.perf_counter()
+            bad = src.compile_all()
+            out["compile_all_s"] = time.perf_counter() - t0
+            out["modules_loaded"] = len(src._variants)
+            t0 = time.perf_counter()
+            for _ in range(a.reps):
+                src.measure(best, profiled=True)
+            out["profiled_step_all_modules_s"] = (time.perf_counter() - t0) / a.reps
+            out["profiled_all_modules_phases_us"] = {k: round(v_ / a.reps, 1) for k, v_ in
+                                                     t.profile_timing(reset=True).items()}
+            del bad
         src.close()
         print(json.dumps(out), flush=True)
 
