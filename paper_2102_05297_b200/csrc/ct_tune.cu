@@ -152,6 +152,11 @@ struct ct_tuner {
     std::string chip;
     std::vector<uint8_t> avail;
     CUpti_RangeProfiler_Object* rp = nullptr;
+    // the metric set the range-profiler object was last configured with: a
+    // SetConfig with another set does not take effect on the same object
+    // (it keeps the first set's pass count and leaves the new metrics NaN),
+    // so a switch of set re-creates the object
+    const void* rp_config = nullptr;
     // host configurations by metric set (building one costs milliseconds)
     std::map<std::string, std::unique_ptr<HostConfig>> configs;
     // wall time of ct_tuner_profile by phase (microseconds, accumulated):
@@ -550,6 +555,16 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     const auto t0 = clk::now();
     HostConfig* hc = nullptr;
     rc = host_config_cached(t, metrics, n, &hc); if (rc) return rc;
+    if (t->rp_config && t->rp_config != hc) {
+        CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
+        dp.pRangeProfilerObject = t->rp;
+        TU_CUPTI(cuptiRangeProfilerDisable(&dp));
+        CUpti_RangeProfiler_Enable_Params ep = {CUpti_RangeProfiler_Enable_Params_STRUCT_SIZE};
+        ep.ctx = t->ctx;
+        TU_CUPTI(cuptiRangeProfilerEnable(&ep));
+        t->rp = ep.pRangeProfilerObject;
+    }
+    t->rp_config = hc;
     const auto t1 = clk::now();
     t->prof_us[7] += us(t0, t1);
     // counter data image for one range (re-initialised per collection)

@@ -72,7 +72,16 @@ constexpr int LH = TH + F - 1;                    // tile rows incl. halo
 constexpr int V4 = (TW + 8) / 4;                  // float4 per staged row: x0-4 .. x0+TW+3
 // packed-FMA path (see above): two copies of the tile, the second shifted by
 // one float, so that every window pair is one aligned 8-byte shared load
-constexpr bool PAIRED = (LOCAL == 2) && (WPTX % 2 == 0);
+// (only where the doubled tile still fits the 227 KB per-block limit; a
+// preprocessor test, since it also selects the packed code path below)
+#define CONV_PAIRED_SMEM (4 * (2 * (TBY * WPTY + FILTER - 1) * ((TBX * WPTX + 8) / 4 * 4 + 2 * PAD) \
+                              + (CACHE_F ? FILTER * FILTER : 0)))
+#if LOCAL == 2 && WPTX % 2 == 0 && CONV_PAIRED_SMEM <= 227 * 1024
+#define CONV_PAIRED 1
+#else
+#define CONV_PAIRED 0
+#endif
+constexpr bool PAIRED = CONV_PAIRED;
 constexpr int SW = PAIRED ? 4 * V4 + 2 * PAD : 4 * V4 + PAD;   // shared row stride (even if PAIRED)
 static_assert(F <= 9, "the staged row holds a halo of at most 4 columns per side");
 constexpr int NT = TBX * TBY;
@@ -139,7 +148,7 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter 
 #pragma unroll
         for (int i = 0; i < WPTX; ++i) acc[wy][i] = 0.0f;
 
-#if LOCAL == 2 && WPTX % 2 == 0
+#if CONV_PAIRED
     {
         // output pairs (2h, 2h + 1); the window row as overlapping pairs
         // pr[k] = (in[k], in[k + 1]), each one 8-byte shared load

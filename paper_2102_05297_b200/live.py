@@ -299,10 +299,13 @@ class ConvBenchmark(Benchmark):
     def smem_bytes(self, v) -> int:
         f = self.filt
         tw, th = v["TBX"] * v["WPTX"], v["TBY"] * v["WPTY"]
-        paired = v["LOCAL"] == 2 and v["WPTX"] % 2 == 0   # conv.cu PAIRED: two tile copies
+        filt = f * f if v["CACHE_F"] else 0
+        # conv.cu PAIRED: two tile copies, where the doubled tile fits 227 KB
+        paired = (v["LOCAL"] == 2 and v["WPTX"] % 2 == 0
+                  and 4 * (2 * (th + f - 1) * (tw + 8 + 2 * v["PAD"]) + filt) <= 227 * 1024)
         tile = ((th + f - 1) * (tw + 8 + v["PAD"] * (2 if paired else 1)) * (2 if paired else 1)
                 if v["LOCAL"] else 0)
-        return 4 * (tile + (f * f if v["CACHE_F"] else 0))
+        return 4 * (tile + filt)
 
     def launch(self, v, bufs):
         tw, th = v["TBX"] * v["WPTX"], v["TBY"] * v["WPTY"]

@@ -191,10 +191,14 @@ def test_distributed_live_search_world1_matches_device_search():
 
 
 @pytest.mark.parametrize("name,rtol", [("coulomb", 2e-6), ("nbody", 2e-6), ("conv", 1e-6),
-                                       ("gemm", 1e-6), ("transpose", 0.0)])
+                                       ("gemm", 1.1e-5), ("transpose", 0.0)])
 def test_best_configuration_at_paper_size_matches_oracle(tuner, name, rtol):
     """The exhaustive sweep's best configuration of every space, at the
-    paper's input size, against the oracle."""
+    paper's input size, against the oracle.
+
+    GEMM at K = 2048: FP32 accumulation of 2048 products, tolerance
+    4 sqrt(K) 2^-24 = 1.1e-5 of the magnitude sum (the rigorous worst case of
+    a K-term FP32 sum is K 2^-24 = 1.2e-4; the K = 128 tests use 1e-6)."""
     import os
     from paper_2102_05297_b200 import formats
     from paper_2102_05297_b200.live import CudaMeasurementSource, benchmark

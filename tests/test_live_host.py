@@ -53,6 +53,8 @@ def test_launch_geometry_covers_problem(name):
     b = live.benchmark(name)
     bufs = {k: 0 for k in ("in", "out", "atoms", "x", "y", "z", "w", "energy", "pm", "m",
                            "acc", "filt", "at", "b", "c", "partial", "arrivals")}
+    if name == "gemm":      # TMA descriptors need a device context; geometry does not
+        b.tensor_maps = lambda v, bufs: ()
     for i in range(len(b.space)):
         v = b.values(i)
         l = b.launch(v, bufs)
