@@ -18,6 +18,7 @@
 
 #include "countertune_b200.h"
 #include "ct_search.cuh"
+#include "ct_tiled.cuh"
 #include "ct_models.cuh"
 
 using namespace ct;
@@ -126,6 +127,9 @@ struct ct_ctx {
     // scratch
     DevBuf<double> scratch_w;
     DevBuf<unsigned char> scratch_head;
+    DevBuf<unsigned char> scratch_tiled;   // tiled path: state, row totals, bits, partials
+    DevBuf<int32_t> tiled_live;            // tiled path: live repetitions (+ host mirror below)
+    int32_t* tiled_live_host = nullptr;
     DevBuf<int32_t> scratch_perm;
     // single-call buffers
     DevBuf<double> vec_a, vec_b;
@@ -733,6 +737,103 @@ int launch_profile_ws_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
     return CT_OK;
 }
 
+// tiled path (ct_tiled.cuh): grid-wide phase kernels per outer iteration,
+// the repetitions in batches that fit the scratch budget
+__global__ void k_tiled_count_live(const TiledArgs t, int32_t* live) {
+    int c = 0;
+    for (int b = threadIdx.x; b < t.batch; b += blockDim.x) c += t.state[b].live;
+    c = __reduce_add_sync(FULL, c);
+    if ((threadIdx.x & 31) == 0) atomicAdd(live, c);
+}
+
+int launch_tiled(ct_ctx* ctx, SearchArgs& a, int n_reps) {
+    const int64_t ntiles = (a.n + TILE_CONFIGS - 1) / TILE_CONFIGS;
+    const int64_t w_stride = (int64_t)a.nrows * 32;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t per_rep = al(sizeof(TiledRep)) + al(8 * (size_t)a.nrows) + al(4 * (size_t)a.nwords) +
+                           al(sizeof(double4) * (size_t)ntiles);
+    const size_t per_rep_all = per_rep + 8 * (size_t)w_stride;
+    size_t free_b = 0, total_b = 0;
+    CT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    size_t budget = std::min<size_t>(free_b / 2, (size_t)48 << 30);
+    if (const char* env = std::getenv("CT_TILED_BUDGET_MB")) budget = (size_t)std::atoll(env) << 20;
+    const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(n_reps, (int64_t)(budget / per_rep_all)));
+    CT_CUDA(ctx->scratch_w.ensure((size_t)batch * w_stride));
+    CT_CUDA(ctx->scratch_tiled.ensure((size_t)batch * per_rep));
+    CT_CUDA(ctx->tiled_live.ensure(1));
+    if (!ctx->tiled_live_host) CT_CUDA(cudaMallocHost(&ctx->tiled_live_host, sizeof(int32_t)));
+    unsigned char* base = ctx->scratch_tiled.p;
+    TiledArgs t;
+    t.state = reinterpret_cast<TiledRep*>(base);
+    base += al(sizeof(TiledRep) * (size_t)batch);
+    t.row_tot = reinterpret_cast<double*>(base);
+    base += al(8 * (size_t)a.nrows * batch);
+    t.expl = reinterpret_cast<uint32_t*>(base);
+    base += al(4 * (size_t)a.nwords * batch);
+    t.partial = reinterpret_cast<double4*>(base);
+    t.w = ctx->scratch_w.p;
+    t.w_stride = w_stride;
+    t.ntiles = (int32_t)ntiles;
+    for (int r0 = 0; r0 < n_reps; r0 += batch) {
+        t.rep0 = r0;
+        t.batch = std::min(batch, n_reps - r0);
+        const int warps_grid = (t.batch + 3) / 4;
+        const dim3 tiles((unsigned)t.batch, (unsigned)ntiles);
+        k_tiled_begin<<<warps_grid, 128, 0, ctx->stream>>>(a, t);
+        CT_CUDA(cudaGetLastError());
+        for (int it = 0; it < a.outer; ++it) {
+            k_tiled_score<<<tiles, TILED_NT, 0, ctx->stream>>>(a, t);
+            k_tiled_reduce<<<warps_grid, 128, 0, ctx->stream>>>(a, t);
+            k_tiled_weights<<<tiles, TILED_NT, 0, ctx->stream>>>(a, t);
+            k_tiled_draw<<<warps_grid, 128, 0, ctx->stream>>>(a, t);
+            CT_CUDA(cudaGetLastError());
+            // stop launching once every repetition of the batch has ended
+            // (searches run until a stop configuration / exhaustion)
+            if ((it & 15) == 15 && it + 1 < a.outer) {
+                CT_CUDA(cudaMemsetAsync(ctx->tiled_live.p, 0, sizeof(int32_t), ctx->stream));
+                k_tiled_count_live<<<1, 256, 0, ctx->stream>>>(t, ctx->tiled_live.p);
+                CT_CUDA(cudaMemcpyAsync(ctx->tiled_live_host, ctx->tiled_live.p, sizeof(int32_t),
+                                        cudaMemcpyDeviceToHost, ctx->stream));
+                CT_CUDA(cudaStreamSynchronize(ctx->stream));
+                if (*ctx->tiled_live_host == 0) break;
+            }
+        }
+    }
+    return CT_OK;
+}
+
+// spaces above this size take the tiled path by default
+constexpr int64_t TILED_MIN_N = 1ll << 40;   // set from measurements
+
+// shared-queue kernel: S repetition slots per CTA of W warps, NCH chunks per phase
+template <int W, int S, int NCH, int MINB, bool SMEM, bool PRE>
+int launch_profile_mq_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
+    auto kern = k_profile_search_mq<W, S, NCH, MINB, SMEM, PRE>;
+    // (the opt-in limit counts the ~4-8 KB of static control blocks too)
+    if (smem > 32 * 1024)
+        CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
+    if (occ < 1) return fail(CT_ERR_CUDA, "search kernel does not fit on an SM");
+    int grid = std::min((n_reps + S - 1) / S, occ * ctx->sm_count);
+    if (!SMEM) {
+        CT_CUDA(ctx->scratch_w.ensure((size_t)S * grid * 64 * (size_t)a.nrows));
+        a.scratch_w = ctx->scratch_w.p;
+    }
+    kern<<<grid, 32 * W, smem, ctx->stream>>>(a);
+    CT_CUDA(cudaGetLastError());
+    return CT_OK;
+}
+
+template <int W, int S, int NCH, int MINB>
+int launch_profile_mq(ct_ctx* ctx, SearchArgs& a, bool pre, bool in_smem, size_t smem, int n_reps) {
+    if (pre)
+        return in_smem ? launch_profile_mq_t<W, S, NCH, MINB, true, true>(ctx, a, smem, n_reps)
+                       : launch_profile_mq_t<W, S, NCH, MINB, false, true>(ctx, a, smem, n_reps);
+    return in_smem ? launch_profile_mq_t<W, S, NCH, MINB, true, false>(ctx, a, smem, n_reps)
+                   : launch_profile_mq_t<W, S, NCH, MINB, false, false>(ctx, a, smem, n_reps);
+}
+
 template <int PW>
 int launch_profile_ws(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int n_reps) {
     return in_smem ? launch_profile_ws_t<PW, true>(ctx, a, smem, n_reps)
@@ -803,6 +904,8 @@ int ct_destroy(ct_ctx* ctx) {
     ctx->stop_bits.release(); ctx->step_index.release(); ctx->step_profiled.release();
     ctx->n_steps.release(); ctx->status.release(); ctx->rep_error.release();
     ctx->stats.release(); ctx->scratch_w.release(); ctx->scratch_head.release();
+    ctx->scratch_tiled.release(); ctx->tiled_live.release();
+    if (ctx->tiled_live_host) { cudaFreeHost(ctx->tiled_live_host); ctx->tiled_live_host = nullptr; }
     ctx->col_flags.release(); ctx->table_rm.release(); ctx->col_part.release();
     ctx->scratch_perm.release(); ctx->vec_a.release();
     ctx->vec_b.release(); ctx->mask_a.release(); ctx->mask_b.release(); ctx->key_a.release();
@@ -1202,6 +1305,11 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     bool pre = a.nrows < 32;
     if (const char* env = std::getenv("CT_SEARCH_PRE")) pre = std::atoi(env) != 0;
     const size_t pref_b = (pre ? 16 : 8) * 32 * (size_t)a.nrows;   // weights [+ in-row prefixes]
+    // large spaces: grid-wide phase kernels (ct_tiled.cuh); CT_SEARCH_TILED
+    // forces (1) or disables (0) the path
+    int tiled = (n > TILED_MIN_N && a.topk < 0) ? 1 : 0;
+    if (const char* env = std::getenv("CT_SEARCH_TILED")) tiled = std::atoi(env) != 0 && a.topk < 0;
+    if (tiled) return launch_tiled(ctx, a, n_reps);
     if (head_b > budget) {
         // the row index (row totals + explored bits) outgrows shared memory:
         // all per-repetition state in a per-CTA slice of global scratch
@@ -1216,6 +1324,35 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     bool in_smem = head_b + pref_b <= per_cta_cap;
     if (const char* env = std::getenv("CT_SEARCH_SMEM")) in_smem = std::atoi(env) != 0 && head_b + pref_b <= budget;
     const size_t smem = head_b + (in_smem ? pref_b : 0);
+    // shared-queue kernel (CT_SEARCH_MQ = "W,S,NCH": warps per CTA, repetition
+    // slots per CTA, chunks per parallel phase)
+    int mq_w = 0, mq_s = 0, mq_nch = 0;
+    if (const char* env = std::getenv("CT_SEARCH_MQ")) {
+        if (std::sscanf(env, "%d,%d,%d", &mq_w, &mq_s, &mq_nch) != 3) mq_w = 0;
+    }
+    if (mq_w > 0 && a.topk < 0) {
+        const int64_t ctas = (n_reps + mq_s - 1) / mq_s;
+        const int64_t per_sm = std::max<int64_t>(1, (ctas + ctx->sm_count - 1) / ctx->sm_count);
+        // (the per-slot control blocks take up to ~8 KB of static shared memory)
+        const size_t cap = std::min<size_t>((size_t)(228 * 1024 / per_sm) - 3 * 1024,
+                                            219 * 1024);
+        if ((size_t)mq_s * head_b <= cap) {
+            bool mq_smem = (size_t)mq_s * (head_b + pref_b) <= cap;
+            if (const char* env = std::getenv("CT_SEARCH_SMEM"))
+                mq_smem = std::atoi(env) != 0 && (size_t)mq_s * (head_b + pref_b) <= 219 * 1024;
+            const size_t smem_mq = (size_t)mq_s * (head_b + (mq_smem ? pref_b : 0));
+            switch (mq_w * 10000 + mq_s * 100 + mq_nch) {
+            case 40104: return launch_profile_mq<4, 1, 4, 7>(ctx, a, pre, mq_smem, smem_mq, n_reps);
+            case 60204: return launch_profile_mq<6, 2, 4, 4>(ctx, a, pre, mq_smem, smem_mq, n_reps);
+            case 80204: return launch_profile_mq<8, 2, 4, 4>(ctx, a, pre, mq_smem, smem_mq, n_reps);
+            case 80304: return launch_profile_mq<8, 3, 4, 3>(ctx, a, pre, mq_smem, smem_mq, n_reps);
+            case 120304: return launch_profile_mq<12, 3, 4, 2>(ctx, a, pre, mq_smem, smem_mq, n_reps);
+            case 120404: return launch_profile_mq<12, 4, 4, 2>(ctx, a, pre, mq_smem, smem_mq, n_reps);
+            case 160404: return launch_profile_mq<16, 4, 4, 2>(ctx, a, pre, mq_smem, smem_mq, n_reps);
+            default: return fail(CT_ERR_VALUE, "CT_SEARCH_MQ: no such build");
+            }
+        }
+    }
     // warp-specialised two-repetition kernel (CT_SEARCH_WS = parallel warps)
     int ws = 0;
     if (const char* env = std::getenv("CT_SEARCH_WS")) ws = std::atoi(env);

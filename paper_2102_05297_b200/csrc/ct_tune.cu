@@ -121,6 +121,10 @@ namespace {
 // Host configuration of a metric set: config image + pass count.
 struct HostConfig {
     CUpti_Profiler_Host_Object* host = nullptr;
+    // the metric names, owned here: every CUPTI call of this configuration
+    // gets these pointers, never the caller's (which live for one call)
+    std::vector<std::string> names;
+    std::vector<const char*> name_ptrs;
     std::vector<uint8_t> image;
     size_t passes = 0;
     std::vector<uint8_t> counter_data;   // one-range counter data image
@@ -266,7 +270,11 @@ int cupti_init(ct_tuner* t) {
     return CT_TUNE_OK;
 }
 
-int host_config(ct_tuner* t, const char* const* metrics, int32_t n, HostConfig* hc) {
+int host_config(ct_tuner* t, const char* const* metrics_in, int32_t n, HostConfig* hc) {
+    hc->names.assign(metrics_in, metrics_in + n);
+    hc->name_ptrs.clear();
+    for (const std::string& m : hc->names) hc->name_ptrs.push_back(m.c_str());
+    const char* const* metrics = hc->name_ptrs.data();
     CUpti_Profiler_Host_Initialize_Params hp = {sizeof(CUpti_Profiler_Host_Initialize_Params)};
     hp.profilerType = CUPTI_PROFILER_TYPE_RANGE_PROFILER;
     hp.pChipName = t->chip.c_str();
@@ -571,7 +579,7 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     if (hc->counter_data.empty()) {
         CUpti_RangeProfiler_GetCounterDataSize_Params cs = {CUpti_RangeProfiler_GetCounterDataSize_Params_STRUCT_SIZE};
         cs.pRangeProfilerObject = t->rp;
-        cs.pMetricNames = const_cast<const char**>(metrics);
+        cs.pMetricNames = hc->name_ptrs.data();
         cs.numMetrics = (size_t)n;
         cs.maxNumOfRanges = 1;
         cs.maxNumRangeTreeNodes = 1;
@@ -632,7 +640,7 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     ev.pCounterDataImage = data.data();
     ev.counterDataImageSize = data.size();
     ev.rangeIndex = 0;
-    ev.ppMetricNames = const_cast<const char**>(metrics);
+    ev.ppMetricNames = hc->name_ptrs.data();
     ev.numMetrics = (size_t)n;
     ev.pMetricValues = values;
     TU_CUPTI(cuptiProfilerHostEvaluateToGpuValues(&ev));

@@ -53,6 +53,7 @@ def main():
         for label, ms in (("sass_group4", sass), ("group1_13", group1),
                           ("non_sass", [m for m in live.TABLE1_METRICS if m not in sass]),
                           ("all24", list(live.TABLE1_METRICS))):
+            print(f"[profile_cost] {name}: {label}", file=sys.stderr, flush=True)
             t.profile(v, launch, ms)                 # host config built outside the timing
             t.profile_timing(reset=True)
             t0 = time.perf_counter()

@@ -5,8 +5,10 @@
   thread-level FP32 instruction count = threads x NFMA exactly, shared-load
   wavefronts = warps x NLDS exactly, executed warp instructions exactly
   linear in the grid size, full warps (WARP_E = WARP_NP_E = 100%);
-* the 8192^2 transpose: DRAM read / write sectors within 5% of the
-  algorithmic 4 n^2 / 32 each;
+* the 8192^2 transpose: DRAM read sectors within 5% of the algorithmic
+  4 n^2 / 32, write sectors within [4 n^2 - L2 bytes, 1.05 x 4 n^2] / 32
+  (the lines still dirty in the L2 at kernel end are written back outside
+  the range);
 * two collections of the same launch agree within 1% (the deterministic
   counters exactly).
 """
@@ -80,7 +82,12 @@ def test_transpose_dram_sectors_match_algorithmic_bytes(tuner):
     n = 8192
     sectors = 4 * n * n / 32
     assert abs(a[0] - sectors) / sectors < 0.05, a
-    assert abs(a[1] - sectors) / sectors < 0.05, a
+    # writes: the lines still dirty in the L2 when the kernel ends are
+    # written back after the range closes, so up to one L2 (126 MB on B200)
+    # of the algorithmic writes goes uncounted
+    import torch
+    l2_sectors = torch.cuda.get_device_properties(0).L2_cache_size / 32
+    assert sectors - l2_sectors <= a[1] <= 1.05 * sectors, a
     assert a[2] >= 0.95 * sectors and a[3] >= 0.95 * sectors, a
     np.testing.assert_allclose(a[:4], b[:4], rtol=0.01)
     assert a[4] == b[4] and a[5] == b[5]        # instruction counts are deterministic

@@ -50,6 +50,43 @@ def test_kernel_variants_match_reference(name, env, monkeypatch):
     _check_trajectories(name)
 
 
+# the shared-queue kernel (k_profile_search_mq<W, S, NCH>): S repetition slots
+# per CTA of W warps, NCH chunks per parallel phase, any warp runs any slot's
+# chunks and serial phases -- every build on every trajectory set (the PRE
+# layout on the small spaces), and with the weights in a global slice
+MQ_BUILDS = ["4,1,4", "6,2,4", "8,2,4", "8,3,4", "12,3,4", "12,4,4", "16,4,4"]
+
+
+@pytest.mark.parametrize("mq", MQ_BUILDS)
+@pytest.mark.parametrize("name", TRAJ_SETS)
+def test_shared_queue_kernel_matches_reference(name, mq, monkeypatch):
+    monkeypatch.setenv("CT_SEARCH_MQ", mq)
+    _check_trajectories(name)
+
+
+@pytest.mark.parametrize("mq", ["8,3,4", "12,4,4"])
+def test_shared_queue_kernel_global_weights_matches_reference(mq, monkeypatch):
+    monkeypatch.setenv("CT_SEARCH_MQ", mq)
+    monkeypatch.setenv("CT_SEARCH_SMEM", "0")
+    _check_trajectories("b200_transpose")
+
+
+# the tiled large-space path (ct_tiled.cuh: grid-wide Eq. 16 / Eq. 17 kernels
+# per outer iteration, one warp per repetition for the draws), forced on every
+# trajectory set (tiles of 4096 configurations: one partial tile here)
+@pytest.mark.parametrize("name", TRAJ_SETS)
+def test_tiled_path_matches_reference(name, monkeypatch):
+    monkeypatch.setenv("CT_SEARCH_TILED", "1")
+    _check_trajectories(name)
+
+
+def test_tiled_path_small_batches_match_reference(monkeypatch):
+    """A scratch budget of 1 MB forces repetition batches of a few each."""
+    monkeypatch.setenv("CT_SEARCH_TILED", "1")
+    monkeypatch.setenv("CT_TILED_BUDGET_MB", "1")
+    _check_trajectories("b200_gemm")
+
+
 def _check_trajectories(name):
     from paper_2102_05297_b200 import _native
     from paper_2102_05297_b200.search import search_params
@@ -276,12 +313,15 @@ def test_large_space_properties():
         assert idx2[r, :nst2[r]].tolist() == res.step_index[3 + r, :res.n_steps[3 + r]].tolist()
 
 
-def test_gemm_full_trajectories_match_reference_with_uncertified_draws():
+@pytest.mark.parametrize("tiled", ["0", "1"], ids=["persistent", "tiled"])
+def test_gemm_full_trajectories_match_reference_with_uncertified_draws(tiled, monkeypatch):
     """N = 205,216 (GEMM-full): 256 repetitions x 40 iterations x 5 draws
     against the reference's own trajectories (make_gemmfull_golden.py).  At
     this size the certificate rejects some draws, which the device re-decides
     with the sequential cumsum: the run must contain such draws and still
-    match the reference everywhere."""
+    match the reference everywhere -- with the per-repetition persistent
+    kernel and with the tiled large-space path."""
+    monkeypatch.setenv("CT_SEARCH_TILED", tiled)
     from paper_2102_05297_b200 import ExactModelSet, _native, spaces
     from paper_2102_05297_b200.search import PredictionTable, search_params
     from paper_2102_05297_b200.space import replay_arrays
@@ -447,12 +487,15 @@ def test_reference_acceptance_criterion_6_portability():
     assert improvement == float(g["c6_improvement"])
 
 
-def test_stress_space_global_row_index_matches_oracle():
+@pytest.mark.parametrize("tiled", ["0", "1"], ids=["persistent", "tiled"])
+def test_stress_space_global_row_index_matches_oracle(tiled, monkeypatch):
     """N = 1,048,576 (BASELINE.md stress size): the row index no longer fits
     shared memory, so row totals, explored bits and weights live in global
     scratch (HG kernel) and the draw walks long row chunks with the whole
     warp.  Trajectories against the oracle (numpy restatement of the
-    reference, pinned by the golden tests) for a few repetitions."""
+    reference, pinned by the golden tests) for a few repetitions; with the
+    persistent kernel and with the tiled large-space path."""
+    monkeypatch.setenv("CT_SEARCH_TILED", tiled)
     import countertune_oracle as oracle
     from paper_2102_05297_b200 import ExactModelSet, harness, spaces
     from paper_2102_05297_b200.space import replay_arrays
