@@ -1343,12 +1343,7 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
             const size_t smem_mq = (size_t)mq_s * (head_b + (mq_smem ? pref_b : 0));
             switch (mq_w * 10000 + mq_s * 100 + mq_nch) {
             case 40104: return launch_profile_mq<4, 1, 4, 7>(ctx, a, pre, mq_smem, smem_mq, n_reps);
-            case 60204: return launch_profile_mq<6, 2, 4, 4>(ctx, a, pre, mq_smem, smem_mq, n_reps);
-            case 80204: return launch_profile_mq<8, 2, 4, 4>(ctx, a, pre, mq_smem, smem_mq, n_reps);
-            case 80304: return launch_profile_mq<8, 3, 4, 3>(ctx, a, pre, mq_smem, smem_mq, n_reps);
-            case 120304: return launch_profile_mq<12, 3, 4, 2>(ctx, a, pre, mq_smem, smem_mq, n_reps);
             case 120404: return launch_profile_mq<12, 4, 4, 2>(ctx, a, pre, mq_smem, smem_mq, n_reps);
-            case 160404: return launch_profile_mq<16, 4, 4, 2>(ctx, a, pre, mq_smem, smem_mq, n_reps);
             default: return fail(CT_ERR_VALUE, "CT_SEARCH_MQ: no such build");
             }
         }

@@ -587,8 +587,8 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
             }
             CT_SUB(2);
             if (!ok) {
-                if (lane == 0) { chosen = sequential_select(w, N, u); ++rs.uncert; }
-                chosen = __shfl_sync(FULL, (long long)chosen, 0);
+                chosen = sequential_select_warp(w, N, u, lane);
+                if (lane == 0) ++rs.uncert;
                 if (chosen >= 0 && chosen < N) { row = (int)(chosen >> 5); l2 = (int)(chosen & 31); }
             }
             if (lane == 0) ++rs.draws;

@@ -121,4 +121,99 @@ __device__ __noinline__ int64_t sequential_select(const double* w, int64_t n, do
     return n;
 }
 
+// The same re-decision by one warp, for large spaces: lane 0 still performs
+// every add of np.cumsum in order, while the whole warp fetches the weights
+// (one coalesced 32-element chunk per load, four chunks ahead) and hands
+// them to lane 0 by shuffle, so the chain runs at the add latency instead of
+// a dependent load per element.  The running sum before every per-th chunk
+// is kept as a checkpoint (<= 256, eight per lane), so finding r needs one
+// interval of the second pass instead of the whole array.  Returns the same
+// index as sequential_select.
+__device__ __forceinline__ double seq_fetch(const double* w, int64_t n, int64_t ch, int lane) {
+    const int64_t e = ch * 32 + lane;
+    return (e < n) ? w[e] : 0.0;
+}
+
+__device__ __noinline__ int64_t sequential_select_warp(const double* w, int64_t n, double u, int lane) {
+    constexpr int CK = 8;
+    const int64_t nchunks = (n + 31) / 32;
+    const int64_t per = max((int64_t)1, (nchunks + 32 * CK - 1) / (32 * CK));
+    double ck[CK];
+#pragma unroll
+    for (int s = 0; s < CK; ++s) ck[s] = 0.0;
+    double c = 0.0;                  // lane 0's running sum (+0.0 padding adds are exact)
+    double v[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) v[d] = seq_fetch(w, n, d, lane);
+    for (int64_t k = 0; k < nchunks; k += 4) {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const int64_t ch = k + d;
+            if (ch < nchunks) {
+                if (ch % per == 0) {
+                    const int64_t slot = ch / per;
+                    const double cb = __shfl_sync(FULL, c, 0);
+#pragma unroll
+                    for (int s = 0; s < CK; ++s)
+                        if (slot == 32 * s + lane) ck[s] = cb;
+                }
+                const double x = v[d];
+                v[d] = seq_fetch(w, n, ch + 4, lane);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const double xj = __shfl_sync(FULL, x, j);
+                    if (lane == 0) c = add(c, xj);
+                }
+            }
+        }
+    }
+    const double total = __shfl_sync(FULL, c, 0);
+    const double r = mul(u, total);
+    // the last checkpoint at or below r (slot 0 holds 0 <= r)
+    const int64_t nslots = (nchunks + per - 1) / per;
+    int64_t best = -1;
+    double from = 0.0;
+#pragma unroll
+    for (int s = 0; s < CK; ++s) {
+        const int64_t slot = 32 * s + lane;
+        if (slot < nslots && ck[s] <= r && slot > best) { best = slot; from = ck[s]; }
+    }
+    int64_t slot = best;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) slot = max(slot, (int64_t)__shfl_xor_sync(FULL, (long long)slot, m));
+    if (slot < 0) slot = 0;
+    const int owner = (int)(slot & 31);
+    c = __shfl_sync(FULL, from, owner);      // the owner's best is this slot
+    int64_t found = n;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) v[d] = seq_fetch(w, n, slot * per + d, lane);
+    for (int64_t k = slot * per; k < nchunks; k += 4) {
+        bool done = false;
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const int64_t ch = k + d;
+            if (ch < nchunks && !done) {
+                const double x = v[d];
+                v[d] = seq_fetch(w, n, ch + 4, lane);
+                int hit = -1;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const double xj = __shfl_sync(FULL, x, j);
+                    if (lane == 0 && hit < 0) {
+                        c = add(c, xj);
+                        if (c > r) hit = j;
+                    }
+                }
+                hit = __shfl_sync(FULL, hit, 0);
+                if (hit >= 0) {
+                    found = min(n, ch * 32 + hit);
+                    done = true;
+                }
+            }
+        }
+        if (done) break;
+    }
+    return found;
+}
+
 }  // namespace ct

@@ -31,7 +31,8 @@
 // moves); the row stride is then even (PAD pads by two floats).
 //
 // The tile lives in dynamic shared memory: the host passes
-// smem_bytes() = 4 * ((TH + F - 1) * (TW + 8 + PAD) + CACHE_F * F * F).
+// smem_bytes() = 4 * ((TH + F - 1) * (TW + 8 + PAD) + CACHE_F * F * F), and
+// with the packed path two tile copies and (CACHE_F) the duplicated taps.
 #ifndef TBX
 #define TBX 32
 #endif
@@ -75,7 +76,7 @@ constexpr int V4 = (TW + 8) / 4;                  // float4 per staged row: x0-4
 // (only where the doubled tile still fits the 227 KB per-block limit; a
 // preprocessor test, since it also selects the packed code path below)
 #define CONV_PAIRED_SMEM (4 * (2 * (TBY * WPTY + FILTER - 1) * ((TBX * WPTX + 8) / 4 * 4 + 2 * PAD) \
-                              + (CACHE_F ? FILTER * FILTER : 0)))
+                              + (CACHE_F ? (FILTER * FILTER + 1) / 2 * 2 + 2 * FILTER * FILTER : 0)))
 #if LOCAL == 2 && WPTX % 2 == 0 && CONV_PAIRED_SMEM <= 227 * 1024
 #define CONV_PAIRED 1
 #else
@@ -99,7 +100,10 @@ __device__ __forceinline__ float load_global(const float* __restrict__ in, int w
                                                              : 0.0f;
 }
 
-struct Filter { float f[FILTER * FILTER]; };
+// the filter by value: the taps, then each tap duplicated as a packed pair
+// (the broadcast operand of the FFMA2 path, read straight from the
+// parameter bank instead of being packed into a register pair per use)
+struct Filter { float f[FILTER * FILTER]; unsigned long long f2[FILTER * FILTER]; };
 
 extern "C" __global__ void __launch_bounds__(NT)
 conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter kf,
@@ -111,8 +115,20 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter 
 #if CACHE_F
     float* sf = dsm + (LOCAL ? (PAIRED ? 2 : 1) * LH * SW : 0);
     for (int i = tid; i < F * F; i += NT) sf[i] = filt[i];
+#if CONV_PAIRED
+    // pairs (f, f) after the taps, 8-byte aligned
+    unsigned long long* sf2 = reinterpret_cast<unsigned long long*>(sf + ((F * F + 1) & ~1));
+    for (int i = tid; i < F * F; i += NT) {
+        const float f = filt[i];
+        unsigned long long p;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(p) : "f"(f));
+        sf2[i] = p;
+    }
+#endif
 #define FILT(fy, fx) sf[(fy) * F + (fx)]
+#define FILT2(fy, fx) sf2[(fy) * F + (fx)]
 #else
+#define FILT2(fy, fx) kf.f2[(fy) * F + (fx)]
 #define FILT(fy, fx) kf.f[(fy) * F + (fx)]
 #endif
 #if LOCAL
@@ -183,17 +199,13 @@ conv(const float* __restrict__ in, const float* __restrict__ filt, const Filter 
                     for (int h = 0; h < H; ++h)
 #pragma unroll kUnrollF
                         for (int fx = 0; fx < F; ++fx) {
-                            const float f = FILT(fy, fx);
-                            f2 fp;
-                            asm("mov.b64 %0, {%1, %1};" : "=l"(fp) : "f"(f));
+                            const f2 fp = FILT2(fy, fx);
                             asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(accp[wy][h]) : "l"(pr[2 * h + fx]), "l"(fp));
                         }
 #else
 #pragma unroll kUnrollF
                     for (int fx = 0; fx < F; ++fx) {
-                        const float f = FILT(fy, fx);
-                        f2 fp;
-                        asm("mov.b64 %0, {%1, %1};" : "=l"(fp) : "f"(f));
+                        const f2 fp = FILT2(fy, fx);
 #pragma unroll
                         for (int h = 0; h < H; ++h)
                             asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(accp[wy][h]) : "l"(pr[2 * h + fx]), "l"(fp));

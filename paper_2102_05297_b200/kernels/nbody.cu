@@ -14,7 +14,7 @@
 // JS and gridDim.y = JB (set by the host, not tuning parameters): the j range
 // is split over JB blocks and, inside a block, over blockDim.y = JS thread
 // rows, so that n = 16,384 bodies still fill the 148 SMs (one thread per body
-// would be 512 warps).  A body's JS partial sums are reduced in shared
+// would be 512 warps) -- in one wave of resident blocks (live.py split()).  A body's JS partial sums are reduced in shared
 // memory, its JB block partials by the last block to finish (fixed order,
 // deterministic; the arrival counters reset themselves, so a launch is
 // idempotent under timing and profiler replay).
@@ -118,7 +118,9 @@ struct BodyPair {
 };
 #endif
 
-extern "C" __global__ void __launch_bounds__(BLOCK * JS)
+// at most 64 registers: 1024 resident threads per SM, which the host's
+// choice of JS / JB fills in one wave (live.NBodyBenchmark.split)
+extern "C" __global__ void __launch_bounds__(BLOCK * JS, (1024 / (BLOCK * JS)) > 0 ? 1024 / (BLOCK * JS) : 1)
 nbody(const float4* __restrict__ pm, const float* __restrict__ x, const float* __restrict__ y,
       const float* __restrict__ z, const float* __restrict__ m, int n, float eps2,
       float4* __restrict__ acc, float4* __restrict__ partial, unsigned* __restrict__ arrivals) {

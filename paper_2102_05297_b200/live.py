@@ -240,21 +240,38 @@ class NBodyBenchmark(Benchmark):
         tuner.memset(out["arrivals"], 0, 4 * groups)
         return out
 
-    SM_THREADS = 148 * 1024      # aim: at least half of the B200's thread slots busy
-    MIN_BLOCKS = 2 * 148         # and at least two blocks per SM
+    # the kernel's launch bounds cap it at 64 registers for 1024 resident
+    # threads per SM (32 warps: 8 per scheduler for the MUFU/FMA latencies)
+    SM_THREADS = 1024
+    SMS = 148
     MAX_JB = 16
 
+    def split(self, v):
+        """(JS, JB): thread rows per block and blocks the j range is split
+        over, minimising waves of resident blocks x j tiles per thread row
+        (a partial extra wave costs a whole one); ties go to fewer splits
+        (less reduction), then to more thread rows (reduced in shared memory,
+        not through global partials)."""
+        B = v["BLOCK"]
+        gx = -(-self.bodies // (B * v["OUTER"]))
+        tiles = -(-self.bodies // B)
+        best = None
+        js = 1
+        while B * js <= 1024:
+            slots = self.SMS * max(1, self.SM_THREADS // (B * js))
+            for jb in range(1, self.MAX_JB + 1):
+                waves = -(-(gx * jb) // slots)
+                key = (waves * -(-tiles // (js * jb)), js * jb, -js)
+                if best is None or key < best[0]:
+                    best = (key, js, jb)
+            js *= 2
+        return best[1], best[2]
+
     def jb(self, v) -> int:
-        """Blocks the j range is split over (gridDim.y): enough blocks for
-        every SM when the bodies alone make fewer."""
-        gx = -(-self.bodies // (v["BLOCK"] * v["OUTER"]))
-        return max(1, min(self.MAX_JB, -(-self.MIN_BLOCKS // gx)))
+        return self.split(v)[1]
 
     def js(self, v) -> int:
-        """Thread rows the j range is split over inside a block (compile-time
-        JS of the kernel): enough threads to fill the GPU, <= 1024 per block."""
-        want = -(-self.SM_THREADS * v["OUTER"] // (self.bodies * self.jb(v)))
-        return max(1, min(1024 // v["BLOCK"], want))
+        return self.split(v)[0]
 
     def options(self, values):
         return super().options(values) + [f"-DJS={self.js(values)}"]
@@ -271,6 +288,20 @@ class NBodyBenchmark(Benchmark):
 
     def work(self):
         return float(self.bodies) ** 2
+
+
+def _conv_filter_arg(filt: np.ndarray):
+    """conv.cu's by-value Filter: the taps, then every tap as a packed pair
+    (f, f) for the FFMA2 path's broadcast operand."""
+    n = filt.size
+
+    class Filter(ctypes.Structure):
+        _fields_ = [("f", ctypes.c_float * n), ("f2", ctypes.c_uint64 * n)]
+
+    taps = np.ascontiguousarray(filt.ravel(), dtype=np.float32)
+    bits = taps.view(np.uint32).astype(np.uint64)
+    return Filter((ctypes.c_float * n)(*taps.tolist()),
+                  (ctypes.c_uint64 * n)(*((bits << np.uint64(32)) | bits).tolist()))
 
 
 class ConvBenchmark(Benchmark):
@@ -299,10 +330,12 @@ class ConvBenchmark(Benchmark):
     def smem_bytes(self, v) -> int:
         f = self.filt
         tw, th = v["TBX"] * v["WPTX"], v["TBY"] * v["WPTY"]
-        filt = f * f if v["CACHE_F"] else 0
-        # conv.cu PAIRED: two tile copies, where the doubled tile fits 227 KB
+        # conv.cu PAIRED: two tile copies and (CACHE_F) the taps duplicated
+        # as packed pairs, where that still fits 227 KB
+        filt2 = ((f * f + 1) // 2 * 2 + 2 * f * f) if v["CACHE_F"] else 0
         paired = (v["LOCAL"] == 2 and v["WPTX"] % 2 == 0
-                  and 4 * (2 * (th + f - 1) * (tw + 8 + 2 * v["PAD"]) + filt) <= 227 * 1024)
+                  and 4 * (2 * (th + f - 1) * (tw + 8 + 2 * v["PAD"]) + filt2) <= 227 * 1024)
+        filt = (filt2 if paired else f * f) if v["CACHE_F"] else 0
         tile = ((th + f - 1) * (tw + 8 + v["PAD"] * (2 if paired else 1)) * (2 if paired else 1)
                 if v["LOCAL"] else 0)
         return 4 * (tile + filt)
@@ -312,7 +345,7 @@ class ConvBenchmark(Benchmark):
         # the filter also travels by value (kernel parameter bank, CACHE_F = 0)
         if getattr(self, "_filt_host", None) is None:
             self._filt_host = self.host_inputs()["filt"]
-        kf = (_f32 * (self.filt * self.filt))(*self._filt_host.ravel().tolist())
+        kf = _conv_filter_arg(self._filt_host)
         return Launch((self.width // tw, self.height // th), (v["TBX"], v["TBY"]),
                       [_u64(bufs["in"]), _u64(bufs["filt"]), kf, _u64(bufs["out"]),
                        _i32(self.width), _i32(self.height)], dynamic_smem=self.smem_bytes(v))

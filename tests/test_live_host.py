@@ -67,7 +67,11 @@ def test_launch_geometry_covers_problem(name):
             assert l.grid[2] * v["Z_ITERATIONS"] >= b.grid
         elif name == "nbody":
             assert l.grid[0] * v["BLOCK"] * v["OUTER"] >= b.bodies
-            assert 1 <= l.grid[1] <= b.MAX_JB and l.grid[0] * l.grid[1] >= min(b.MIN_BLOCKS, l.grid[0] * b.MAX_JB)
+            assert 1 <= l.grid[1] <= b.MAX_JB and l.block[0] * l.block[1] <= 1024
+            # the j range splits evenly enough that no thread row is idle
+            splits = l.grid[1] * l.block[1]
+            tiles = -(-b.bodies // v["BLOCK"])
+            assert -(-tiles // splits) * (splits - 1) < tiles
         elif name == "conv":
             assert l.grid[0] * v["TBX"] * v["WPTX"] == b.width
             assert l.grid[1] * v["TBY"] * v["WPTY"] == b.height
