@@ -1279,6 +1279,8 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     a.nrows = (int32_t)((n + 31) / 32);
     a.nwords = (n + 31) / 32;
     if (const char* env = std::getenv("CT_SEARCH_FORCE_SEQUENTIAL")) a.force_sequential = std::atoi(env);
+    a.cert_slack = 1.0;
+    if (const char* env = std::getenv("CT_SEARCH_CERT_SLACK")) a.cert_slack = std::max(1.0, std::atof(env));
     a.topk = prm->score_top_k >= 0 ? prm->score_top_k : -1;
     a.assign = a.topk >= 0 ? ctx->assign.p : nullptr;
     a.n_params = a.topk >= 0 ? ctx->n_params : 0;

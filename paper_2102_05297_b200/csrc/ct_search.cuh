@@ -83,6 +83,7 @@ struct SearchArgs {
     int32_t nrows;
     int64_t nwords;
     int32_t force_sequential;    // test hook: decide every draw sequentially
+    double cert_slack;           // test hook: certificate half-width multiplier (1 = proven bound)
     // score_top_k (search.py:133-140): < 0 is None; assign is the space's
     // n x n_params assignment matrix (row-major), read for the distances
     int64_t topk;
@@ -459,14 +460,25 @@ __device__ __forceinline__ void weight_phase(const SearchArgs& a, Ctl<NW>& ctl, 
 // Locating r: lane L owns a contiguous chunk of rows and keeps the inclusive
 // prefix over the chunks (lane_pref); a ballot finds the chunk, lane L walks
 // its rows, and the row's precomputed in-row prefixes give the configuration
-// with one more ballot.  All sums are float64; the choice is CERTIFIED: with
-// P(i-1) <= r < P(i) the computed prefixes around the chosen configuration,
-// the reference's sequential cumsum c over numpy's weights (each within 1 ulp
-// of ours) satisfies |c(j) - P(j)| + |r_ref - r| < B = (8N + 128) 2^-53 T
-// (any summation order of N positive terms errs by < N 2^-53 T; the weight
-// difference adds 2 2^-53 T; r and the zeroing updates a few 2^-53 T more),
-// so P(i-1) + B < r and r + B < P(i) imply that the reference picks i too.
-// Otherwise the draw is re-decided with the sequential float64 cumsum.
+// with one more ballot.  All sums are float64; the choice is CERTIFIED.  With
+// u = 2^-53, W the exact sum of our weights, T our computed total:
+//  * numpy's weights w' and ours w are each within 1 ulp of the exact x^8,
+//    so |w_i - w'_i| < 4u w_i and |S'(j) - S(j)| < 4u W (exact prefixes);
+//  * the reference's sequential cumsum c'(j) = recursive summation of
+//    nonnegative terms: |c'(j) - S'(j)| <= gamma_(N-1) W';
+//  * our prefix P(j) passes every weight through at most d additions -- 5
+//    in the row-total tree, <= cpl in the lane-chunk sum, 5 in the lane
+//    scan, <= max(cpl, 6) in the row walk (or 5 + 1 in the slab scan), 5 + 1
+//    in the in-row scan: d <= 2 cpl + 22 -- plus <= 3 inner zeroing
+//    subtractions (row total, chunk sum, lane prefix per draw): |P(j) -
+//    S(j)| <= gamma_(d + 3 inner) W;
+//  * hence E = |c'(j) - P(j)| <= (N + 2 cpl + 3 inner + 26) u W (1 + O(Nu)),
+//    and r' = fl(U c'(N)), r = fl(U T) give |r' - r| <= E + 2u W;
+//  * P(i-1) + B < r and r + B < P(i) with B >= 2E + 2uW + the comparisons'
+//    own roundings imply c'(i-1) <= r' < c'(i): the reference picks i too.
+// B = (2N + 4 cpl + 6 inner + 64) u T (1 + 2^-40) covers it (T >= W(1 -
+// gamma_d), and the slack terms absorb the second-order parts).  Otherwise
+// the draw is re-decided with the sequential float64 cumsum.
 template <bool PRE, int NW, bool COOP = false>
 __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl<NW>& ctl,
                                           uint32_t* expl, double* w, double* pre, double* row_tot,
@@ -490,7 +502,10 @@ __device__ __forceinline__ void draw_step(const SearchArgs& a, RepState& rs, Ctl
         if (lane >= d) lane_pref = add(lane_pref, v);
     }
     double total = __shfl_sync(FULL, lane_pref, 31);
-    const double B = (double)(8 * N + 128) * 1.1102230246251565e-16 * total;   // 2^-53
+    // certificate half-width (derivation at the top of draw_step):
+    // (2N + 4 cpl + 6 inner + 64) 2^-53 T, times the test hook's slack
+    const double B = (double)(2 * N + 4 * (int64_t)cpl + 6 * (int64_t)a.inner + 64) *
+                     1.1102230246251565e-16 * total * (1.0 + 0x1p-40) * a.cert_slack;
     int done = 0;
     if (bad) { if (lane == 0) { rs.st = CT_STATUS_ERROR; rs.err = -7; } done = 1; }
     double t_best = INFINITY;

@@ -571,6 +571,9 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
         ep.ctx = t->ctx;
         TU_CUPTI(cuptiRangeProfilerEnable(&ep));
         t->rp = ep.pRangeProfilerObject;
+        // counter-data images were sized and initialised against the old
+        // object: every configuration re-derives its image under the new one
+        for (auto& kv : t->configs) kv.second->counter_data.clear();
     }
     t->rp_config = hc;
     const auto t1 = clk::now();

@@ -313,15 +313,19 @@ def test_large_space_properties():
         assert idx2[r, :nst2[r]].tolist() == res.step_index[3 + r, :res.n_steps[3 + r]].tolist()
 
 
-@pytest.mark.parametrize("tiled", ["0", "1"], ids=["persistent", "tiled"])
-def test_gemm_full_trajectories_match_reference_with_uncertified_draws(tiled, monkeypatch):
+@pytest.mark.parametrize("tiled,slack", [("0", "1"), ("0", "4"), ("1", "1"), ("1", "4")],
+                         ids=["persistent", "persistent-slack4", "tiled", "tiled-slack4"])
+def test_gemm_full_trajectories_match_reference_with_uncertified_draws(tiled, slack, monkeypatch):
     """N = 205,216 (GEMM-full): 256 repetitions x 40 iterations x 5 draws
     against the reference's own trajectories (make_gemmfull_golden.py).  At
     this size the certificate rejects some draws, which the device re-decides
-    with the sequential cumsum: the run must contain such draws and still
-    match the reference everywhere -- with the per-repetition persistent
-    kernel and with the tiled large-space path."""
+    with the sequential cumsum: the run must still match the reference
+    everywhere -- with the per-repetition persistent kernel and with the
+    tiled large-space path, under the proven half-width and under 4x it
+    (CT_SEARCH_CERT_SLACK, about round 1's (8N + 128) u T), which must leave
+    draws to the re-decision."""
     monkeypatch.setenv("CT_SEARCH_TILED", tiled)
+    monkeypatch.setenv("CT_SEARCH_CERT_SLACK", slack)
     from paper_2102_05297_b200 import ExactModelSet, _native, spaces
     from paper_2102_05297_b200.search import PredictionTable, search_params
     from paper_2102_05297_b200.space import replay_arrays
@@ -343,7 +347,8 @@ def test_gemm_full_trajectories_match_reference_with_uncertified_draws(tiled, mo
         assert got == want[r], f"rep {r}: first divergence at " \
             f"{next((k for k, (a, b) in enumerate(zip(got, want[r])) if a != b), min(len(got), len(want[r])))}"
     print(f"gemm_full: {stats.draws} draws, {stats.uncertified} uncertified")
-    assert stats.uncertified > 0
+    if slack != "1":
+        assert stats.uncertified > 0
 
 
 def test_inline_division_is_ddiv_rn():
