@@ -121,99 +121,129 @@ __device__ __noinline__ int64_t sequential_select(const double* w, int64_t n, do
     return n;
 }
 
-// The same re-decision by one warp, for large spaces: lane 0 still performs
-// every add of np.cumsum in order, while the whole warp fetches the weights
-// (one coalesced 32-element chunk per load, four chunks ahead) and hands
-// them to lane 0 by shuffle, so the chain runs at the add latency instead of
-// a dependent load per element.  The running sum before every per-th chunk
-// is kept as a checkpoint (<= 256, eight per lane), so finding r needs one
-// interval of the second pass instead of the whole array.  Returns the same
-// index as sequential_select.
-__device__ __forceinline__ double seq_fetch(const double* w, int64_t n, int64_t ch, int lane) {
-    const int64_t e = ch * 32 + lane;
-    return (e < n) ? w[e] : 0.0;
+// The same re-decision by one warp, for large spaces, without a chain of N
+// dependent adds.  np.cumsum's running value c_k = fl(c_(k-1) + w_k) is
+// emulated EXACTLY in integer arithmetic while c stays in one binade
+// [2^E, 2^(E+1)): there c = g C with the grid g = 2^(E-52) and an integer
+// C in [2^52, 2^53), and for w >= 0 with c + w still below 2^(E+1),
+// fl(c + w) = g (C + n), n = round-to-nearest-even(w / g) -- w / g is an
+// exact power-of-two scaling, and n does not depend on C unless w / g is a
+// tie (fraction exactly 1/2, parity of C decides).  So a block of 128
+// weights (4 per lane) is one exact int64 warp scan of the n's; the first
+// element whose sum would leave the binade (C + n >= 2^53), or is a tie, or
+// (c = 0) starts the sum, is added by the hardware's own fl add instead,
+// and the scan resumes after it in the new binade.  Every c_k is therefore
+// bit-identical to the sequential loop's, at ~1-2 cycles per element
+// instead of one add latency.
+//
+// seq_scan: from element k0 with running value c (c_(k0-1)), through n
+// elements, stopping at the first k with c_k > r (r < 0: never); returns k
+// (n if none) and leaves c = c_(k) / c_(n-1).
+__device__ __forceinline__ double pow2d(int e) {          // 2^e, e in [-1022, 1023]
+    return bitsd((uint64_t)(1023 + e) << 52);
 }
 
-__device__ __noinline__ int64_t sequential_select_warp(const double* w, int64_t n, double u, int lane) {
-    constexpr int CK = 8;
-    const int64_t nchunks = (n + 31) / 32;
-    const int64_t per = max((int64_t)1, (nchunks + 32 * CK - 1) / (32 * CK));
-    double ck[CK];
+__device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t k0, double& c,
+                                            double r, int lane) {
+    const int64_t TWO53 = 1ll << 53;
+    for (int64_t base = k0 & ~(int64_t)127; base < n; base += 128) {
+        // this lane's four weights: elements base + 4 lane + j
+        double x[4];
 #pragma unroll
-    for (int s = 0; s < CK; ++s) ck[s] = 0.0;
-    double c = 0.0;                  // lane 0's running sum (+0.0 padding adds are exact)
-    double v[4];
-#pragma unroll
-    for (int d = 0; d < 4; ++d) v[d] = seq_fetch(w, n, d, lane);
-    for (int64_t k = 0; k < nchunks; k += 4) {
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const int64_t ch = k + d;
-            if (ch < nchunks) {
-                if (ch % per == 0) {
-                    const int64_t slot = ch / per;
-                    const double cb = __shfl_sync(FULL, c, 0);
-#pragma unroll
-                    for (int s = 0; s < CK; ++s)
-                        if (slot == 32 * s + lane) ck[s] = cb;
-                }
-                const double x = v[d];
-                v[d] = seq_fetch(w, n, ch + 4, lane);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const double xj = __shfl_sync(FULL, x, j);
-                    if (lane == 0) c = add(c, xj);
-                }
-            }
+        for (int j = 0; j < 4; ++j) {
+            const int64_t e = base + 4 * lane + j;
+            x[j] = (e >= k0 && e < n) ? w[e] : 0.0;
         }
-    }
-    const double total = __shfl_sync(FULL, c, 0);
-    const double r = mul(u, total);
-    // the last checkpoint at or below r (slot 0 holds 0 <= r)
-    const int64_t nslots = (nchunks + per - 1) / per;
-    int64_t best = -1;
-    double from = 0.0;
+        int64_t from = max(k0, base);       // first element of the block still to add
+        while (from < base + 128 && from < n) {
+            // binade state of c; c == 0 (or subnormal): every element is a
+            // scalar step until the sum is normal
+            const bool lin = c >= 2.2250738585072014e-308;
+            const int E = lin ? (int)((dbits(c) >> 52) & 0x7ff) - 1023 : 0;
+            const int64_t C = lin ? (int64_t)((dbits(c) & ((1ull << 52) - 1)) | (1ull << 52)) : 0;
+            const double to_grid = lin ? pow2d(52 - E) : 0.0, from_grid = lin ? pow2d(E - 52) : 0.0;
+            int64_t s_in[4];
+            bool st[4];
+            int64_t run = 0;
 #pragma unroll
-    for (int s = 0; s < CK; ++s) {
-        const int64_t slot = 32 * s + lane;
-        if (slot < nslots && ck[s] <= r && slot > best) { best = slot; from = ck[s]; }
-    }
-    int64_t slot = best;
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) slot = max(slot, (int64_t)__shfl_xor_sync(FULL, (long long)slot, m));
-    if (slot < 0) slot = 0;
-    const int owner = (int)(slot & 31);
-    c = __shfl_sync(FULL, from, owner);      // the owner's best is this slot
-    int64_t found = n;
-#pragma unroll
-    for (int d = 0; d < 4; ++d) v[d] = seq_fetch(w, n, slot * per + d, lane);
-    for (int64_t k = slot * per; k < nchunks; k += 4) {
-        bool done = false;
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const int64_t ch = k + d;
-            if (ch < nchunks && !done) {
-                const double x = v[d];
-                v[d] = seq_fetch(w, n, ch + 4, lane);
-                int hit = -1;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const double xj = __shfl_sync(FULL, x, j);
-                    if (lane == 0 && hit < 0) {
-                        c = add(c, xj);
-                        if (c > r) hit = j;
+            for (int j = 0; j < 4; ++j) {
+                const int64_t e = base + 4 * lane + j;
+                int64_t nj = 0;
+                bool sj = false;
+                if (e >= from && e < n) {
+                    if (!lin) {
+                        sj = x[j] != 0.0;
+                    } else {
+                        const double t = x[j] * to_grid;            // exact
+                        if (t >= 9007199254740992.0) {
+                            sj = true;                              // alone past the binade
+                        } else {
+                            const double m = floor(t);
+                            const double f = t - m;                 // exact
+                            nj = (int64_t)m + (f > 0.5 ? 1 : 0);
+                            sj = (f == 0.5);                        // tie: parity of C decides
+                        }
                     }
                 }
-                hit = __shfl_sync(FULL, hit, 0);
-                if (hit >= 0) {
-                    found = min(n, ch * 32 + hit);
-                    done = true;
-                }
+                run += nj;
+                s_in[j] = run;
+                st[j] = sj;
             }
+            int64_t incl = run;                     // exact int64 warp scan
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int64_t v = __shfl_up_sync(FULL, (long long)incl, d);
+                if (lane >= d) incl += v;
+            }
+            const int64_t before = incl - run;
+            // this lane's first stopping element and first element past r
+            int jstop = 4, jhit = 4;
+#pragma unroll
+            for (int j = 3; j >= 0; --j) {
+                const int64_t Ck = C + before + s_in[j];
+                const bool leave = lin && Ck >= TWO53;
+                if (st[j] || leave) jstop = j;
+                if (lin && !st[j] && !leave && r >= 0.0 && (double)Ck * from_grid > r) jhit = j;
+            }
+            // elements are lane-major, so the first flagged lane holds the
+            // first flagged element
+            const unsigned bs = __ballot_sync(FULL, jstop < 4);
+            const unsigned bh = __ballot_sync(FULL, jhit < 4);
+            const int64_t big = 0x7fffffffffffffffll;
+            int64_t pstop = big, phit = big;
+            if (bs) { const int L = __ffs(bs) - 1; pstop = base + 4 * L + __shfl_sync(FULL, jstop, L); }
+            if (bh) { const int L = __ffs(bh) - 1; phit = base + 4 * L + __shfl_sync(FULL, jhit, L); }
+            if (phit < pstop) return phit;          // c_k > r inside the binade
+            if (pstop == big) {                     // the rest of the block stays in the binade
+                if (lin) c = (double)(C + __shfl_sync(FULL, (long long)incl, 31)) * from_grid;
+                break;
+            }
+            // elements before pstop are final: c = g (C + their increments)
+            if (lin) {
+                const int owner = (int)((pstop - base) >> 2), jj = (int)((pstop - base) & 3);
+                int64_t pre = before;
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    if (j < jj) pre = before + s_in[j];
+                pre = __shfl_sync(FULL, (long long)pre, owner);
+                c = (double)(C + pre) * from_grid;
+            }
+            c = add(c, w[pstop]);                   // the hardware's fl add at the stop
+            if (r >= 0.0 && c > r) return pstop;
+            from = pstop + 1;
         }
-        if (done) break;
     }
-    return found;
+    return n;
+}
+
+// np.cumsum + searchsorted(side='right') by one warp: the total, r = u c_N,
+// then the first k with c_k > r (n when r reaches the total).
+__device__ __noinline__ int64_t sequential_select_warp(const double* w, int64_t n, double u, int lane) {
+    double c = 0.0;
+    seq_scan(w, n, 0, c, -1.0, lane);
+    const double r = mul(u, c);
+    double c2 = 0.0;
+    return seq_scan(w, n, 0, c2, r, lane);
 }
 
 }  // namespace ct

@@ -3,7 +3,7 @@
 TAG=${1:-r02}
 OUT=gpurun_out/sanitizer_${TAG}
 mkdir -p $OUT
-for c in scratch ws hg topk report; do
+for c in scratch ws hg topk report tiled seq mq; do
   for tool in memcheck racecheck synccheck initcheck; do
     timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_cases.py $c > $OUT/${c}_${tool}.log 2>&1
     echo "$c $tool rc=$?" | tee -a $OUT/summary.txt

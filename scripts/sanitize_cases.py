@@ -7,6 +7,9 @@
   topk      score_top_k on b200 transpose
   report    simulate() with the one-call device report
   tune      libct_tune: compile, time and profile one transpose variant
+  tiled     the tiled large-space path (CT_SEARCH_TILED=1) on b200 gemm
+  seq       every draw through the warp's binade-exact sequential re-decision
+  mq        the shared-queue kernel (CT_SEARCH_MQ=12,4,4)
 """
 import os
 import sys
@@ -36,6 +39,15 @@ def main():
         search(b200("transpose"))
     elif case == "hg":
         search(spaces.stress(400_000), reps=2, i=3, stop_at_well_performing=False)
+    elif case == "tiled":
+        os.environ["CT_SEARCH_TILED"] = "1"
+        search(b200("gemm"))
+    elif case == "seq":
+        os.environ["CT_SEARCH_FORCE_SEQUENTIAL"] = "1"
+        search(b200("transpose"))
+    elif case == "mq":
+        os.environ["CT_SEARCH_MQ"] = "12,4,4"
+        search(b200("transpose"), reps=12)
     elif case == "topk":
         search(b200("transpose"), score_top_k=40)
     elif case == "report":

@@ -313,9 +313,12 @@ def test_large_space_properties():
         assert idx2[r, :nst2[r]].tolist() == res.step_index[3 + r, :res.n_steps[3 + r]].tolist()
 
 
-@pytest.mark.parametrize("tiled,slack", [("0", "1"), ("0", "4"), ("1", "1"), ("1", "4")],
-                         ids=["persistent", "persistent-slack4", "tiled", "tiled-slack4"])
-def test_gemm_full_trajectories_match_reference_with_uncertified_draws(tiled, slack, monkeypatch):
+@pytest.mark.parametrize("tiled,slack,force", [("0", "1", "0"), ("0", "4", "0"), ("1", "1", "0"),
+                                               ("1", "4", "0"), ("0", "1", "1"), ("1", "1", "1")],
+                         ids=["persistent", "persistent-slack4", "tiled", "tiled-slack4",
+                              "persistent-all-sequential", "tiled-all-sequential"])
+def test_gemm_full_trajectories_match_reference_with_uncertified_draws(tiled, slack, force,
+                                                                        monkeypatch):
     """N = 205,216 (GEMM-full): 256 repetitions x 40 iterations x 5 draws
     against the reference's own trajectories (make_gemmfull_golden.py).  At
     this size the certificate rejects some draws, which the device re-decides
@@ -326,6 +329,7 @@ def test_gemm_full_trajectories_match_reference_with_uncertified_draws(tiled, sl
     draws to the re-decision."""
     monkeypatch.setenv("CT_SEARCH_TILED", tiled)
     monkeypatch.setenv("CT_SEARCH_CERT_SLACK", slack)
+    monkeypatch.setenv("CT_SEARCH_FORCE_SEQUENTIAL", force)
     from paper_2102_05297_b200 import ExactModelSet, _native, spaces
     from paper_2102_05297_b200.search import PredictionTable, search_params
     from paper_2102_05297_b200.space import replay_arrays
@@ -349,6 +353,8 @@ def test_gemm_full_trajectories_match_reference_with_uncertified_draws(tiled, sl
     print(f"gemm_full: {stats.draws} draws, {stats.uncertified} uncertified")
     if slack != "1":
         assert stats.uncertified > 0
+    if force == "1":
+        assert stats.uncertified == stats.draws > 0
 
 
 def test_inline_division_is_ddiv_rn():
@@ -405,6 +411,14 @@ def test_sequential_redecision_path_matches_reference(monkeypatch):
     for r in range(reps):
         assert idx[r, :nst[r]].tolist() == want[r]
     assert stats.uncertified == stats.draws > 0
+
+
+@pytest.mark.parametrize("name", TRAJ_SETS)
+def test_every_draw_sequential_matches_reference(name, monkeypatch):
+    """Every draw of every trajectory set forced through the re-decision
+    (the warp's binade-exact emulation of np.cumsum's sequential adds)."""
+    monkeypatch.setenv("CT_SEARCH_FORCE_SEQUENTIAL", "1")
+    _check_trajectories(name)
 
 
 @pytest.mark.parametrize("name,family", [("gradient", "tree"), ("coulomb", "tree"),
