@@ -777,6 +777,8 @@ int launch_tiled(ct_ctx* ctx, SearchArgs& a, int n_reps) {
     for (int r0 = 0; r0 < n_reps; r0 += batch) {
         t.rep0 = r0;
         t.batch = std::min(batch, n_reps - r0);
+        // defined bytes everywhere (the score kernel copies whole control blocks)
+        CT_CUDA(cudaMemsetAsync(t.state, 0, sizeof(TiledRep) * (size_t)t.batch, ctx->stream));
         const int warps_grid = (t.batch + 3) / 4;
         const dim3 tiles((unsigned)t.batch, (unsigned)ntiles);
         k_tiled_begin<<<warps_grid, 128, 0, ctx->stream>>>(a, t);
@@ -804,35 +806,6 @@ int launch_tiled(ct_ctx* ctx, SearchArgs& a, int n_reps) {
 
 // spaces above this size take the tiled path by default
 constexpr int64_t TILED_MIN_N = 1ll << 40;   // set from measurements
-
-// shared-queue kernel: S repetition slots per CTA of W warps, NCH chunks per phase
-template <int W, int S, int NCH, int MINB, bool SMEM, bool PRE>
-int launch_profile_mq_t(ct_ctx* ctx, SearchArgs& a, size_t smem, int n_reps) {
-    auto kern = k_profile_search_mq<W, S, NCH, MINB, SMEM, PRE>;
-    // (the opt-in limit counts the ~4-8 KB of static control blocks too)
-    if (smem > 32 * 1024)
-        CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
-    if (occ < 1) return fail(CT_ERR_CUDA, "search kernel does not fit on an SM");
-    int grid = std::min((n_reps + S - 1) / S, occ * ctx->sm_count);
-    if (!SMEM) {
-        CT_CUDA(ctx->scratch_w.ensure((size_t)S * grid * 64 * (size_t)a.nrows));
-        a.scratch_w = ctx->scratch_w.p;
-    }
-    kern<<<grid, 32 * W, smem, ctx->stream>>>(a);
-    CT_CUDA(cudaGetLastError());
-    return CT_OK;
-}
-
-template <int W, int S, int NCH, int MINB>
-int launch_profile_mq(ct_ctx* ctx, SearchArgs& a, bool pre, bool in_smem, size_t smem, int n_reps) {
-    if (pre)
-        return in_smem ? launch_profile_mq_t<W, S, NCH, MINB, true, true>(ctx, a, smem, n_reps)
-                       : launch_profile_mq_t<W, S, NCH, MINB, false, true>(ctx, a, smem, n_reps);
-    return in_smem ? launch_profile_mq_t<W, S, NCH, MINB, true, false>(ctx, a, smem, n_reps)
-                   : launch_profile_mq_t<W, S, NCH, MINB, false, false>(ctx, a, smem, n_reps);
-}
 
 template <int PW>
 int launch_profile_ws(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int n_reps) {
@@ -1326,30 +1299,6 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     bool in_smem = head_b + pref_b <= per_cta_cap;
     if (const char* env = std::getenv("CT_SEARCH_SMEM")) in_smem = std::atoi(env) != 0 && head_b + pref_b <= budget;
     const size_t smem = head_b + (in_smem ? pref_b : 0);
-    // shared-queue kernel (CT_SEARCH_MQ = "W,S,NCH": warps per CTA, repetition
-    // slots per CTA, chunks per parallel phase)
-    int mq_w = 0, mq_s = 0, mq_nch = 0;
-    if (const char* env = std::getenv("CT_SEARCH_MQ")) {
-        if (std::sscanf(env, "%d,%d,%d", &mq_w, &mq_s, &mq_nch) != 3) mq_w = 0;
-    }
-    if (mq_w > 0 && a.topk < 0) {
-        const int64_t ctas = (n_reps + mq_s - 1) / mq_s;
-        const int64_t per_sm = std::max<int64_t>(1, (ctas + ctx->sm_count - 1) / ctx->sm_count);
-        // (the per-slot control blocks take up to ~8 KB of static shared memory)
-        const size_t cap = std::min<size_t>((size_t)(228 * 1024 / per_sm) - 3 * 1024,
-                                            219 * 1024);
-        if ((size_t)mq_s * head_b <= cap) {
-            bool mq_smem = (size_t)mq_s * (head_b + pref_b) <= cap;
-            if (const char* env = std::getenv("CT_SEARCH_SMEM"))
-                mq_smem = std::atoi(env) != 0 && (size_t)mq_s * (head_b + pref_b) <= 219 * 1024;
-            const size_t smem_mq = (size_t)mq_s * (head_b + (mq_smem ? pref_b : 0));
-            switch (mq_w * 10000 + mq_s * 100 + mq_nch) {
-            case 40104: return launch_profile_mq<4, 1, 4, 7>(ctx, a, pre, mq_smem, smem_mq, n_reps);
-            case 120404: return launch_profile_mq<12, 4, 4, 2>(ctx, a, pre, mq_smem, smem_mq, n_reps);
-            default: return fail(CT_ERR_VALUE, "CT_SEARCH_MQ: no such build");
-            }
-        }
-    }
     // warp-specialised two-repetition kernel (CT_SEARCH_WS = parallel warps)
     int ws = 0;
     if (const char* env = std::getenv("CT_SEARCH_WS")) ws = std::atoi(env);
@@ -1581,6 +1530,8 @@ int ct_report(ct_ctx* ctx, double overhead, int32_t time_reps, int32_t* n_steps,
     double* d_tcq = d_tcs + AGG_GRID;
     AggMeta* d_meta = reinterpret_cast<AggMeta*>(d_tcq + AGG_GRID);
     CT_CUDA(ctx->agg_sampled.ensure((size_t)TR * AGG_GRID));
+    // the time-grid sums past the grid's length are copied but never written
+    CT_CUDA(cudaMemsetAsync(d_tcs, 0, 8 * 2 * (size_t)AGG_GRID, s));
     k_agg_rows<<<(int)std::min<int64_t>((R + 7) / 8, 8 * (int64_t)ctx->sm_count), 256, 0, s>>>(
         ctx->step_index.p, ctx->step_profiled.p, ctx->n_steps.p, (int32_t)R, W, ctx->runtime.p,
         overhead, ctx->agg_bsf.p, ctx->agg_times.p, d_total, d_first);

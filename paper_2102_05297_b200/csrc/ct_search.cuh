@@ -1079,218 +1079,6 @@ k_profile_search_ws(const SearchArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_profile_search_mq: S repetitions per CTA over one shared work queue.
-//
-// In k_profile_search a repetition's serial phases (profile step + expert
-// system, the n draws) keep its CTA's other warps idle at the barrier; with
-// R ~ 7 repetitions per SM there is no other repetition to run there.  Here a
-// CTA of W warps owns S repetition slots, and no warp has a fixed role.  Each
-// parallel phase of a slot is cut into NCH chunks -- exactly the shares the
-// warps of an NCH-warp k_profile_search take (score_phase / weight_phase
-// with ptid = 32 c + lane, pw = c) -- which any warp claims from the slot's
-// queue word.  The warp that completes a slot's last Eq. 16 chunk publishes
-// its Eq. 17 phase; the warp that completes its last Eq. 17 chunk runs the
-// slot's draws and next profile step itself and publishes the next Eq. 16
-// phase (or starts the slot's next repetition).  Meanwhile the other warps
-// take the other slots' chunks.  Every repetition executes the phases of
-// k_profile_search with NCH warps in the same order, so its trajectory is
-// identical.
-//
-// Queue word (one per slot): epoch << 32 | claimed-chunk count.  Publishing
-// a phase stores (epoch << 32); a claim is one 64-bit shared atomic add, and
-// the epoch it returns names the phase (even: Eq. 16, odd: Eq. 17) -- a
-// claim can never land in a later phase than the one it read, because a
-// phase completes only after all its chunks, the claimed one included.
-// Release/acquire: chunk results are published by __syncwarp + a block fence
-// before the completion atomic, and read after the completing atomic + fence.
-enum : unsigned { MQ_SCORE_PARITY = 0u };
-// a retired slot: the count field far above any NCH, and far enough below
-// 2^32 that stray claim increments can never carry into the epoch field
-constexpr unsigned long long MQ_EXHAUSTED = (0xffffffffull << 32) | 0x40000000ull;
-
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
-    return *reinterpret_cast<const volatile unsigned long long*>(p);
-}
-
-// Doorbell: an mbarrier with one expected arrival per phase.  Every publish
-// arrives on it (completing a phase) and bumps a counter; a warp that found
-// no chunk suspends in mbarrier.try_wait on the parity of the phase that was
-// current when it started looking, so it wakes at the next publish (or after
-// the hardware's suspend limit, and then simply looks again) instead of
-// spinning on the queue words and taking issue slots from working warps.
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}"
-                 ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
-    unsigned ok;
-    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}"
-                 : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
-    return ok != 0;
-}
-
-template <int W, int S, int NCH, int MINB, bool SMEM, bool PRE>
-__global__ void __launch_bounds__(32 * W, MINB)
-k_profile_search_mq(const SearchArgs a) {
-    static_assert(W >= S, "one warp per slot starts the slots");
-    constexpr int PT = 32 * NCH;
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ Ctl<NCH> ctl[S];
-    __shared__ RepState rs[S];
-    __shared__ unsigned long long claim[S];
-    __shared__ int done_cnt[S];
-    __shared__ int rep_of[S], it_of[S];
-    __shared__ unsigned epoch_of[S];
-    __shared__ int live;
-    __shared__ unsigned long long bell_bar;
-    __shared__ unsigned bell;
-    __shared__ uint32_t seed_sh[SEED_INLINE_WORDS];
-    __shared__ u128 jA[33], jC[33];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) { Pcg64::jump_tables(jA, jC, 32); live = S; bell = 0; mbar_init(&bell_bar, 1); }
-    load_seed_words(a.seed, seed_sh);      // ends with __syncthreads()
-
-    // dynamic shared memory, per slot: row totals | explored bits | [weights | in-row prefixes]
-    const size_t head = (16 * (size_t)a.nrows + 4 * (size_t)a.nwords + 15) & ~(size_t)15;
-    const size_t per_slot = head + (SMEM ? (PRE ? 16 : 8) * 32 * (size_t)a.nrows : 0);
-    const int stride = S * gridDim.x;
-    const int pcol = (lane < N_COMP) ? a.delta_col[lane] : -1;
-
-    auto slot_ptrs = [&](int s, double*& row_tot, uint32_t*& expl, double*& w, double*& pre) {
-        unsigned char* base = smem + per_slot * s;
-        row_tot = reinterpret_cast<double*>(base);
-        expl = reinterpret_cast<uint32_t*>(base + 16 * (size_t)a.nrows);
-        w = SMEM ? reinterpret_cast<double*>(base + head)
-                 : a.scratch_w + (size_t)(S * blockIdx.x + s) * 64 * (size_t)a.nrows;
-        pre = w + 32 * (size_t)a.nrows;
-    };
-    // publish slot s's next phase (the calling warp has written its inputs)
-    auto publish = [&](int s, unsigned epoch) {
-        __syncwarp();
-        if (lane == 0) {
-            epoch_of[s] = epoch;
-            done_cnt[s] = 0;
-            __threadfence_block();
-            atomicExch(&claim[s], (unsigned long long)epoch << 32);
-            mbar_arrive(&bell_bar);
-            atomicAdd(&bell, 1u);
-        }
-        __syncwarp();
-    };
-    // start slot s's next repetition that has a parallel phase to run
-    // (a repetition can end at its first profile step), or retire the slot
-    auto next_rep = [&](int s, int rep) {
-        double *row_tot, *w, *pre;
-        uint32_t* expl;
-        slot_ptrs(s, row_tot, expl, w, pre);
-        for (; rep < a.n_reps; rep += stride) {
-            int32_t* out_idx = a.step_index + (size_t)rep * a.max_steps;
-            uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
-            rep_begin(a, seed_sh, rep, rs[s], ctl[s], expl, lane);
-            if (a.outer > 0) profile_step(a, rs[s], ctl[s], expl, out_idx, out_prof, lane, pcol);
-            if (a.outer > 0 && !ctl[s].done) {
-                if (lane == 0) { rep_of[s] = rep; it_of[s] = 0; }
-                publish(s, (epoch_of[s] + 1u) & ~1u);     // next even epoch: Eq. 16
-                return;
-            }
-            if (lane == 0) rep_end(a, rep, rs[s]);
-            __syncwarp();
-        }
-        if (lane == 0) {
-            __threadfence_block();
-            atomicExch(&claim[s], MQ_EXHAUSTED);
-            atomicSub(&live, 1);
-            mbar_arrive(&bell_bar);
-            atomicAdd(&bell, 1u);
-        }
-        __syncwarp();
-    };
-
-    if (tid < S) { claim[tid] = MQ_EXHAUSTED; epoch_of[tid] = 1u; done_cnt[tid] = 0; }
-    __syncthreads();
-    if (warp < S) next_rep(warp, blockIdx.x * S + warp);
-    __syncthreads();
-
-    long long idle_since = -1;
-    int s0 = warp % S;
-    for (;;) {
-        int s = -1;
-        unsigned long long got = 0;
-        const unsigned bell0 = *reinterpret_cast<volatile unsigned*>(&bell);
-        // claim a chunk from the first slot (round robin from s0) that has one
-#pragma unroll 1
-        for (int i = 0; i < S; ++i) {
-            const int t = (s0 + i) % S;
-            const unsigned long long peek = ld_volatile_u64(&claim[t]);
-            if ((peek & 0xffffffffull) >= (unsigned long long)NCH) continue;
-            unsigned long long old = 0;
-            if (lane == 0) old = atomicAdd(&claim[t], 1ull);
-            old = __shfl_sync(FULL, old, 0);
-            if ((old & 0xffffffffull) < (unsigned long long)NCH) { s = t; got = old; break; }
-        }
-        if (s < 0) {
-            if (*reinterpret_cast<volatile int*>(&live) == 0) break;
-            // watchdog: a lost hand-off must end in an error, never a hang
-            const long long now = clock64();
-            if (idle_since < 0) idle_since = now;
-            else if (now - idle_since > (1ll << 35)) __trap();
-            mbar_try_wait(&bell_bar, bell0 & 1u);
-            continue;
-        }
-        idle_since = -1;
-        s0 = (s + 1) % S;
-        __threadfence_block();
-        const unsigned epoch = (unsigned)(got >> 32);
-        const int c = (int)(got & 0xffffffffull);
-        double *row_tot, *w, *pre;
-        uint32_t* expl;
-        slot_ptrs(s, row_tot, expl, w, pre);
-        if ((epoch & 1u) == MQ_SCORE_PARITY)
-            score_phase<PT, NCH>(a, ctl[s], expl, w, 32 * c + lane);
-        else
-            weight_phase<PRE, NCH>(a, ctl[s], expl, w, pre, row_tot, c);
-        __syncwarp();
-        int fin = 0;
-        if (lane == 0) {
-            __threadfence_block();
-            fin = atomicAdd(&done_cnt[s], 1) == NCH - 1;
-            __threadfence_block();
-        }
-        fin = __shfl_sync(FULL, fin, 0);
-        if (!fin) continue;
-        // this warp completed the phase
-        if ((epoch & 1u) == MQ_SCORE_PARITY) {
-            publish(s, epoch + 1u);                     // Eq. 17
-            continue;
-        }
-        const int rep = rep_of[s];
-        int32_t* out_idx = a.step_index + (size_t)rep * a.max_steps;
-        uint8_t* out_prof = a.step_profiled + (size_t)rep * a.max_steps;
-        draw_step<PRE, NCH, false>(a, rs[s], ctl[s], expl, w, pre, row_tot, jA, jC, out_idx,
-                                   out_prof, lane);
-        const int it = it_of[s] + 1;
-        if (!ctl[s].done && it < a.outer) {
-            profile_step(a, rs[s], ctl[s], expl, out_idx, out_prof, lane, pcol);
-            if (!ctl[s].done) {
-                if (lane == 0) it_of[s] = it;
-                publish(s, epoch + 1u);                 // next iteration's Eq. 16
-                continue;
-            }
-        }
-        if (lane == 0) rep_end(a, rep, rs[s]);
-        __syncwarp();
-        next_rep(s, rep + stride);
-    }
-}
-
-// ---------------------------------------------------------------------------
 // run_random_search (search.py:317-335): one thread per repetition shuffles
 // arange(N) with numpy's Fisher-Yates (random_interval) in a scratch slice and
 // emits the prefix up to the first stop configuration.

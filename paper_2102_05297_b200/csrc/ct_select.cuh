@@ -146,14 +146,23 @@ __device__ __forceinline__ double pow2d(int e) {          // 2^e, e in [-1022, 1
 __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t k0, double& c,
                                             double r, int lane) {
     const int64_t TWO53 = 1ll << 53;
-    for (int64_t base = k0 & ~(int64_t)127; base < n; base += 128) {
-        // this lane's four weights: elements base + 4 lane + j
-        double x[4];
+    // this lane's four weights of a block: elements base + 4 lane + j; the
+    // next block's are fetched while this one is scanned (the chain is then
+    // bound by the scan, not by a memory round trip per block)
+    auto fetch = [&](int64_t base, double* x) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int64_t e = base + 4 * lane + j;
             x[j] = (e >= k0 && e < n) ? w[e] : 0.0;
         }
+    };
+    double xn[4];
+    fetch(k0 & ~(int64_t)127, xn);
+    for (int64_t base = k0 & ~(int64_t)127; base < n; base += 128) {
+        double x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = xn[j];
+        fetch(base + 128, xn);
         int64_t from = max(k0, base);       // first element of the block still to add
         while (from < base + 128 && from < n) {
             // binade state of c; c == 0 (or subnormal): every element is a

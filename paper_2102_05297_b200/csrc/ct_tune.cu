@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
+#include <cstdio>
 #include <cupti_profiler_host.h>
 #include <cupti_profiler_target.h>
 #include <cupti_range_profiler.h>
@@ -601,8 +602,16 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     sc.pConfig = hc->image.data();
     sc.counterDataImageSize = data.size();
     sc.pCounterDataImage = data.data();
-    sc.range = CUPTI_UserRange;
-    sc.replayMode = CUPTI_UserReplay;
+    // CT_TUNE_REPLAY=kernel: CUPTI replays the launch itself (auto range,
+    // kernel replay, device memory saved and restored between passes);
+    // default: user range + user replay, one launch of ours per pass
+    static const bool kernel_replay = [] {
+        const char* e = std::getenv("CT_TUNE_REPLAY");
+        return e && std::string(e) == "kernel";
+    }();
+    static const bool trace = std::getenv("CT_TUNE_TRACE") != nullptr;
+    sc.range = kernel_replay ? CUPTI_AutoRange : CUPTI_UserRange;
+    sc.replayMode = kernel_replay ? CUPTI_KernelReplay : CUPTI_UserReplay;
     sc.maxRangesPerPass = 1;
     sc.numNestingLevels = 1;
     sc.minNestingLevel = 1;
@@ -612,23 +621,35 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     const auto t2 = clk::now();
     int used = 0;
     for (;;) {
+        const auto q0 = clk::now();
         CUpti_RangeProfiler_Start_Params st = {CUpti_RangeProfiler_Start_Params_STRUCT_SIZE};
         st.pRangeProfilerObject = t->rp;
         TU_CUPTI(cuptiRangeProfilerStart(&st));
-        CUpti_RangeProfiler_PushRange_Params pr = {CUpti_RangeProfiler_PushRange_Params_STRUCT_SIZE};
-        pr.pRangeProfilerObject = t->rp;
-        pr.pRangeName = "variant";
-        TU_CUPTI(cuptiRangeProfilerPushRange(&pr));
+        const auto q1 = clk::now();
+        if (!kernel_replay) {
+            CUpti_RangeProfiler_PushRange_Params pr = {CUpti_RangeProfiler_PushRange_Params_STRUCT_SIZE};
+            pr.pRangeProfilerObject = t->rp;
+            pr.pRangeName = "variant";
+            TU_CUPTI(cuptiRangeProfilerPushRange(&pr));
+        }
         rc = launch_once(t, v, l);
-        CUpti_RangeProfiler_PopRange_Params po = {CUpti_RangeProfiler_PopRange_Params_STRUCT_SIZE};
-        po.pRangeProfilerObject = t->rp;
-        TU_CUPTI(cuptiRangeProfilerPopRange(&po));
+        const auto q2 = clk::now();
+        if (!kernel_replay) {
+            CUpti_RangeProfiler_PopRange_Params po = {CUpti_RangeProfiler_PopRange_Params_STRUCT_SIZE};
+            po.pRangeProfilerObject = t->rp;
+            TU_CUPTI(cuptiRangeProfilerPopRange(&po));
+        }
         CUpti_RangeProfiler_Stop_Params sp = {CUpti_RangeProfiler_Stop_Params_STRUCT_SIZE};
         sp.pRangeProfilerObject = t->rp;
         TU_CUPTI(cuptiRangeProfilerStop(&sp));
+        const auto q3 = clk::now();
+        if (trace)
+            std::fprintf(stderr, "[ct_tune] pass %d: start %.1f us, push+launch %.1f us, pop+stop %.1f us%s\n",
+                         used, us(q0, q1), us(q1, q2), us(q2, q3),
+                         sp.isAllPassSubmitted ? " (all passes submitted)" : "");
         if (rc) return rc;
         ++used;
-        if (sp.isAllPassSubmitted) break;
+        if (sp.isAllPassSubmitted || kernel_replay) break;
         if (used > 64) return fail(CT_TUNE_ERR_PROFILER, "range profiler did not finish its passes");
     }
     const auto t3 = clk::now();
@@ -655,7 +676,7 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     t->prof_us[4] += us(t5, t6);
     t->prof_us[5] += 1;
     t->prof_us[6] += used;
-    if (passes) *passes = used;
+    if (passes) *passes = kernel_replay ? (int32_t)hc->passes : used;
     return CT_TUNE_OK;
 }
 

@@ -443,7 +443,14 @@ class CudaMeasurementSource:
 
     def __init__(self, bench: Benchmark, device: int = 0, tuner: Optional[Tuner] = None,
                  warmup: int = 1, reps: int = 3, flush_l2: bool = True,
-                 metrics: Sequence[str] = TABLE1_METRICS, slow_us: float = 5000.0):
+                 metrics: Sequence[str] = TABLE1_METRICS, slow_us: float = 5000.0,
+                 fill_from=None):
+        """metrics: the CUPTI metric set of a profiled step (Table 1, 24
+        metrics, 5 replay passes on B200).  fill_from: a PredictionTable; with
+        a reduced set -- GROUP1_METRICS, the largest single-pass subset
+         -- the Table-1 counters not collected are taken from its
+        prediction for the profiled configuration (mode "group1+model"),
+        a labelled approximation of the reference's full profile."""
         self.bench = bench
         self.tuner = tuner if tuner is not None else Tuner(device)
         self._own_tuner = tuner is None
@@ -452,6 +459,13 @@ class CudaMeasurementSource:
         self.warmup, self.reps, self.flush_l2 = warmup, reps, flush_l2
         self.slow_us = slow_us
         self.metrics = tuple(metrics)
+        self.fill_from = fill_from
+        collected = {cc.canonicalize(m, 1.0, self.arch)[0] for m in self.metrics}
+        self.filled = tuple(a for a in TABLE1_ABBRS if a not in collected)
+        if self.filled and fill_from is None:
+            raise ValueError("a reduced metric set needs fill_from (the model that predicts "
+                             f"{', '.join(self.filled)})")
+        self.mode = "full" if not self.filled else "group1+model"
         self._bufs = bench.setup(self.tuner)
         self._variants: Dict[int, int] = {}
         self.profile_passes = 0
@@ -524,6 +538,10 @@ class CudaMeasurementSource:
         for name, value in zip(self.metrics, vals):
             abbr, canonical = cc.canonicalize(name, float(value), self.arch)
             counter_map[abbr] = clamp_counter(abbr, canonical)
+        if self.filled:
+            row = self.fill_from.matrix[config_index]
+            for abbr in self.filled:
+                counter_map[abbr] = clamp_counter(abbr, float(row[self.fill_from.column[abbr]]))
         return Measurement(runtime_us=runtime, global_threads=launch.threads,
                            counters=counter_map)
 

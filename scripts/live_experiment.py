@@ -47,15 +47,22 @@ def replay(ds, reps, seed, overhead):
     return out
 
 
-def live(name, ds, k, seed):
-    """k real searches per searcher; wall seconds to the first <=1.1x config."""
+def live(name, ds, k, seed, mode="full"):
+    """k real searches per searcher; wall seconds to the first <=1.1x config.
+    mode "group1": profiled steps collect the single-pass 13-metric group and
+    take the other Table-1 counters from the model (labelled approximation)."""
     from paper_2102_05297_b200 import ExactModelSet, ProfileSearcher
-    from paper_2102_05297_b200.live import CudaMeasurementSource, benchmark
+    from paper_2102_05297_b200.live import GROUP1_METRICS, CudaMeasurementSource, benchmark
+    from paper_2102_05297_b200.search import PredictionTable
     from paper_2102_05297_b200.space import well_performing_set
     bench = benchmark(name)
-    src = CudaMeasurementSource(bench)
-    stop = set(well_performing_set(ds, 1.1))
     model = ExactModelSet(ds)
+    if mode == "group1":
+        src = CudaMeasurementSource(bench, metrics=GROUP1_METRICS,
+                                    fill_from=PredictionTable.from_model_set(model, ds.space))
+    else:
+        src = CudaMeasurementSource(bench)
+    stop = set(well_performing_set(ds, 1.1))
     res = {"profile_wall_s": [], "profile_steps": [], "random_wall_s": [], "random_steps": []}
     seeds = np.random.SeedSequence(seed).spawn(2 * k)
     for r in range(k):
@@ -94,6 +101,7 @@ def live(name, ds, k, seed):
     res["profiled_step_s"] = (t2 - t1) / 3
     res["timed_step_s"] = (t1 - t0) / 3
     res["profile_passes"] = src.profile_passes
+    res["mode"] = src.mode
     src.close()
     return res
 
@@ -106,6 +114,7 @@ def main():
     ap.add_argument("--live", type=int, default=0)
     ap.add_argument("--overhead", type=float, default=3.0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--mode", default="full", choices=("full", "group1"))
     a = ap.parse_args()
     from paper_2102_05297_b200 import formats, well_performing_set
     results = {}
@@ -117,7 +126,7 @@ def main():
              "well_performing": len(well_performing_set(ds, 1.1))}
         overhead = a.overhead
         if a.live:
-            r["live"] = live(name, ds, a.live, a.seed)
+            r["live"] = live(name, ds, a.live, a.seed, a.mode)
             overhead = r["live"]["profiled_step_s"] / max(r["live"]["timed_step_s"], 1e-9)
             r["measured_profiling_overhead"] = overhead
         r["replay"] = replay(ds, a.reps, a.seed, overhead)

@@ -22,8 +22,6 @@ def main():
     ap.add_argument("--kernel-only", action="store_true", help="one launch per space (ncu)")
     ap.add_argument("--env", default="",
                     help="';'-separated environment variants, each 'K=V+K=V' (e.g. CT_SEARCH_TILED=1)")
-    ap.add_argument("--mq", default="off",
-                    help="';'-separated CT_SEARCH_MQ builds ('W,S,NCH'; 'off' = k_profile_search)")
     a = ap.parse_args()
     import torch
     from paper_2102_05297_b200 import ExactModelSet, harness, spaces
@@ -54,7 +52,7 @@ def main():
         params, _ = harness.prepare_device(ctx, spec)
         ref = None
         envs = a.env.split(";") if a.env else [""]
-        for nt, mq, ev in [(x, y, z) for z in envs for y in a.mq.split(";") for x in a.nt.split(",")]:
+        for nt, ev in [(x, z) for z in envs for x in a.nt.split(",")]:
             for kv in [k for k in (a.env.replace(";", "+").split("+") if a.env else []) if k]:
                 os.environ.pop(kv.split("=")[0], None)
             for kv in [k for k in ev.split("+") if k]:
@@ -64,10 +62,6 @@ def main():
                 os.environ.pop("CT_SEARCH_NT", None)     # the launcher's choice
             else:
                 os.environ["CT_SEARCH_NT"] = nt
-            if mq == "off":
-                os.environ.pop("CT_SEARCH_MQ", None)
-            else:
-                os.environ["CT_SEARCH_MQ"] = mq
             harness.launch(ctx, spec, params, 0, a.reps)   # warm-up
             times = []
             for _ in range(0 if a.kernel_only else a.runs):
@@ -87,7 +81,7 @@ def main():
                 continue
             ms = sorted(times)[len(times) // 2]
             gbs = stats.algorithmic_bytes / (ms / 1e3) / 1e9
-            print(json.dumps({"space": name, "n": len(ds.space), "nt": nt, "mq": mq, "env": ev, "ms": ms,
+            print(json.dumps({"space": name, "n": len(ds.space), "nt": nt, "env": ev, "ms": ms,
                               "reps": a.reps, "outer": a.outer,
                               "algorithmic_bytes": int(stats.algorithmic_bytes),
                               "configs_per_s": stats.configs_scored / (ms / 1e3),
@@ -95,7 +89,6 @@ def main():
                               "uncertified": int(stats.uncertified),
                               "same_as_first": same}), flush=True)
     os.environ.pop("CT_SEARCH_NT", None)
-    os.environ.pop("CT_SEARCH_MQ", None)
 
 
 if __name__ == "__main__":

@@ -50,27 +50,6 @@ def test_kernel_variants_match_reference(name, env, monkeypatch):
     _check_trajectories(name)
 
 
-# the shared-queue kernel (k_profile_search_mq<W, S, NCH>): S repetition slots
-# per CTA of W warps, NCH chunks per parallel phase, any warp runs any slot's
-# chunks and serial phases -- every build on every trajectory set (the PRE
-# layout on the small spaces), and with the weights in a global slice
-MQ_BUILDS = ["4,1,4", "12,4,4"]
-
-
-@pytest.mark.parametrize("mq", MQ_BUILDS)
-@pytest.mark.parametrize("name", TRAJ_SETS)
-def test_shared_queue_kernel_matches_reference(name, mq, monkeypatch):
-    monkeypatch.setenv("CT_SEARCH_MQ", mq)
-    _check_trajectories(name)
-
-
-@pytest.mark.parametrize("mq", ["12,4,4"])
-def test_shared_queue_kernel_global_weights_matches_reference(mq, monkeypatch):
-    monkeypatch.setenv("CT_SEARCH_MQ", mq)
-    monkeypatch.setenv("CT_SEARCH_SMEM", "0")
-    _check_trajectories("b200_transpose")
-
-
 # the tiled large-space path (ct_tiled.cuh: grid-wide Eq. 16 / Eq. 17 kernels
 # per outer iteration, one warp per repetition for the draws), forced on every
 # trajectory set (tiles of 4096 configurations: one partial tile here)
