@@ -99,6 +99,14 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l,
                      const char* const* metrics, int32_t n_metrics, double* values,
                      int32_t* passes);
 
+/* The same collection for k launches at once (an exhaustive sweep): one
+ * range per launch, every pass launches all k, so the profiler's
+ * per-collection cost (configuration, the SASS-instrumentation passes) is
+ * paid once per k configurations.  values[k * n_metrics], row i = launch i. */
+int ct_tuner_profile_batch(ct_tuner* t, int32_t k, const int32_t* variants,
+                           const ct_launch* launches, const char* const* metrics,
+                           int32_t n_metrics, double* values, int32_t* passes);
+
 /* Number of replay passes the metric set needs on this device (host-side
  * configuration only, no launch). */
 int ct_tuner_profile_passes(ct_tuner* t, const char* const* metrics, int32_t n_metrics,

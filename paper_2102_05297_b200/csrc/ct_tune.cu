@@ -602,16 +602,11 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     sc.pConfig = hc->image.data();
     sc.counterDataImageSize = data.size();
     sc.pCounterDataImage = data.data();
-    // CT_TUNE_REPLAY=kernel: CUPTI replays the launch itself (auto range,
-    // kernel replay, device memory saved and restored between passes);
-    // default: user range + user replay, one launch of ours per pass
-    static const bool kernel_replay = [] {
-        const char* e = std::getenv("CT_TUNE_REPLAY");
-        return e && std::string(e) == "kernel";
-    }();
+    // user range + user replay: one launch of ours per pass (CUPTI's kernel
+    // replay with an auto range returned zeros for every metric here)
     static const bool trace = std::getenv("CT_TUNE_TRACE") != nullptr;
-    sc.range = kernel_replay ? CUPTI_AutoRange : CUPTI_UserRange;
-    sc.replayMode = kernel_replay ? CUPTI_KernelReplay : CUPTI_UserReplay;
+    sc.range = CUPTI_UserRange;
+    sc.replayMode = CUPTI_UserReplay;
     sc.maxRangesPerPass = 1;
     sc.numNestingLevels = 1;
     sc.minNestingLevel = 1;
@@ -626,19 +621,15 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
         st.pRangeProfilerObject = t->rp;
         TU_CUPTI(cuptiRangeProfilerStart(&st));
         const auto q1 = clk::now();
-        if (!kernel_replay) {
-            CUpti_RangeProfiler_PushRange_Params pr = {CUpti_RangeProfiler_PushRange_Params_STRUCT_SIZE};
-            pr.pRangeProfilerObject = t->rp;
-            pr.pRangeName = "variant";
-            TU_CUPTI(cuptiRangeProfilerPushRange(&pr));
-        }
+        CUpti_RangeProfiler_PushRange_Params pr = {CUpti_RangeProfiler_PushRange_Params_STRUCT_SIZE};
+        pr.pRangeProfilerObject = t->rp;
+        pr.pRangeName = "variant";
+        TU_CUPTI(cuptiRangeProfilerPushRange(&pr));
         rc = launch_once(t, v, l);
         const auto q2 = clk::now();
-        if (!kernel_replay) {
-            CUpti_RangeProfiler_PopRange_Params po = {CUpti_RangeProfiler_PopRange_Params_STRUCT_SIZE};
-            po.pRangeProfilerObject = t->rp;
-            TU_CUPTI(cuptiRangeProfilerPopRange(&po));
-        }
+        CUpti_RangeProfiler_PopRange_Params po = {CUpti_RangeProfiler_PopRange_Params_STRUCT_SIZE};
+        po.pRangeProfilerObject = t->rp;
+        TU_CUPTI(cuptiRangeProfilerPopRange(&po));
         CUpti_RangeProfiler_Stop_Params sp = {CUpti_RangeProfiler_Stop_Params_STRUCT_SIZE};
         sp.pRangeProfilerObject = t->rp;
         TU_CUPTI(cuptiRangeProfilerStop(&sp));
@@ -649,7 +640,7 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
                          sp.isAllPassSubmitted ? " (all passes submitted)" : "");
         if (rc) return rc;
         ++used;
-        if (sp.isAllPassSubmitted || kernel_replay) break;
+        if (sp.isAllPassSubmitted) break;
         if (used > 64) return fail(CT_TUNE_ERR_PROFILER, "range profiler did not finish its passes");
     }
     const auto t3 = clk::now();
@@ -676,7 +667,101 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     t->prof_us[4] += us(t5, t6);
     t->prof_us[5] += 1;
     t->prof_us[6] += used;
-    if (passes) *passes = kernel_replay ? (int32_t)hc->passes : used;
+    if (passes) *passes = used;
+    return CT_TUNE_OK;
+}
+
+int ct_tuner_profile_batch(ct_tuner* t, int32_t k, const int32_t* variants,
+                           const ct_launch* launches, const char* const* metrics, int32_t n,
+                           double* values, int32_t* passes) {
+    int rc = activate(t); if (rc) return rc;
+    if (k < 1 || !variants || !launches || !metrics || n < 1 || !values)
+        return fail(CT_TUNE_ERR_VALUE, "bad batch profile arguments");
+    std::vector<Variant*> vs((size_t)k);
+    for (int i = 0; i < k; ++i) { rc = get_variant(t, variants[i], &vs[i]); if (rc) return rc; }
+    rc = cupti_init(t); if (rc) return rc;
+    HostConfig* hc = nullptr;
+    rc = host_config_cached(t, metrics, n, &hc); if (rc) return rc;
+    if (t->rp_config && t->rp_config != hc) {
+        CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
+        dp.pRangeProfilerObject = t->rp;
+        TU_CUPTI(cuptiRangeProfilerDisable(&dp));
+        CUpti_RangeProfiler_Enable_Params ep = {CUpti_RangeProfiler_Enable_Params_STRUCT_SIZE};
+        ep.ctx = t->ctx;
+        TU_CUPTI(cuptiRangeProfilerEnable(&ep));
+        t->rp = ep.pRangeProfilerObject;
+        for (auto& kv : t->configs) kv.second->counter_data.clear();
+    }
+    t->rp_config = hc;
+    // a counter-data image for k ranges (per call: k varies)
+    CUpti_RangeProfiler_GetCounterDataSize_Params cs = {CUpti_RangeProfiler_GetCounterDataSize_Params_STRUCT_SIZE};
+    cs.pRangeProfilerObject = t->rp;
+    cs.pMetricNames = hc->name_ptrs.data();
+    cs.numMetrics = (size_t)n;
+    cs.maxNumOfRanges = (size_t)k;
+    cs.maxNumRangeTreeNodes = (size_t)k;
+    TU_CUPTI(cuptiRangeProfilerGetCounterDataSize(&cs));
+    std::vector<uint8_t> data(cs.counterDataSize, 0);
+    CUpti_RangeProfiler_CounterDataImage_Initialize_Params ci = {CUpti_RangeProfiler_CounterDataImage_Initialize_Params_STRUCT_SIZE};
+    ci.pRangeProfilerObject = t->rp;
+    ci.counterDataSize = data.size();
+    ci.pCounterData = data.data();
+    TU_CUPTI(cuptiRangeProfilerCounterDataImageInitialize(&ci));
+    CUpti_RangeProfiler_SetConfig_Params sc = {CUpti_RangeProfiler_SetConfig_Params_STRUCT_SIZE};
+    sc.pRangeProfilerObject = t->rp;
+    sc.configSize = hc->image.size();
+    sc.pConfig = hc->image.data();
+    sc.counterDataImageSize = data.size();
+    sc.pCounterDataImage = data.data();
+    sc.range = CUPTI_UserRange;
+    sc.replayMode = CUPTI_UserReplay;
+    sc.maxRangesPerPass = (size_t)k;
+    sc.numNestingLevels = 1;
+    sc.minNestingLevel = 1;
+    sc.passIndex = 0;
+    sc.targetNestingLevel = 1;
+    TU_CUPTI(cuptiRangeProfilerSetConfig(&sc));
+    std::vector<std::string> names((size_t)k);
+    for (int i = 0; i < k; ++i) names[i] = "r" + std::to_string(i);
+    int used = 0;
+    for (;;) {
+        CUpti_RangeProfiler_Start_Params st = {CUpti_RangeProfiler_Start_Params_STRUCT_SIZE};
+        st.pRangeProfilerObject = t->rp;
+        TU_CUPTI(cuptiRangeProfilerStart(&st));
+        for (int i = 0; i < k && rc == 0; ++i) {
+            CUpti_RangeProfiler_PushRange_Params pr = {CUpti_RangeProfiler_PushRange_Params_STRUCT_SIZE};
+            pr.pRangeProfilerObject = t->rp;
+            pr.pRangeName = names[i].c_str();
+            TU_CUPTI(cuptiRangeProfilerPushRange(&pr));
+            rc = launch_once(t, vs[i], &launches[i]);
+            CUpti_RangeProfiler_PopRange_Params po = {CUpti_RangeProfiler_PopRange_Params_STRUCT_SIZE};
+            po.pRangeProfilerObject = t->rp;
+            TU_CUPTI(cuptiRangeProfilerPopRange(&po));
+        }
+        CUpti_RangeProfiler_Stop_Params sp = {CUpti_RangeProfiler_Stop_Params_STRUCT_SIZE};
+        sp.pRangeProfilerObject = t->rp;
+        TU_CUPTI(cuptiRangeProfilerStop(&sp));
+        if (rc) return rc;
+        ++used;
+        if (sp.isAllPassSubmitted) break;
+        if (used > 64) return fail(CT_TUNE_ERR_PROFILER, "range profiler did not finish its passes");
+    }
+    TU_RT(cudaStreamSynchronize(t->stream));
+    CUpti_RangeProfiler_DecodeData_Params dd = {CUpti_RangeProfiler_DecodeData_Params_STRUCT_SIZE};
+    dd.pRangeProfilerObject = t->rp;
+    TU_CUPTI(cuptiRangeProfilerDecodeData(&dd));
+    for (int i = 0; i < k; ++i) {
+        CUpti_Profiler_Host_EvaluateToGpuValues_Params ev = {sizeof(CUpti_Profiler_Host_EvaluateToGpuValues_Params)};
+        ev.pHostObject = hc->host;
+        ev.pCounterDataImage = data.data();
+        ev.counterDataImageSize = data.size();
+        ev.rangeIndex = (size_t)i;
+        ev.ppMetricNames = hc->name_ptrs.data();
+        ev.numMetrics = (size_t)n;
+        ev.pMetricValues = values + (size_t)i * n;
+        TU_CUPTI(cuptiProfilerHostEvaluateToGpuValues(&ev));
+    }
+    if (passes) *passes = used;
     return CT_TUNE_OK;
 }
 

@@ -446,11 +446,15 @@ class CudaMeasurementSource:
                  metrics: Sequence[str] = TABLE1_METRICS, slow_us: float = 5000.0,
                  fill_from=None):
         """metrics: the CUPTI metric set of a profiled step (Table 1, 24
-        metrics, 5 replay passes on B200).  fill_from: a PredictionTable; with
-        a reduced set -- GROUP1_METRICS, the largest single-pass subset
-         -- the Table-1 counters not collected are taken from its
-        prediction for the profiled configuration (mode "group1+model"),
-        a labelled approximation of the reference's full profile."""
+        metrics, 5 replay passes on B200).  With a reduced set --
+        GROUP1_METRICS, the largest single-pass subset -- the
+        Table-1 counters not collected are taken from fill_from for the
+        profiled configuration (mode "group1+model"), a labelled
+        approximation of the reference's full profile: a PredictionTable
+        (its model's prediction; the exact/tree models do not predict the
+        utilisations, so SHR_U -- outside group 1, a second pass on B200 --
+        needs the next source) or a Dataset (a recorded sweep of the space,
+        which is what the exact model replays)."""
         self.bench = bench
         self.tuner = tuner if tuner is not None else Tuner(device)
         self._own_tuner = tuner is None
@@ -462,9 +466,18 @@ class CudaMeasurementSource:
         self.fill_from = fill_from
         collected = {cc.canonicalize(m, 1.0, self.arch)[0] for m in self.metrics}
         self.filled = tuple(a for a in TABLE1_ABBRS if a not in collected)
-        if self.filled and fill_from is None:
-            raise ValueError("a reduced metric set needs fill_from (the model that predicts "
-                             f"{', '.join(self.filled)})")
+        if self.filled:
+            if fill_from is None:
+                raise ValueError("a reduced metric set needs fill_from (the model that predicts "
+                                 f"{', '.join(self.filled)})")
+            names = (fill_from.column if hasattr(fill_from, "column")
+                     else {a: j for j, a in enumerate(fill_from.counter_names)})
+            missing = [a for a in self.filled if a not in names]
+            if missing:
+                raise ValueError(f"fill_from does not provide {', '.join(missing)}")
+            self._fill_col = {a: names[a] for a in self.filled}
+            self._fill_rows = (fill_from.matrix if hasattr(fill_from, "column")
+                               else fill_from.counter_matrix)
         self.mode = "full" if not self.filled else "group1+model"
         self._bufs = bench.setup(self.tuner)
         self._variants: Dict[int, int] = {}
@@ -539,11 +552,32 @@ class CudaMeasurementSource:
             abbr, canonical = cc.canonicalize(name, float(value), self.arch)
             counter_map[abbr] = clamp_counter(abbr, canonical)
         if self.filled:
-            row = self.fill_from.matrix[config_index]
+            row = self._fill_rows[config_index]
             for abbr in self.filled:
-                counter_map[abbr] = clamp_counter(abbr, float(row[self.fill_from.column[abbr]]))
+                counter_map[abbr] = clamp_counter(abbr, float(row[self._fill_col[abbr]]))
         return Measurement(runtime_us=runtime, global_threads=launch.threads,
                            counters=counter_map)
+
+    def profile_many(self, indices: Sequence[int]):
+        """The profiled half of measure() for several configurations in ONE
+        CUPTI collection (ct_tuner_profile_batch: one range per launch, the
+        per-collection cost paid once) -> [(global_threads, counters)]."""
+        vs = [self.variant(i) for i in indices]
+        launches = [self.launch_of(i) for i in indices]
+        vals, passes = self.tuner.profile_batch(vs, launches, self.metrics)
+        self.profile_passes = passes
+        out = []
+        for i, launch, row in zip(indices, launches, vals):
+            counter_map: Dict[str, float] = {}
+            for name, value in zip(self.metrics, row):
+                abbr, canonical = cc.canonicalize(name, float(value), self.arch)
+                counter_map[abbr] = clamp_counter(abbr, canonical)
+            if self.filled:
+                frow = self._fill_rows[i]
+                for abbr in self.filled:
+                    counter_map[abbr] = clamp_counter(abbr, float(frow[self._fill_col[abbr]]))
+            out.append((launch.threads, counter_map))
+        return out
 
     def output(self, config_index: int) -> np.ndarray:
         """Run the variant once and fetch its output (for oracle checks)."""
@@ -573,7 +607,7 @@ class SweepResult:
 
 def sweep(source: CudaMeasurementSource, profiled: bool = True, checkpoint: Optional[str] = None,
           compile_threads: int = 0, progress=None,
-          budget_s: Optional[float] = None) -> SweepResult:
+          budget_s: Optional[float] = None, batch: int = 32) -> SweepResult:
     """Exhaustive sweep of the source's space -> a replay Dataset in the
     reference's layout (runtime, threads, the Table-1 counters canonicalised).
 
@@ -595,27 +629,43 @@ def sweep(source: CudaMeasurementSource, profiled: bool = True, checkpoint: Opti
     source.compile_all([i for i in range(n) if not done[i]], threads=compile_threads)
     t1 = time.perf_counter()
     failures = dict(source.compile_failures)
-    for i in range(n):
-        if done[i] or i in failures:
-            continue
+    todo = [i for i in range(n) if not done[i] and i not in failures]
+    # chunks of `batch` configurations: each timed on its own (median of the
+    # source's reps, L2 flushed), then profiled together in one CUPTI
+    # collection (profile_many); a chunk whose collection fails is profiled
+    # one configuration at a time
+    for c0 in range(0, len(todo), batch):
         if budget_s is not None and time.perf_counter() - t0 > budget_s:
             break
-        try:
-            m = source.measure(i, profiled=profiled)
-        except CounterTuneError as e:
-            failures[i] = str(e)
-            continue
-        runtime[i] = m.runtime_us
-        if profiled:
-            threads[i] = m.global_threads
-            cm[i] = [m.counters[a] for a in names]
-        done[i] = True
-        if checkpoint and (i % 64 == 63 or i == n - 1):
+        timed = []
+        for i in todo[c0:c0 + batch]:
+            try:
+                runtime[i] = source.measure(i, profiled=False).runtime_us
+                timed.append(i)
+            except CounterTuneError as e:
+                failures[i] = str(e)
+        if profiled and timed:
+            try:
+                got = source.profile_many(timed)
+            except CounterTuneError:
+                got = []
+                for i in list(timed):
+                    try:
+                        got.append(source.profile_many([i])[0])
+                    except CounterTuneError as e:
+                        failures[i] = str(e)
+                        timed.remove(i)
+            for i, (th, counters) in zip(timed, got):
+                threads[i] = th
+                cm[i] = [counters[a] for a in names]
+        for i in timed:
+            done[i] = True
+        if checkpoint:
             np.savez(checkpoint, runtime=runtime, threads=threads, counters=cm, done=done)
+        if progress and timed:
+            progress(timed[-1], n)
     if checkpoint:
         np.savez(checkpoint, runtime=runtime, threads=threads, counters=cm, done=done)
-        if progress:
-            progress(i, n)
     t2 = time.perf_counter()
     # configurations that failed to build or launch carry no record: replaying
     # them raises, as the reference's replay source does (search.py:205-214)

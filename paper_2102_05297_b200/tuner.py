@@ -74,6 +74,8 @@ SIGNATURES = {
     "ct_tuner_profile": (ctypes.c_int, [_vp, _i32, _P(LaunchC), _P(_cp), _i32,
                                         _P(ctypes.c_double), _P(_i32)]),
     "ct_tuner_profile_passes": (ctypes.c_int, [_vp, _P(_cp), _i32, _P(_i32)]),
+    "ct_tuner_profile_batch": (ctypes.c_int, [_vp, _i32, _P(_i32), _P(LaunchC), _P(_cp), _i32,
+                                              _P(ctypes.c_double), _P(_i32)]),
     "ct_tuner_profile_timing": (ctypes.c_int, [_vp, _P(ctypes.c_double), _i32]),
     "ct_tuner_tensor_map_2d": (ctypes.c_int, [_vp, _u64, _u64, _u64, _u64, ctypes.c_uint32,
                                               ctypes.c_uint32, _vp]),
@@ -264,6 +266,21 @@ class Tuner:
                                           _cstrings(metrics), len(metrics),
                                           vals.ctypes.data_as(_P(ctypes.c_double)),
                                           ctypes.byref(passes)))
+        return vals, passes.value
+
+    def profile_batch(self, variants: Sequence[int], launches: Sequence[Launch],
+                      metrics: Sequence[str]) -> Tuple[np.ndarray, int]:
+        """ct_tuner_profile_batch: one collection over k launches, one range
+        each -> (k x len(metrics) values, replay passes)."""
+        k = len(variants)
+        vals = np.zeros((k, len(metrics)), dtype=np.float64)
+        vs = (_i32 * k)(*[int(v) for v in variants])
+        ls = (LaunchC * k)(*[l.c for l in launches])
+        passes = _i32()
+        _check(self._lib.ct_tuner_profile_batch(self._h, k, vs, ls, _cstrings(metrics),
+                                                len(metrics),
+                                                vals.ctypes.data_as(_P(ctypes.c_double)),
+                                                ctypes.byref(passes)))
         return vals, passes.value
 
     def tensor_map_2d(self, ptr: int, dim0: int, dim1: int, row_stride_bytes: int, box0: int,

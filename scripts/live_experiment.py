@@ -50,16 +50,15 @@ def replay(ds, reps, seed, overhead):
 def live(name, ds, k, seed, mode="full"):
     """k real searches per searcher; wall seconds to the first <=1.1x config.
     mode "group1": profiled steps collect the single-pass 13-metric group and
-    take the other Table-1 counters from the model (labelled approximation)."""
+    take the other Table-1 counters from the recorded sweep (labelled
+    approximation)."""
     from paper_2102_05297_b200 import ExactModelSet, ProfileSearcher
     from paper_2102_05297_b200.live import GROUP1_METRICS, CudaMeasurementSource, benchmark
-    from paper_2102_05297_b200.search import PredictionTable
     from paper_2102_05297_b200.space import well_performing_set
     bench = benchmark(name)
     model = ExactModelSet(ds)
     if mode == "group1":
-        src = CudaMeasurementSource(bench, metrics=GROUP1_METRICS,
-                                    fill_from=PredictionTable.from_model_set(model, ds.space))
+        src = CudaMeasurementSource(bench, metrics=GROUP1_METRICS, fill_from=ds)
     else:
         src = CudaMeasurementSource(bench)
     stop = set(well_performing_set(ds, 1.1))

@@ -10,7 +10,7 @@
   (the lines still dirty in the L2 at kernel end are written back outside
   the range);
 * two collections of the same launch agree within 1% (the deterministic
-  counters exactly).
+  counters exactly; DRAM writes only within the L2 bound above).
 """
 
 import os
@@ -87,7 +87,34 @@ def test_transpose_dram_sectors_match_algorithmic_bytes(tuner):
     # of the algorithmic writes goes uncounted
     import torch
     l2_sectors = torch.cuda.get_device_properties(0).L2_cache_size / 32
-    assert sectors - l2_sectors <= a[1] <= 1.05 * sectors, a
+    for x in (a, b):
+        assert sectors - l2_sectors <= x[1] <= 1.05 * sectors, x
     assert a[2] >= 0.95 * sectors and a[3] >= 0.95 * sectors, a
-    np.testing.assert_allclose(a[:4], b[:4], rtol=0.01)
+    # two collections agree (DRAM writes excepted: how many of the previous
+    # launch's dirty lines drain inside the range depends on the L2's state)
+    np.testing.assert_allclose(a[[0, 2, 3]], b[[0, 2, 3]], rtol=0.01)
     assert a[4] == b[4] and a[5] == b[5]        # instruction counts are deterministic
+
+
+def test_batched_collection_matches_single_collections(tuner):
+    """ct_tuner_profile_batch (one CUPTI collection, one range per launch --
+    what the sweeps use) reads the same counters as one collection per
+    launch: instruction counts and shared-memory wavefronts exactly, L2
+    sector counts within 2%."""
+    from paper_2102_05297_b200.live import TABLE1_METRICS, CudaMeasurementSource, benchmark
+    from paper_2102_05297_b200 import counters as cc
+    src = CudaMeasurementSource(benchmark("transpose", width=1024, height=1024), tuner=tuner)
+    idx = list(range(0, len(src.space), max(1, len(src.space) // 12)))[:12]
+    vs = [src.variant(i) for i in idx]
+    ls = [src.launch_of(i) for i in idx]
+    ms = list(TABLE1_METRICS)
+    batch, passes = tuner.profile_batch(vs, ls, ms)
+    assert batch.shape == (len(idx), len(ms)) and passes > 1
+    exact = [k for k, m in enumerate(ms) if m.endswith(".sum")
+             and ("inst_executed" in m or "wavefronts" in m)]
+    l2 = [k for k, m in enumerate(ms) if m.startswith("lts__t_sectors") and m.endswith(".sum")]
+    assert exact and l2
+    for row, v, l in zip(batch, vs, ls):
+        single, _ = tuner.profile(v, l, ms)
+        np.testing.assert_array_equal(row[exact], single[exact])
+        np.testing.assert_allclose(row[l2], single[l2], rtol=0.02)

@@ -166,9 +166,10 @@ def test_live_profile_search_runs(tuner):
 def test_group1_single_pass_profiled_step(tuner):
     """The labelled single-pass mode: a profiled step collects the 13-metric
     group 1 in ONE CUPTI pass and takes the other Table-1 counters from the
-    model's prediction for the profiled configuration; a live search runs on
-    it, and the collected counters agree with a full 24-metric profile of
-    the same launch (DRAM / L2 sectors and instruction counts within 5%)."""
+    recorded sweep of the space (what the exact model replays; SHR_U is in
+    no model and not in group 1); a live search runs on it, and the
+    collected counters agree with a full 24-metric profile of the same
+    launch (DRAM / L2 sectors and instruction counts within 5%)."""
     from paper_2102_05297_b200 import ExactModelSet, run_profile_search
     from paper_2102_05297_b200.live import (GROUP1_ABBRS, GROUP1_METRICS, CudaMeasurementSource,
                                             benchmark, sweep)
@@ -177,7 +178,9 @@ def test_group1_single_pass_profiled_step(tuner):
     full = CudaMeasurementSource(b, tuner=tuner, reps=2)
     ds = sweep(full, profiled=True).dataset
     table = PredictionTable.from_model_set(ExactModelSet(ds), ds.space)
-    g1 = CudaMeasurementSource(b, tuner=tuner, reps=2, metrics=GROUP1_METRICS, fill_from=table)
+    with pytest.raises(ValueError, match="SHR_U"):       # no model predicts it
+        CudaMeasurementSource(b, tuner=tuner, metrics=GROUP1_METRICS, fill_from=table)
+    g1 = CudaMeasurementSource(b, tuner=tuner, reps=2, metrics=GROUP1_METRICS, fill_from=ds)
     assert g1.mode == "group1+model" and full.mode == "full"
     best = int(np.argmin(ds.runtime_us))
     m1 = g1.measure(best, profiled=True)
@@ -188,8 +191,9 @@ def test_group1_single_pass_profiled_step(tuner):
     for a in ("DRAM_RT", "L2_RT", "L2_WT", "INST_EXE"):
         assert a in GROUP1_ABBRS
         assert abs(m1.counters[a] - mf.counters[a]) <= 0.05 * max(mf.counters[a], 1.0), a
-    for a in set(mf.counters) - set(GROUP1_ABBRS):   # from the model's row
-        assert m1.counters[a] == pytest.approx(table.matrix[best, table.column[a]]), a
+    col = {a: j for j, a in enumerate(ds.counter_names)}
+    for a in set(mf.counters) - set(GROUP1_ABBRS):   # from the recorded sweep
+        assert m1.counters[a] == pytest.approx(ds.counter_matrix[best, col[a]]), a
     trace = run_profile_search(g1, ExactModelSet(ds), i=3, seed=2)
     assert len(trace.steps) == 3 * 6
 
