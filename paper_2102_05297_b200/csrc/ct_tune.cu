@@ -162,6 +162,7 @@ struct ct_tuner {
     // (it keeps the first set's pass count and leaves the new metrics NaN),
     // so a switch of set re-creates the object
     const void* rp_config = nullptr;
+    int32_t rp_ranges = 0;            // ranges per pass it was configured for
     // host configurations by metric set (building one costs milliseconds)
     std::map<std::string, std::unique_ptr<HostConfig>> configs;
     // wall time of ct_tuner_profile by phase (microseconds, accumulated):
@@ -315,6 +316,29 @@ int host_config_cached(ct_tuner* t, const char* const* metrics, int32_t n, HostC
         it = t->configs.emplace(key, std::move(hc)).first;
     }
     *out = it->second.get();
+    return CT_TUNE_OK;
+}
+
+// The range-profiler object serves one collection shape: a SetConfig with
+// another metric set does not take effect on it (the first set's pass count
+// stays, the new metrics read NaN), and after a k-range collection a 1-range
+// counter-data image no longer initialises against it.  A change of (metric
+// set, ranges per pass) therefore re-creates the object.
+int rp_shape(ct_tuner* t, HostConfig* hc, int32_t ranges) {
+    if (t->rp_config && (t->rp_config != hc || t->rp_ranges != ranges)) {
+        CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
+        dp.pRangeProfilerObject = t->rp;
+        TU_CUPTI(cuptiRangeProfilerDisable(&dp));
+        CUpti_RangeProfiler_Enable_Params ep = {CUpti_RangeProfiler_Enable_Params_STRUCT_SIZE};
+        ep.ctx = t->ctx;
+        TU_CUPTI(cuptiRangeProfilerEnable(&ep));
+        t->rp = ep.pRangeProfilerObject;
+        // counter-data images were sized and initialised against the old
+        // object: every configuration re-derives its image under the new one
+        for (auto& kv : t->configs) kv.second->counter_data.clear();
+    }
+    t->rp_config = hc;
+    t->rp_ranges = ranges;
     return CT_TUNE_OK;
 }
 
@@ -564,19 +588,7 @@ int ct_tuner_profile(ct_tuner* t, int32_t variant, const ct_launch* l, const cha
     const auto t0 = clk::now();
     HostConfig* hc = nullptr;
     rc = host_config_cached(t, metrics, n, &hc); if (rc) return rc;
-    if (t->rp_config && t->rp_config != hc) {
-        CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
-        dp.pRangeProfilerObject = t->rp;
-        TU_CUPTI(cuptiRangeProfilerDisable(&dp));
-        CUpti_RangeProfiler_Enable_Params ep = {CUpti_RangeProfiler_Enable_Params_STRUCT_SIZE};
-        ep.ctx = t->ctx;
-        TU_CUPTI(cuptiRangeProfilerEnable(&ep));
-        t->rp = ep.pRangeProfilerObject;
-        // counter-data images were sized and initialised against the old
-        // object: every configuration re-derives its image under the new one
-        for (auto& kv : t->configs) kv.second->counter_data.clear();
-    }
-    t->rp_config = hc;
+    rc = rp_shape(t, hc, 1); if (rc) return rc;
     const auto t1 = clk::now();
     t->prof_us[7] += us(t0, t1);
     // counter data image for one range (re-initialised per collection)
@@ -682,17 +694,7 @@ int ct_tuner_profile_batch(ct_tuner* t, int32_t k, const int32_t* variants,
     rc = cupti_init(t); if (rc) return rc;
     HostConfig* hc = nullptr;
     rc = host_config_cached(t, metrics, n, &hc); if (rc) return rc;
-    if (t->rp_config && t->rp_config != hc) {
-        CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
-        dp.pRangeProfilerObject = t->rp;
-        TU_CUPTI(cuptiRangeProfilerDisable(&dp));
-        CUpti_RangeProfiler_Enable_Params ep = {CUpti_RangeProfiler_Enable_Params_STRUCT_SIZE};
-        ep.ctx = t->ctx;
-        TU_CUPTI(cuptiRangeProfilerEnable(&ep));
-        t->rp = ep.pRangeProfilerObject;
-        for (auto& kv : t->configs) kv.second->counter_data.clear();
-    }
-    t->rp_config = hc;
+    rc = rp_shape(t, hc, k); if (rc) return rc;
     // a counter-data image for k ranges (per call: k varies)
     CUpti_RangeProfiler_GetCounterDataSize_Params cs = {CUpti_RangeProfiler_GetCounterDataSize_Params_STRUCT_SIZE};
     cs.pRangeProfilerObject = t->rp;
