@@ -804,8 +804,14 @@ int launch_tiled(ct_ctx* ctx, SearchArgs& a, int n_reps) {
     return CT_OK;
 }
 
-// spaces above this size take the tiled path by default
-constexpr int64_t TILED_MIN_N = 1ll << 40;   // set from measurements
+// spaces in [TILED_MIN_N, TILED_MAX_N] take the tiled path by default
+// (measured, profiles/r02/r02l_n_sweep.jsonl): from ~10^5 configurations the
+// grid-wide phases beat one CTA per repetition (GEMM-full 205k: 142 vs
+// 176 ms, 1M: 113 vs 123 ms); at 4M the rare re-decided draws, which stall
+// every repetition at the iteration barrier of the tiled path but only
+// their own CTA in the persistent kernel, tip it back (692 vs 555 ms)
+constexpr int64_t TILED_MIN_N = 131072;
+constexpr int64_t TILED_MAX_N = 1ll << 21;
 
 template <int PW>
 int launch_profile_ws(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int n_reps) {
@@ -1282,7 +1288,7 @@ int ct_profile_search_launch(ct_ctx* ctx, const ct_search_params* prm, const ct_
     const size_t pref_b = (pre ? 16 : 8) * 32 * (size_t)a.nrows;   // weights [+ in-row prefixes]
     // large spaces: grid-wide phase kernels (ct_tiled.cuh); CT_SEARCH_TILED
     // forces (1) or disables (0) the path
-    int tiled = (n > TILED_MIN_N && a.topk < 0) ? 1 : 0;
+    int tiled = (n >= TILED_MIN_N && n <= TILED_MAX_N && a.topk < 0) ? 1 : 0;
     if (const char* env = std::getenv("CT_SEARCH_TILED")) tiled = std::atoi(env) != 0 && a.topk < 0;
     if (tiled) return launch_tiled(ctx, a, n_reps);
     if (head_b > budget) {

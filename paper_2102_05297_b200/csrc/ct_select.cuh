@@ -128,8 +128,8 @@ __device__ __noinline__ int64_t sequential_select(const double* w, int64_t n, do
 // C in [2^52, 2^53), and for w >= 0 with c + w still below 2^(E+1),
 // fl(c + w) = g (C + n), n = round-to-nearest-even(w / g) -- w / g is an
 // exact power-of-two scaling, and n does not depend on C unless w / g is a
-// tie (fraction exactly 1/2, parity of C decides).  So a block of 128
-// weights (4 per lane) is one exact int64 warp scan of the n's; the first
+// tie (fraction exactly 1/2, parity of C decides).  So a block of 256
+// weights (8 per lane) is one exact int64 warp scan of the n's; the first
 // element whose sum would leave the binade (C + n >= 2^53), or is a tie, or
 // (c = 0) starts the sum, is added by the hardware's own fl add instead,
 // and the scan resumes after it in the new binade.  Every c_k is therefore
@@ -145,38 +145,39 @@ __device__ __forceinline__ double pow2d(int e) {          // 2^e, e in [-1022, 1
 
 __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t k0, double& c,
                                             double r, int lane) {
+    constexpr int EPL = 8, BLK = 32 * EPL;   // elements per lane, per block
     const int64_t TWO53 = 1ll << 53;
-    // this lane's four weights of a block: elements base + 4 lane + j; the
+    // this lane's EPL weights of a block: elements base + EPL lane + j; the
     // next block's are fetched while this one is scanned (the chain is then
     // bound by the scan, not by a memory round trip per block)
     auto fetch = [&](int64_t base, double* x) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t e = base + 4 * lane + j;
+        for (int j = 0; j < EPL; ++j) {
+            const int64_t e = base + EPL * lane + j;
             x[j] = (e >= k0 && e < n) ? w[e] : 0.0;
         }
     };
-    double xn[4];
-    fetch(k0 & ~(int64_t)127, xn);
-    for (int64_t base = k0 & ~(int64_t)127; base < n; base += 128) {
-        double x[4];
+    double xn[EPL];
+    fetch(k0 & ~(int64_t)(BLK - 1), xn);
+    for (int64_t base = k0 & ~(int64_t)(BLK - 1); base < n; base += BLK) {
+        double x[EPL];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = xn[j];
-        fetch(base + 128, xn);
+        for (int j = 0; j < EPL; ++j) x[j] = xn[j];
+        fetch(base + BLK, xn);
         int64_t from = max(k0, base);       // first element of the block still to add
-        while (from < base + 128 && from < n) {
+        while (from < base + BLK && from < n) {
             // binade state of c; c == 0 (or subnormal): every element is a
             // scalar step until the sum is normal
             const bool lin = c >= 2.2250738585072014e-308;
             const int E = lin ? (int)((dbits(c) >> 52) & 0x7ff) - 1023 : 0;
             const int64_t C = lin ? (int64_t)((dbits(c) & ((1ull << 52) - 1)) | (1ull << 52)) : 0;
             const double to_grid = lin ? pow2d(52 - E) : 0.0, from_grid = lin ? pow2d(E - 52) : 0.0;
-            int64_t s_in[4];
-            bool st[4];
+            int64_t s_in[EPL];
+            bool st[EPL];
             int64_t run = 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int64_t e = base + 4 * lane + j;
+            for (int j = 0; j < EPL; ++j) {
+                const int64_t e = base + EPL * lane + j;
                 int64_t nj = 0;
                 bool sj = false;
                 if (e >= from && e < n) {
@@ -206,9 +207,9 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             }
             const int64_t before = incl - run;
             // this lane's first stopping element and first element past r
-            int jstop = 4, jhit = 4;
+            int jstop = EPL, jhit = EPL;
 #pragma unroll
-            for (int j = 3; j >= 0; --j) {
+            for (int j = EPL - 1; j >= 0; --j) {
                 const int64_t Ck = C + before + s_in[j];
                 const bool leave = lin && Ck >= TWO53;
                 if (st[j] || leave) jstop = j;
@@ -216,12 +217,12 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             }
             // elements are lane-major, so the first flagged lane holds the
             // first flagged element
-            const unsigned bs = __ballot_sync(FULL, jstop < 4);
-            const unsigned bh = __ballot_sync(FULL, jhit < 4);
+            const unsigned bs = __ballot_sync(FULL, jstop < EPL);
+            const unsigned bh = __ballot_sync(FULL, jhit < EPL);
             const int64_t big = 0x7fffffffffffffffll;
             int64_t pstop = big, phit = big;
-            if (bs) { const int L = __ffs(bs) - 1; pstop = base + 4 * L + __shfl_sync(FULL, jstop, L); }
-            if (bh) { const int L = __ffs(bh) - 1; phit = base + 4 * L + __shfl_sync(FULL, jhit, L); }
+            if (bs) { const int L = __ffs(bs) - 1; pstop = base + EPL * L + __shfl_sync(FULL, jstop, L); }
+            if (bh) { const int L = __ffs(bh) - 1; phit = base + EPL * L + __shfl_sync(FULL, jhit, L); }
             if (phit < pstop) return phit;          // c_k > r inside the binade
             if (pstop == big) {                     // the rest of the block stays in the binade
                 if (lin) c = (double)(C + __shfl_sync(FULL, (long long)incl, 31)) * from_grid;
@@ -229,10 +230,10 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             }
             // elements before pstop are final: c = g (C + their increments)
             if (lin) {
-                const int owner = (int)((pstop - base) >> 2), jj = (int)((pstop - base) & 3);
+                const int owner = (int)((pstop - base) / EPL), jj = (int)((pstop - base) % EPL);
                 int64_t pre = before;
 #pragma unroll
-                for (int j = 0; j < 3; ++j)
+                for (int j = 0; j < EPL - 1; ++j)
                     if (j < jj) pre = before + s_in[j];
                 pre = __shfl_sync(FULL, (long long)pre, owner);
                 c = (double)(C + pre) * from_grid;
