@@ -228,6 +228,7 @@ class NBodyBenchmark(Benchmark):
         return {"pm": pm}
 
     def setup(self, tuner):
+        self.SMS = tuner.sm_count          # the device's SMs (148 on B200) for split()
         pm = self.host_inputs()["pm"]
         soa = np.ascontiguousarray(pm.T)
         out = {"pm": tuner.upload(pm)}
@@ -243,7 +244,7 @@ class NBodyBenchmark(Benchmark):
     # the kernel's launch bounds cap it at 64 registers for 1024 resident
     # threads per SM (32 warps: 8 per scheduler for the MUFU/FMA latencies)
     SM_THREADS = 1024
-    SMS = 148
+    SMS = 148                         # replaced by the device's count in setup()
     MAX_JB = 16
 
     def split(self, v):
