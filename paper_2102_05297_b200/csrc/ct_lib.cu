@@ -1536,8 +1536,9 @@ int ct_report(ct_ctx* ctx, double overhead, int32_t time_reps, int32_t* n_steps,
     double* d_tcq = d_tcs + AGG_GRID;
     AggMeta* d_meta = reinterpret_cast<AggMeta*>(d_tcq + AGG_GRID);
     CT_CUDA(ctx->agg_sampled.ensure((size_t)TR * AGG_GRID));
-    // the time-grid sums past the grid's length are copied but never written
-    CT_CUDA(cudaMemsetAsync(d_tcs, 0, 8 * 2 * (size_t)AGG_GRID, s));
+    // the column sums past the longest trajectory and the time-grid sums past
+    // the grid's length are copied but never written (one contiguous block)
+    CT_CUDA(cudaMemsetAsync(d_sum, 0, 8 * (2 * (size_t)W + 2 * (size_t)AGG_GRID), s));
     k_agg_rows<<<(int)std::min<int64_t>((R + 7) / 8, 8 * (int64_t)ctx->sm_count), 256, 0, s>>>(
         ctx->step_index.p, ctx->step_profiled.p, ctx->n_steps.p, (int32_t)R, W, ctx->runtime.p,
         overhead, ctx->agg_bsf.p, ctx->agg_times.p, d_total, d_first);

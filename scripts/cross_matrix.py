@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 FAMILIES = {
     "gemm": ["gemm", "gemm-128", "gemm-16x4096", "gemm-4096x16"],
-    "nbody": ["nbody", "nbody-131072"],
+    "nbody": ["nbody", "nbody-32768"],
     "conv": ["conv", "conv-8192"],
 }
 

@@ -53,6 +53,17 @@ def one(name, label, reps):
             src.measure(best, profiled=True)
         out["profiled_step_s"] = (time.perf_counter() - t0) / reps
         out["overhead"] = out["profiled_step_s"] / out["timed_step_s"]
+        # a live step of a search also compiles the configuration (NVRTC +
+        # module load; every search starts with no variant loaded)
+        cs = []
+        for _ in range(reps):
+            src.reset_variants()
+            t0 = time.perf_counter()
+            src.variant(best)
+            cs.append(time.perf_counter() - t0)
+        out["compile_s"] = float(np.median(cs))
+        out["overhead_with_compile"] = ((out["compile_s"] + out["profiled_step_s"])
+                                        / (out["compile_s"] + out["timed_step_s"]))
         out["profiled_phases_us_per_call"] = {k: round(v / reps, 1) for k, v in
                                               t.profile_timing(reset=True).items()}
     else:

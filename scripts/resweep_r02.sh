@@ -18,5 +18,6 @@ for x in ${@:-coulomb transpose nbody gemm conv nbody-131072 gemm-128 gemm-16x40
     gemm-4096x16) run $x gemm m=4096,n=16,k=4096 ;;
     conv-8192) run $x conv width=8192,height=8192 ;;
     nbody-131072) run $x nbody bodies=131072 ;;
+    nbody-32768) run $x nbody bodies=32768 ;;
   esac
 done
