@@ -353,7 +353,7 @@ def run_ours(args):
     value = world * configs_per_step * args.steps / t_total
     per_launch = t_total / args.steps
     hbm, peak_kind = _peaks()
-    traffic, traffic_src, prof = _traffic()
+    traffic, traffic_src, kprof = _traffic()
     achieved_gbs = bytes_per_step / per_launch / 1e9
     print(f"[bench] rank {rank}: {configs_per_step} configs/step, {per_launch * 1e3:.3f} ms/step, "
           f"{value:.4g} configs/s, {achieved_gbs:.1f} GB/s algorithmic, "
@@ -459,9 +459,9 @@ def run_ours(args):
                      "note": "8*C_used+16 B per scored config (BASELINE.md); the 271 KB table "
                              "is L2-resident across repetitions, so HBM does not bind here: "
                              "the kernel is FP64-issue bound (fp64_pipe)",
-                     "fp64_pipe": {"active_frac": prof.get("fp64_pipe_active"),
-                                   "issue_active_frac": prof.get("issue_active"),
-                                   "source": prof.get("fp64_source")}},
+                     "fp64_pipe": {"active_frac": kprof.get("fp64_pipe_active"),
+                                   "issue_active_frac": kprof.get("issue_active"),
+                                   "source": kprof.get("fp64_source")}},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
         "gpu_launches": args.steps,

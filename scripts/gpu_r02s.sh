@@ -16,4 +16,10 @@ timeout 1500 python scripts/search_sweep.py --nt auto --spaces b200:coulomb,b200
 timeout 1500 python scripts/search_sweep.py --nt auto --spaces stress:1048576,stress:4194304 --reps 444 --outer 10 --runs 2 >> gpurun_out/${TAG}_search_sweep.jsonl 2>> gpurun_out/${TAG}_search_sweep.err
 CT_BENCH_SHARED_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 bench.py --gpus 2 --steps 5 --warmup 3 > gpurun_out/${TAG}_bench_2rank_shared.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_bench_2rank_shared.log
 timeout 1500 python scripts/cross_matrix.py --out gpurun_out/${TAG}_cross_input.json > gpurun_out/${TAG}_cross.log 2>&1
+# ncu reports are summarised on the box (gpurun_out must stay under 64 MiB)
+python scripts/ncu_summary.py --launches gpurun_out/${TAG}_launches.csv --full gpurun_out/${TAG}_search_full.ncu-rep --title "${TAG}: k_profile_search, bench workload" --out gpurun_out/${TAG}_search.md > /dev/null 2>&1
+python scripts/ncu_summary.py --full gpurun_out/${TAG}_tiled_score.ncu-rep --title "${TAG}: k_tiled_score, stress 1M, R=444" --out gpurun_out/${TAG}_tiled_score.md > /dev/null 2>&1
+python scripts/ncu_summary.py --full gpurun_out/${TAG}_tiled_weights.ncu-rep --title "${TAG}: k_tiled_weights, stress 1M, R=444" --out gpurun_out/${TAG}_tiled_weights.md > /dev/null 2>&1
+rm -f gpurun_out/${TAG}_tiled_score.ncu-rep gpurun_out/${TAG}_tiled_weights.ncu-rep
+du -sh gpurun_out
 for f in gpurun_out/${TAG}_*.log gpurun_out/${TAG}_*.jsonl; do echo "== $f"; tail -n 6 "$f" | cut -c1-400; done
