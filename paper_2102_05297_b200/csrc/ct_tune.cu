@@ -325,10 +325,12 @@ int host_config_cached(ct_tuner* t, const char* const* metrics, int32_t n, HostC
 // counter-data image no longer initialises against it.  A change of (metric
 // set, ranges per pass) therefore re-creates the object.
 int rp_shape(ct_tuner* t, HostConfig* hc, int32_t ranges) {
-    if (t->rp_config && (t->rp_config != hc || t->rp_ranges != ranges)) {
-        CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
-        dp.pRangeProfilerObject = t->rp;
-        TU_CUPTI(cuptiRangeProfilerDisable(&dp));
+    if (!t->rp || (t->rp_config && (t->rp_config != hc || t->rp_ranges != ranges))) {
+        if (t->rp) {
+            CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
+            dp.pRangeProfilerObject = t->rp;
+            TU_CUPTI(cuptiRangeProfilerDisable(&dp));
+        }
         CUpti_RangeProfiler_Enable_Params ep = {CUpti_RangeProfiler_Enable_Params_STRUCT_SIZE};
         ep.ctx = t->ctx;
         TU_CUPTI(cuptiRangeProfilerEnable(&ep));
@@ -493,6 +495,18 @@ int ct_tuner_unload(ct_tuner* t, int32_t variant) {
     int rc = activate(t); if (rc) return rc;
     Variant* v = nullptr;
     rc = get_variant(t, variant, &v); if (rc) return rc;
+    // the range profiler keeps per-module state for the kernels it has
+    // instrumented (the SASS-patched instruction-class metrics): unloading
+    // a module under a live profiler object crashed a later collection, so
+    // the object is released first and re-created by the next collection
+    if (t->rp) {
+        CUpti_RangeProfiler_Disable_Params dp = {CUpti_RangeProfiler_Disable_Params_STRUCT_SIZE};
+        dp.pRangeProfilerObject = t->rp;
+        TU_CUPTI(cuptiRangeProfilerDisable(&dp));
+        t->rp = nullptr;
+        t->rp_config = nullptr;
+        for (auto& kv : t->configs) kv.second->counter_data.clear();
+    }
     TU_CU(D.cuModuleUnload(v->mod));
     v->mod = nullptr;
     v->fn = nullptr;
