@@ -114,6 +114,8 @@ def main():
     ap.add_argument("--overhead", type=float, default=3.0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--mode", default="full", choices=("full", "group1"))
+    ap.add_argument("--measured-overhead", action="store_true",
+                    help="replay with the dataset's profiling_overhead.json (scripts/profile_cost.py)")
     a = ap.parse_args()
     from paper_2102_05297_b200 import formats, well_performing_set
     results = {}
@@ -124,6 +126,11 @@ def main():
              "best_us": float(ds.best_runtime),
              "well_performing": len(well_performing_set(ds, 1.1))}
         overhead = a.overhead
+        ovf = os.path.join(d, "profiling_overhead.json")
+        if a.measured_overhead and os.path.exists(ovf):
+            with open(ovf) as fh:
+                overhead = float(json.load(fh)["profiling_overhead"])
+            r["profiling_overhead_file"] = overhead
         if a.live:
             r["live"] = live(name, ds, a.live, a.seed, a.mode)
             overhead = r["live"]["profiled_step_s"] / max(r["live"]["timed_step_s"], 1e-9)
