@@ -1,7 +1,7 @@
 """Cross-input model reuse (BASELINE config 4),
 recorded with the reference itself (build container only).
 
-Datasets (B200 sweeps, scripts/sweep_cross.sh + scripts/live_sweep.py):
+Datasets (B200 sweeps, scripts/resweep_r02.sh + scripts/live_sweep.py):
   GEMM   datasets/gemm-b200 (2048^3), gemm-128-b200, gemm-16x4096-b200,
          gemm-4096x16-b200 (configurations that do not tile an input are
          not in its space)
