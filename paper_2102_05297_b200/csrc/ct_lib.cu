@@ -805,13 +805,12 @@ int launch_tiled(ct_ctx* ctx, SearchArgs& a, int n_reps) {
 }
 
 // spaces in [TILED_MIN_N, TILED_MAX_N] take the tiled path by default
-// (measured, profiles/r02/r02l_n_sweep.jsonl): from ~10^5 configurations the
-// grid-wide phases beat one CTA per repetition (GEMM-full 205k: 142 vs
-// 176 ms, 1M: 113 vs 123 ms); at 4M the rare re-decided draws, which stall
-// every repetition at the iteration barrier of the tiled path but only
-// their own CTA in the persistent kernel, tip it back (692 vs 555 ms)
+// (measured, profiles/r02/r02z_large_space_sweep.jsonl): from ~10^5
+// configurations the grid-wide phases beat one CTA per repetition
+// (GEMM-full 205k R=1000: 142 vs 176 ms; 1M R=444: 97 vs 121 ms; 4M: 452 vs
+// 498 ms); above 2^22 nothing was measured
 constexpr int64_t TILED_MIN_N = 131072;
-constexpr int64_t TILED_MAX_N = 1ll << 21;
+constexpr int64_t TILED_MAX_N = 1ll << 22;
 
 template <int PW>
 int launch_profile_ws(ct_ctx* ctx, SearchArgs& a, bool in_smem, size_t smem, int n_reps) {

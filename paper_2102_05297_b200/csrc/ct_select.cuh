@@ -143,9 +143,34 @@ __device__ __forceinline__ double pow2d(int e) {          // 2^e, e in [-1022, 1
     return bitsd((uint64_t)(1023 + e) << 52);
 }
 
+constexpr int SEQ_EPL = 16, SEQ_BLK = 32 * SEQ_EPL;  // elements per lane, per block
+constexpr int SEQ_CK = 8;                          // checkpoints per lane (256 in all)
+
+// increment of one element in the binade grid (see above); stop = the
+// element must take the hardware's fl add (a tie, alone past the binade, or
+// the first nonzero while c = 0)
+__device__ __forceinline__ int64_t seq_inc(double x, bool lin, double to_grid, bool& stop) {
+    if (!lin) { stop = x != 0.0; return 0; }
+    const double t = x * to_grid;                                // exact
+    if (t >= 9007199254740992.0) { stop = true; return 0; }
+    const double m = floor(t);
+    const double f = t - m;                                      // exact
+    stop = (f == 0.5);
+    return (int64_t)m + (f > 0.5 ? 1 : 0);
+}
+
+// ck / per: with ck != nullptr the running value at the start of every
+// per-th block is kept (lane L, slot s: block (32 s + L) per).
+//
+// A block's common path is one increment per element, one exact int64 warp
+// scan of the lane totals and one ballot: an event -- a stop, leaving the
+// binade, passing r -- can only lie in the first lane whose running total
+// shows one (the increments are >= 0), and only that lane then walks its
+// elements to find it.
 __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t k0, double& c,
-                                            double r, int lane) {
-    constexpr int EPL = 8, BLK = 32 * EPL;   // elements per lane, per block
+                                            double r, int lane, double* ck = nullptr,
+                                            int64_t per = 1) {
+    constexpr int EPL = SEQ_EPL, BLK = SEQ_BLK;
     const int64_t TWO53 = 1ll << 53;
     // this lane's EPL weights of a block: elements base + EPL lane + j; the
     // next block's are fetched while this one is scanned (the chain is then
@@ -164,40 +189,41 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
 #pragma unroll
         for (int j = 0; j < EPL; ++j) x[j] = xn[j];
         fetch(base + BLK, xn);
+        {
+            // one warp streams the weights: without deeper memory-level
+            // parallelism it waits a DRAM round trip per block, so each lane
+            // also pulls its 128-byte segment of the block 16 ahead into L2
+            const int64_t e = base + 16 * (int64_t)BLK + EPL * lane;
+            if (e < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + e));
+        }
+        if (ck) {
+            const int64_t b = base / BLK;
+            if (b % per == 0) {
+                const int64_t slot = b / per;
+#pragma unroll
+                for (int q = 0; q < SEQ_CK; ++q)
+                    if (slot == 32 * q + lane) ck[q] = c;    // c is warp-uniform here
+            }
+        }
         int64_t from = max(k0, base);       // first element of the block still to add
+        const int64_t mine0 = base + EPL * lane;
         while (from < base + BLK && from < n) {
-            // binade state of c; c == 0 (or subnormal): every element is a
-            // scalar step until the sum is normal
+            // binade state of c; c == 0 (or subnormal): every nonzero element
+            // is a scalar step until the sum is normal
             const bool lin = c >= 2.2250738585072014e-308;
             const int E = lin ? (int)((dbits(c) >> 52) & 0x7ff) - 1023 : 0;
             const int64_t C = lin ? (int64_t)((dbits(c) & ((1ull << 52) - 1)) | (1ull << 52)) : 0;
             const double to_grid = lin ? pow2d(52 - E) : 0.0, from_grid = lin ? pow2d(E - 52) : 0.0;
-            int64_t s_in[EPL];
-            bool st[EPL];
             int64_t run = 0;
+            bool st_any = false;
 #pragma unroll
             for (int j = 0; j < EPL; ++j) {
-                const int64_t e = base + EPL * lane + j;
-                int64_t nj = 0;
+                const int64_t e = mine0 + j;
                 bool sj = false;
-                if (e >= from && e < n) {
-                    if (!lin) {
-                        sj = x[j] != 0.0;
-                    } else {
-                        const double t = x[j] * to_grid;            // exact
-                        if (t >= 9007199254740992.0) {
-                            sj = true;                              // alone past the binade
-                        } else {
-                            const double m = floor(t);
-                            const double f = t - m;                 // exact
-                            nj = (int64_t)m + (f > 0.5 ? 1 : 0);
-                            sj = (f == 0.5);                        // tie: parity of C decides
-                        }
-                    }
-                }
-                run += nj;
-                s_in[j] = run;
-                st[j] = sj;
+                const int64_t nj = seq_inc(x[j], lin, to_grid, sj);
+                const bool live = e >= from && e < n;
+                run += live ? nj : 0;
+                st_any |= live && sj;
             }
             int64_t incl = run;                     // exact int64 warp scan
 #pragma unroll
@@ -205,42 +231,45 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
                 const int64_t v = __shfl_up_sync(FULL, (long long)incl, d);
                 if (lane >= d) incl += v;
             }
-            const int64_t before = incl - run;
-            // this lane's first stopping element and first element past r
-            int jstop = EPL, jhit = EPL;
-#pragma unroll
-            for (int j = EPL - 1; j >= 0; --j) {
-                const int64_t Ck = C + before + s_in[j];
-                const bool leave = lin && Ck >= TWO53;
-                if (st[j] || leave) jstop = j;
-                if (lin && !st[j] && !leave && r >= 0.0 && (double)Ck * from_grid > r) jhit = j;
-            }
-            // elements are lane-major, so the first flagged lane holds the
-            // first flagged element
-            const unsigned bs = __ballot_sync(FULL, jstop < EPL);
-            const unsigned bh = __ballot_sync(FULL, jhit < EPL);
-            const int64_t big = 0x7fffffffffffffffll;
-            int64_t pstop = big, phit = big;
-            if (bs) { const int L = __ffs(bs) - 1; pstop = base + EPL * L + __shfl_sync(FULL, jstop, L); }
-            if (bh) { const int L = __ffs(bh) - 1; phit = base + EPL * L + __shfl_sync(FULL, jhit, L); }
-            if (phit < pstop) return phit;          // c_k > r inside the binade
-            if (pstop == big) {                     // the rest of the block stays in the binade
+            const bool leave = lin && C + incl >= TWO53;
+            const bool hit = lin && r >= 0.0 && (double)(C + incl) * from_grid > r;
+            const unsigned bal = __ballot_sync(FULL, st_any || leave || hit);
+            if (!bal) {                             // the rest of the block stays in the binade
                 if (lin) c = (double)(C + __shfl_sync(FULL, (long long)incl, 31)) * from_grid;
                 break;
             }
-            // elements before pstop are final: c = g (C + their increments)
-            if (lin) {
-                const int owner = (int)((pstop - base) / EPL), jj = (int)((pstop - base) % EPL);
-                int64_t pre = before;
+            // the first flagged lane walks its elements to the event
+            const int L = __ffs(bal) - 1;
+            int kind = 0, jev = EPL;                // kind: 1 stop, 2 hit
+            int64_t pre = 0;                        // increments before the event (in-lane)
+            if (lane == L) {
+                int64_t acc = incl - run;           // exclusive prefix of this lane
 #pragma unroll
-                for (int j = 0; j < EPL - 1; ++j)
-                    if (j < jj) pre = before + s_in[j];
-                pre = __shfl_sync(FULL, (long long)pre, owner);
-                c = (double)(C + pre) * from_grid;
+                for (int j = 0; j < EPL; ++j) {
+                    const int64_t e = mine0 + j;
+                    if (kind == 0 && e >= from && e < n) {
+                        bool sj = false;
+                        const int64_t nj = seq_inc(x[j], lin, to_grid, sj);
+                        if (sj || (lin && C + acc + nj >= TWO53)) {
+                            kind = 1; jev = j; pre = acc;
+                        } else if (lin && r >= 0.0 && (double)(C + acc + nj) * from_grid > r) {
+                            kind = 2; jev = j;
+                        } else {
+                            acc += nj;
+                        }
+                    }
+                }
             }
-            c = add(c, w[pstop]);                   // the hardware's fl add at the stop
-            if (r >= 0.0 && c > r) return pstop;
-            from = pstop + 1;
+            kind = __shfl_sync(FULL, kind, L);
+            jev = __shfl_sync(FULL, jev, L);
+            pre = __shfl_sync(FULL, (long long)pre, L);
+            const int64_t p = base + EPL * L + jev;
+            if (kind == 2) return p;                // c_p > r inside the binade
+            // kind == 1: the elements before p are final, then the hardware add
+            if (lin) c = (double)(C + pre) * from_grid;
+            c = add(c, w[p]);
+            if (r >= 0.0 && c > r) return p;
+            from = p + 1;
         }
     }
     return n;
@@ -249,11 +278,30 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
 // np.cumsum + searchsorted(side='right') by one warp: the total, r = u c_N,
 // then the first k with c_k > r (n when r reaches the total).
 __device__ __noinline__ int64_t sequential_select_warp(const double* w, int64_t n, double u, int lane) {
+    // pass 1: the total, keeping the exact running value at <= 256 block
+    // boundaries; pass 2 starts from the last boundary at or below r
+    const int64_t nblocks = (n + SEQ_BLK - 1) / SEQ_BLK;
+    const int64_t per = max((int64_t)1, (nblocks + 32 * SEQ_CK - 1) / (32 * SEQ_CK));
+    double ck[SEQ_CK];
+#pragma unroll
+    for (int q = 0; q < SEQ_CK; ++q) ck[q] = 0.0;
     double c = 0.0;
-    seq_scan(w, n, 0, c, -1.0, lane);
+    seq_scan(w, n, 0, c, -1.0, lane, ck, per);
     const double r = mul(u, c);
-    double c2 = 0.0;
-    return seq_scan(w, n, 0, c2, r, lane);
+    const int64_t nslots = (nblocks + per - 1) / per;
+    int64_t best = 0;
+    double from = 0.0;
+#pragma unroll
+    for (int q = 0; q < SEQ_CK; ++q) {
+        const int64_t slot = 32 * q + lane;
+        if (slot < nslots && ck[q] <= r && slot > best) { best = slot; from = ck[q]; }
+    }
+    int64_t slot = best;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) slot = max(slot, (int64_t)__shfl_xor_sync(FULL, (long long)slot, m));
+    double c2 = __shfl_sync(FULL, from, (int)(slot & 31));   // the owner's best is this slot
+    if (slot == 0) c2 = 0.0;
+    return seq_scan(w, n, slot * per * SEQ_BLK, c2, r, lane);
 }
 
 }  // namespace ct
