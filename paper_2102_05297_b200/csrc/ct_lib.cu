@@ -805,10 +805,10 @@ int launch_tiled(ct_ctx* ctx, SearchArgs& a, int n_reps) {
 }
 
 // spaces in [TILED_MIN_N, TILED_MAX_N] take the tiled path by default
-// (measured, profiles/r02/r02z_large_space_sweep.jsonl): from ~10^5
+// (measured, profiles/r02/r02ab_large_space_sweep.jsonl): from ~10^5
 // configurations the grid-wide phases beat one CTA per repetition
-// (GEMM-full 205k R=1000: 142 vs 176 ms; 1M R=444: 97 vs 121 ms; 4M: 452 vs
-// 498 ms); above 2^22 nothing was measured
+// (GEMM-full 205k R=444: 15.1 vs 19.2 ms; 1M: 87 vs 118 ms; 4M: 385 vs
+// 493 ms); above 2^22 nothing was measured
 constexpr int64_t TILED_MIN_N = 131072;
 constexpr int64_t TILED_MAX_N = 1ll << 22;
 

@@ -150,13 +150,18 @@ constexpr int SEQ_CK = 8;                          // checkpoints per lane (256 
 // element must take the hardware's fl add (a tie, alone past the binade, or
 // the first nonzero while c = 0)
 __device__ __forceinline__ int64_t seq_inc(double x, bool lin, double to_grid, bool& stop) {
-    if (!lin) { stop = x != 0.0; return 0; }
+    // n = round-to-nearest-even(x / g) without a float-to-integer
+    // conversion (slow on the FP64 units): t + 2^52 rounds t to an integer
+    // (RNE) for 0 <= t < 2^52 and holds it in its low mantissa bits.
+    // Branch-free (lin is warp-uniform, but the selects keep the unrolled
+    // block loop straight-line).
     const double t = x * to_grid;                                // exact
-    if (t >= 9007199254740992.0) { stop = true; return 0; }
-    const double m = floor(t);
-    const double f = t - m;                                      // exact
-    stop = (f == 0.5);
-    return (int64_t)m + (f > 0.5 ? 1 : 0);
+    const double big = 4503599627370496.0;                       // 2^52
+    const double s = t + big;
+    const double rne = s - big;                                  // exact
+    const double d = t - rne;                                    // exact, |d| <= 1/2
+    stop = lin ? ((t >= big) | (fabs(d) == 0.5)) : (x != 0.0);   // too large, a tie; or c = 0
+    return lin ? (int64_t)(dbits(s) & ((1ull << 52) - 1)) : 0;
 }
 
 // ck / per: with ck != nullptr the running value at the start of every
@@ -172,58 +177,62 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
                                             int64_t per = 1) {
     constexpr int EPL = SEQ_EPL, BLK = SEQ_BLK;
     const int64_t TWO53 = 1ll << 53;
-    // this lane's EPL weights of a block: elements base + EPL lane + j; the
-    // next block's are fetched while this one is scanned (the chain is then
-    // bound by the scan, not by a memory round trip per block)
+    // this lane's EPL weights of a block: elements base + EPL lane + j (0.0
+    // outside [k0, n): adding +0.0 is exact and never an event); the next
+    // block's are fetched while this one is scanned
     auto fetch = [&](int64_t base, double* x) {
+        if (base >= k0 && base + BLK <= n) {            // a whole block: 8 x 16-byte loads
+            const double2* q = reinterpret_cast<const double2*>(w + base + EPL * lane);
 #pragma unroll
-        for (int j = 0; j < EPL; ++j) {
-            const int64_t e = base + EPL * lane + j;
-            x[j] = (e >= k0 && e < n) ? w[e] : 0.0;
+            for (int j = 0; j < EPL / 2; ++j) { const double2 v = q[j]; x[2 * j] = v.x; x[2 * j + 1] = v.y; }
+        } else {
+#pragma unroll
+            for (int j = 0; j < EPL; ++j) {
+                const int64_t e = base + EPL * lane + j;
+                x[j] = (e >= k0 && e < n) ? w[e] : 0.0;
+            }
         }
     };
     double xn[EPL];
-    fetch(k0 & ~(int64_t)(BLK - 1), xn);
-    for (int64_t base = k0 & ~(int64_t)(BLK - 1); base < n; base += BLK) {
+    const int64_t first = k0 & ~(int64_t)(BLK - 1);
+    fetch(first, xn);
+    int64_t blk = first / BLK, next_ck = 0, slot = 0;   // checkpoint bookkeeping, no division
+    for (int64_t base = first; base < n; base += BLK, ++blk) {
         double x[EPL];
 #pragma unroll
         for (int j = 0; j < EPL; ++j) x[j] = xn[j];
         fetch(base + BLK, xn);
         {
-            // one warp streams the weights: without deeper memory-level
-            // parallelism it waits a DRAM round trip per block, so each lane
-            // also pulls its 128-byte segment of the block 16 ahead into L2
+            // one warp streams the weights: each lane also pulls its 128-byte
+            // segment of the block 16 ahead into L2
             const int64_t e = base + 16 * (int64_t)BLK + EPL * lane;
             if (e < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + e));
         }
-        if (ck) {
-            const int64_t b = base / BLK;
-            if (b % per == 0) {
-                const int64_t slot = b / per;
+        if (ck && blk == next_ck) {
 #pragma unroll
-                for (int q = 0; q < SEQ_CK; ++q)
-                    if (slot == 32 * q + lane) ck[q] = c;    // c is warp-uniform here
-            }
+            for (int q = 0; q < SEQ_CK; ++q)
+                if (slot == 32 * q + lane) ck[q] = c;        // c is warp-uniform here
+            ++slot;
+            next_ck += per;
         }
-        int64_t from = max(k0, base);       // first element of the block still to add
         const int64_t mine0 = base + EPL * lane;
-        while (from < base + BLK && from < n) {
+        for (;;) {
             // binade state of c; c == 0 (or subnormal): every nonzero element
             // is a scalar step until the sum is normal
             const bool lin = c >= 2.2250738585072014e-308;
             const int E = lin ? (int)((dbits(c) >> 52) & 0x7ff) - 1023 : 0;
             const int64_t C = lin ? (int64_t)((dbits(c) & ((1ull << 52) - 1)) | (1ull << 52)) : 0;
             const double to_grid = lin ? pow2d(52 - E) : 0.0, from_grid = lin ? pow2d(E - 52) : 0.0;
+            // c_k > r  <=>  C_k > floor(r / g) (C_k integer); r / g exact
+            const double rg = (lin && r >= 0.0) ? r * to_grid : 1.0e300;
+            const int64_t Rint = (rg < 9007199254740992.0) ? (int64_t)floor(rg) : (int64_t)1 << 62;
             int64_t run = 0;
             bool st_any = false;
 #pragma unroll
             for (int j = 0; j < EPL; ++j) {
-                const int64_t e = mine0 + j;
                 bool sj = false;
-                const int64_t nj = seq_inc(x[j], lin, to_grid, sj);
-                const bool live = e >= from && e < n;
-                run += live ? nj : 0;
-                st_any |= live && sj;
+                run += seq_inc(x[j], lin, to_grid, sj);
+                st_any |= sj;
             }
             int64_t incl = run;                     // exact int64 warp scan
 #pragma unroll
@@ -232,7 +241,7 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
                 if (lane >= d) incl += v;
             }
             const bool leave = lin && C + incl >= TWO53;
-            const bool hit = lin && r >= 0.0 && (double)(C + incl) * from_grid > r;
+            const bool hit = lin && C + incl > Rint;
             const unsigned bal = __ballot_sync(FULL, st_any || leave || hit);
             if (!bal) {                             // the rest of the block stays in the binade
                 if (lin) c = (double)(C + __shfl_sync(FULL, (long long)incl, 31)) * from_grid;
@@ -241,18 +250,17 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             // the first flagged lane walks its elements to the event
             const int L = __ffs(bal) - 1;
             int kind = 0, jev = EPL;                // kind: 1 stop, 2 hit
-            int64_t pre = 0;                        // increments before the event (in-lane)
+            int64_t pre = 0;                        // increments before the event
             if (lane == L) {
                 int64_t acc = incl - run;           // exclusive prefix of this lane
 #pragma unroll
                 for (int j = 0; j < EPL; ++j) {
-                    const int64_t e = mine0 + j;
-                    if (kind == 0 && e >= from && e < n) {
+                    if (kind == 0) {
                         bool sj = false;
                         const int64_t nj = seq_inc(x[j], lin, to_grid, sj);
                         if (sj || (lin && C + acc + nj >= TWO53)) {
                             kind = 1; jev = j; pre = acc;
-                        } else if (lin && r >= 0.0 && (double)(C + acc + nj) * from_grid > r) {
+                        } else if (lin && C + acc + nj > Rint) {
                             kind = 2; jev = j;
                         } else {
                             acc += nj;
@@ -269,7 +277,10 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             if (lin) c = (double)(C + pre) * from_grid;
             c = add(c, w[p]);
             if (r >= 0.0 && c > r) return p;
-            from = p + 1;
+            // the elements up to p are added: they no longer take part
+#pragma unroll
+            for (int j = 0; j < EPL; ++j)
+                if (mine0 + j <= p) x[j] = 0.0;
         }
     }
     return n;
