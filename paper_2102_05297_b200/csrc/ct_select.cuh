@@ -206,7 +206,7 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             // one warp streams the weights: each lane also pulls its 128-byte
             // segment of the block 16 ahead into L2
             const int64_t e = base + 16 * (int64_t)BLK + EPL * lane;
-            if (e < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + e));
+            if (e < n) asm volatile("prefetch.L2 [%0];" ::"l"(w + e));   // generic: w may be shared memory
         }
         if (ck && blk == next_ck) {
 #pragma unroll
