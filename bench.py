@@ -405,6 +405,46 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
+    # the BASELINE.md section 3 stress size where the table (152 MB) no
+    # longer fits the L2: the same search at N = 2^20 on the default (tiled)
+    # path, CUDA events on the context's stream, for the HBM-bound roofline
+    large = None
+    if not args.no_large_space:
+        try:
+            from paper_2102_05297_b200 import ExactModelSet, ExperimentSpec, spaces
+            lds = spaces.stress(1 << 20)
+            lspec = ExperimentSpec(dataset=lds, searcher="profile", model=ExactModelSet(lds),
+                                   repetitions=444, outer_iterations=10, seed=SEED,
+                                   stop_at_well_performing=False)
+            lparams, _ = harness.prepare_device(ctx, lspec)
+            harness.launch(ctx, lspec, lparams, 0, 444)            # warm-up
+            lt = []
+            for _ in range(3):
+                flush.add_(1.0)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                harness.launch(ctx, lspec, lparams, 0, 444)
+                e1.record(stream)
+                e1.synchronize()
+                lt.append(e0.elapsed_time(e1) / 1e3)
+            lst = ctx.fetch_stats()
+            lsec = float(np.median(lt))
+            lgbs = lst.algorithmic_bytes / lsec / 1e9
+            large = {"workload": "stress space, 1,048,576 configurations x 19 counter columns "
+                                 "(table 152 MB > L2), R = 444, i = 10, n = 5, default "
+                                 "dispatch (tiled path)",
+                     "ms_per_step": lsec * 1e3, "configs_per_s": lst.configs_scored / lsec,
+                     "roofline": {"bound": "hbm", "achieved": lgbs, "peak": hbm, "unit": "GB/s",
+                                  "frac": lgbs / hbm,
+                                  "algorithmic_bytes_per_launch": int(lst.algorithmic_bytes),
+                                  "traffic_source": "profiles/r02/r02s_tiled_score.md, "
+                                                    "r02s_tiled_weights.md (ncu, per kernel)"},
+                     "uncertified_draws": int(lst.uncertified)}
+            params, _ = harness.prepare_device(ctx, spec)         # restore the bench space
+        except Exception as exc:  # report, never hide
+            large = {"error": repr(exc)}
+
     # steps metric on the same space: profile vs random, stop at <= 1.1x best
     steps_info = {}
     try:
@@ -467,6 +507,7 @@ def run_ours(args):
         "gpu_launches": args.steps,
         "steps_metric": steps_info,
         "uncertified_draws_per_step": stats0.uncertified,
+        "large_space": large,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -480,6 +521,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-large-space", action="store_true",
+                    help="skip the 1M-configuration stress measurement")
     ap.add_argument("--kernel-only", action="store_true",
                     help="time the search kernel only (for ncu captures)")
     args = ap.parse_args()
