@@ -169,6 +169,14 @@ __global__ void __launch_bounds__(TILED_NT) k_tiled_weights(const SearchArgs a, 
     double* row_tot = t.row_tot + (size_t)b * a.nrows;
     const int r0 = tile * (TILE_CONFIGS / 32);
     const int r1 = min(a.nrows, r0 + TILE_CONFIGS / 32);
+    // the tile's 32 KB of raw scores are pulled into L2 at once (one 128-byte
+    // line per thread): the row groups below then wait an L2 round trip,
+    // not a DRAM one, and the kernel streams instead of stalling per group
+    static_assert(TILE_CONFIGS == TILED_NT * 16, "one line of 16 doubles per thread");
+    {
+        const int64_t e = (int64_t)tile * TILE_CONFIGS + 16 * threadIdx.x;
+        if (e < a.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + e));
+    }
     int bad = 0;
     if (cert) weight_pass<true, false>(a, warp, NW, smax, smin, expl, w, w, row_tot, bad, r0, r1);
     else weight_pass<false, false>(a, warp, NW, smax, smin, expl, w, w, row_tot, bad, r0, r1);
