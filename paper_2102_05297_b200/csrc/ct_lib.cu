@@ -805,10 +805,10 @@ int launch_tiled(ct_ctx* ctx, SearchArgs& a, int n_reps) {
 }
 
 // spaces in [TILED_MIN_N, TILED_MAX_N] take the tiled path by default
-// (measured, profiles/r02/r02af_large_space_sweep.jsonl): from ~10^5
+// (measured, profiles/r02/r02ah_large_space_sweep.jsonl): from ~10^5
 // configurations the grid-wide phases beat one CTA per repetition
-// (GEMM-full 205k R=444: 13.6 vs 19.3 ms; 1M: 80 vs 118 ms; 4M: 370 vs
-// 493 ms); above 2^22 nothing was measured
+// (GEMM-full 205k R=444: 13.6 vs 18.9 ms; 1M: 79 vs 119 ms; 4M: 347 vs
+// 497 ms); above 2^22 nothing was measured
 constexpr int64_t TILED_MIN_N = 131072;
 constexpr int64_t TILED_MAX_N = 1ll << 22;
 

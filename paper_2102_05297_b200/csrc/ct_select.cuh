@@ -197,6 +197,12 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
     const int64_t first = k0 & ~(int64_t)(BLK - 1);
     fetch(first, xn);
     int64_t blk = first / BLK, next_ck = 0, slot = 0;   // checkpoint bookkeeping, no division
+    // the next block's lane total and stop flag, computed while this block's
+    // scan is in flight, under this block's binade (key: E, or -9999 for
+    // c = 0); reused when the next block starts in the same binade
+    int spec_key = 0x7fffffff;
+    int64_t spec_run = 0;
+    bool spec_st = false;
     for (int64_t base = first; base < n; base += BLK, ++blk) {
         double x[EPL];
 #pragma unroll
@@ -216,6 +222,7 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             next_ck += per;
         }
         const int64_t mine0 = base + EPL * lane;
+        bool fresh = true;                  // no event yet in this block
         for (;;) {
             // binade state of c; c == 0 (or subnormal): every nonzero element
             // is a scalar step until the sum is normal
@@ -226,13 +233,30 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             // c_k > r  <=>  C_k > floor(r / g) (C_k integer); r / g exact
             const double rg = (lin && r >= 0.0) ? r * to_grid : 1.0e300;
             const int64_t Rint = (rg < 9007199254740992.0) ? (int64_t)floor(rg) : (int64_t)1 << 62;
+            const int key = lin ? E : -9999;
             int64_t run = 0;
             bool st_any = false;
+            if (fresh && key == spec_key) {
+                run = spec_run;
+                st_any = spec_st;
+            } else {
 #pragma unroll
-            for (int j = 0; j < EPL; ++j) {
-                bool sj = false;
-                run += seq_inc(x[j], lin, to_grid, sj);
-                st_any |= sj;
+                for (int j = 0; j < EPL; ++j) {
+                    bool sj = false;
+                    run += seq_inc(x[j], lin, to_grid, sj);
+                    st_any |= sj;
+                }
+            }
+            if (fresh) {                            // speculate the next block
+                spec_key = key;
+                spec_run = 0;
+                spec_st = false;
+#pragma unroll
+                for (int j = 0; j < EPL; ++j) {
+                    bool sj = false;
+                    spec_run += seq_inc(xn[j], lin, to_grid, sj);
+                    spec_st |= sj;
+                }
             }
             int64_t incl = run;                     // exact int64 warp scan
 #pragma unroll
@@ -281,6 +305,7 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
 #pragma unroll
             for (int j = 0; j < EPL; ++j)
                 if (mine0 + j <= p) x[j] = 0.0;
+            fresh = false;
         }
     }
     return n;
