@@ -92,13 +92,15 @@ def run_profile_search_distributed(source, models, *, i: int, n: int = DEFAULT_I
                                    literal_sign: bool = False,
                                    stop_indices: Optional[Set[int]] = None,
                                    score_top_k: Optional[int] = None, profile_rank: int = 0,
-                                   core_factory: Optional[Callable] = None) -> SearchTrace:
+                                   core_factory: Optional[Callable] = None,
+                                   shard_space: bool = False) -> SearchTrace:
     """run_profile_search over the default process group; every rank passes
     its own measurement source (its GPU) and gets the same trace back.
 
     ``seed`` must be regenerable (an int or SeedSequence), so that all ranks
     draw the same stream.  ``core_factory`` replaces the device searcher
-    (tests drive the protocol with a host stand-in)."""
+    (tests drive the protocol with a host stand-in).  ``shard_space`` also
+    splits every Eq. 16 pass over the ranks' GPUs (dist_space.py)."""
     import torch
     import torch.distributed as dist
     if i < 1:
@@ -112,10 +114,14 @@ def run_profile_search_distributed(source, models, *, i: int, n: int = DEFAULT_I
     space = source.space
     if core_factory is None:
         table = _as_table(models, space)
+        score_fn = None
+        if shard_space:
+            from .dist_space import score_configurations_sharded
+            score_fn = score_configurations_sharded
         core = _profile_search_batches(space, source.arch, table, len(space), i=i, n=n,
                                        seed=seed, inst_reaction=inst_reaction,
                                        literal_sign=literal_sign, stop_indices=stop_indices,
-                                       score_top_k=score_top_k)
+                                       score_top_k=score_top_k, score_fn=score_fn)
     else:
         core = core_factory(space, source.arch, i=i, n=n, seed=seed,
                             inst_reaction=inst_reaction, literal_sign=literal_sign,

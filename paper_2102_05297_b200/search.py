@@ -500,7 +500,7 @@ def _profile_search_host_driven(source, table, total, *, i, n, seed, inst_reacti
 
 
 def _profile_search_batches(space, arch, table, total, *, i, n, seed, inst_reaction,
-                            literal_sign, stop_indices, score_top_k):
+                            literal_sign, stop_indices, score_top_k, score_fn=None):
     """run_profile_search (search.py:338-399) as a generator of measurement
     batches: it yields ``(indices, profiled)`` -- the profiled configuration
     alone, then the n draws of the outer iteration together -- and is sent the
@@ -554,7 +554,7 @@ def _profile_search_batches(space, arch, table, total, *, i, n, seed, inst_react
         delta = dict(zip(cc.DELTA_KEYS, map(float, deltas)))
         if not (~explored).any():
             return finish(STATUS_EXHAUSTED)
-        scores = score_configurations(table, c_profile, delta, space, explored,
+        scores = (score_fn or score_configurations)(table, c_profile, delta, space, explored,
                                       literal_sign=literal_sign, score_top_k=score_top_k)
         scores = normalize_scores(scores)
         chosen: List[int] = []
