@@ -203,6 +203,8 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
     int spec_key = 0x7fffffff;
     int64_t spec_run = 0;
     bool spec_st = false;
+    int rint_key = 0x7fffffff;
+    int64_t Rint = (int64_t)1 << 62;
     for (int64_t base = first; base < n; base += BLK, ++blk) {
         double x[EPL];
 #pragma unroll
@@ -230,10 +232,15 @@ __device__ __forceinline__ int64_t seq_scan(const double* w, int64_t n, int64_t 
             const int E = lin ? (int)((dbits(c) >> 52) & 0x7ff) - 1023 : 0;
             const int64_t C = lin ? (int64_t)((dbits(c) & ((1ull << 52) - 1)) | (1ull << 52)) : 0;
             const double to_grid = lin ? pow2d(52 - E) : 0.0, from_grid = lin ? pow2d(E - 52) : 0.0;
-            // c_k > r  <=>  C_k > floor(r / g) (C_k integer); r / g exact
-            const double rg = (lin && r >= 0.0) ? r * to_grid : 1.0e300;
-            const int64_t Rint = (rg < 9007199254740992.0) ? (int64_t)floor(rg) : (int64_t)1 << 62;
+            // c_k > r  <=>  C_k > floor(r / g) (C_k integer); r / g exact.
+            // Recomputed only when the binade changes (the float-to-integer
+            // conversion is slow, and the binade changes ~40 times in a pass)
             const int key = lin ? E : -9999;
+            if (key != rint_key) {
+                const double rg = (lin && r >= 0.0) ? r * to_grid : 1.0e300;
+                Rint = (rg < 9007199254740992.0) ? (int64_t)floor(rg) : (int64_t)1 << 62;
+                rint_key = key;
+            }
             int64_t run = 0;
             bool st_any = false;
             if (fresh && key == spec_key) {

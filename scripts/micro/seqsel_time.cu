@@ -16,6 +16,15 @@ __global__ void k_pass(const double* w, int64_t n, int64_t* out) {   // one seq_
     int64_t a = seq_scan(w, n, 0, c, -1.0, threadIdx.x & 31);
     if (threadIdx.x == 0) { out[0] = a; out[1] = (int64_t)c; }
 }
+__global__ void k_pass_ck(const double* w, int64_t n, int64_t* out) {   // pass 1 with checkpoints
+    double ck[SEQ_CK];
+    for (int q = 0; q < SEQ_CK; ++q) ck[q] = 0.0;
+    const int64_t nblocks = (n + SEQ_BLK - 1) / SEQ_BLK;
+    const int64_t per = max((int64_t)1, (nblocks + 32 * SEQ_CK - 1) / (32 * SEQ_CK));
+    double c = 0.0;
+    int64_t a = seq_scan(w, n, 0, c, -1.0, threadIdx.x & 31, ck, per);
+    if (threadIdx.x == 0) { out[0] = a; out[1] = (int64_t)ck[1]; }
+}
 __global__ void k_seq(const double* w, int64_t n, double u, int64_t* out) {
     if (threadIdx.x == 0) out[0] = sequential_select(w, n, u);
 }
@@ -36,6 +45,8 @@ int main() {
     printf("warp select: %.3f ms -> %lld\n", ms, (long long)r1);
     cudaEventRecord(a); k_pass<<<1, 32>>>(w, n, o); cudaEventRecord(b); cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b); printf("one binade pass: %.3f ms\n", ms);
+    cudaEventRecord(a); k_pass_ck<<<1, 32>>>(w, n, o); cudaEventRecord(b); cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b); printf("one pass with checkpoints: %.3f ms\n", ms);
     cudaEventRecord(a); k_seq<<<1, 32>>>(w, n, 0.37, o); cudaEventRecord(b); cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b); cudaMemcpy(&r2, o, 8, cudaMemcpyDeviceToHost);
     printf("scalar select: %.3f ms -> %lld (%s)\n", ms, (long long)r2, r1 == r2 ? "same" : "DIFFERENT");
