@@ -13,6 +13,11 @@ For every dataset directory given (written by scripts/live_sweep.py):
      profiling inside the loop), wall-clock seconds until a configuration
      within 1.1x of the dataset's best was measured.
 
+Run the live part with CUDA_CACHE_DISABLE=1 (scripts/gpu_r02al.sh): the
+driver's compute cache otherwise serves every configuration compiled earlier
+on the box in ~9 ms instead of 50-1500 ms (scripts/debug/compile_cache.py),
+so later searches -- and whichever searcher runs second -- pay less.
+
     python scripts/live_experiment.py gpurun_out/datasets/*-b200 [--live 5] \
         [--out gpurun_out/experiments.json]
 """
